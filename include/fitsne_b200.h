@@ -1,0 +1,181 @@
+/*
+ * fitsne_b200.h -- C-ABI of the B200 (sm_100a) FIt-SNE gradient library.
+ *
+ * The reference (`fftsne`, /root/reference/pkg/src/fftsne) is a pure-Python
+ * package with no FFI of its own: its boundary for this path is the Python API
+ * of fftsne.nbody and fftsne.optimizer.  Every entry point below replaces the
+ * reference function named beside it; the Python mirror
+ * (paper_1712_09005_b200/{nbody,optimizer}.py) binds them through ctypes with
+ * the reference's names, argument meaning and exceptions, and INTEGRATION.md
+ * shows the ctypes stub a maintainer of the reference would add.
+ *
+ * Conventions
+ *   - All array arguments are DEVICE pointers (cudaMalloc / torch CUDA tensors)
+ *     unless the name ends in `_host`.  The caller owns every buffer; the
+ *     library owns only the context (scratch grids, FFT work areas, twiddles).
+ *   - Embeddings Y are row-major (N, dims) in the context dtype
+ *     (FITSNE_F32 -> float, FITSNE_F64 -> double).  The point index is the
+ *     row; dims in {1, 2}.
+ *   - Every call is stream-ordered on `stream` (a cudaStream_t; 0 = legacy
+ *     default).  The only host synchronisation is the grid-size readback in
+ *     fitsne_make_grid (the FFT length depends on the data, nbody.py:134).
+ *   - Return value: FITSNE_OK or an error code; fitsne_last_error() gives a
+ *     thread-local message.  The Python layer maps FITSNE_EINVAL/FITSNE_EOUTSIDE/
+ *     FITSNE_EZ to ValueError and FITSNE_ENONFINITE to FloatingPointError,
+ *     exactly as the reference raises (optimizer.py:242-243, 310-313;
+ *     nbody.py:127-128, 210-211).
+ */
+#ifndef FITSNE_B200_H
+#define FITSNE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define FITSNE_ABI_VERSION 1
+
+enum fitsne_status {
+  FITSNE_OK = 0,
+  FITSNE_EINVAL = 1,      /* bad argument / shape / config -> ValueError */
+  FITSNE_ENONFINITE = 2,  /* non-finite input or gradient -> FloatingPointError */
+  FITSNE_EZ = 3,          /* normalisation Z <= 0 -> ValueError (optimizer.py:242) */
+  FITSNE_ECUDA = 4,       /* CUDA runtime error */
+  FITSNE_ENOMEM = 5,      /* device allocation failed */
+  FITSNE_EOUTSIDE = 6,    /* point outside grid bounds -> ValueError (nbody.py:210) */
+  FITSNE_ETOOBIG = 7      /* grid larger than the FFT kernels support */
+};
+
+enum fitsne_dtype { FITSNE_F32 = 0, FITSNE_F64 = 1 };
+enum fitsne_kernel { FITSNE_CAUCHY = 0, FITSNE_CAUCHY_SQUARED = 1 };  /* nbody.py:38-42 */
+
+/* Interpolation grid, the device-side twin of nbody.InterpGrid (nbody.py:62-104). */
+typedef struct fitsne_grid {
+  double lo[2];
+  double hi[2];
+  double spacing[2];   /* (hi - lo) / nodes_per_dim, nbody.py:97-99 */
+  int32_t dims;
+  int32_t n_intervals;
+  int32_t points_per_interval;
+  int32_t nodes_per_dim;   /* n = n_intervals * points_per_interval */
+  int32_t fft_len;         /* L >= 2n-1, 2^a 3^b (reference: next_fast_len, nbody.py:267) */
+  int32_t status;          /* 0, or FITSNE_ENONFINITE if a coordinate was not finite */
+} fitsne_grid;
+
+typedef struct fitsne_ctx fitsne_ctx;
+
+const char* fitsne_last_error(void);
+int fitsne_abi_version(void);
+
+/* Context: one per (device, dtype, dims, interpolation options).
+ * intervals_per_integer: FIt-SNE's option; the reference hard-codes 1.0
+ * (nbody.py:134) and only 1.0 has an oracle. */
+int fitsne_create(fitsne_ctx** out, int device, int dims, int dtype,
+                  int points_per_interval, int min_intervals,
+                  double intervals_per_integer);
+int fitsne_destroy(fitsne_ctx* ctx);
+int fitsne_set_interp(fitsne_ctx* ctx, int points_per_interval, int min_intervals,
+                      double intervals_per_integer);
+
+/* --- a1: make_grid (nbody.py:118-150).  Device bbox reduction + fp64 grid
+ * formulas; the grid is copied to *grid_host (one host sync) and kept as the
+ * context's current grid. */
+int fitsne_make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, fitsne_grid* grid_host,
+                     void* stream);
+/* Local bounding box only (multi-GPU: the caller all-reduces MIN/MAX, then
+ * calls fitsne_grid_from_bbox on every rank).  bbox_host = {min_0..min_{s-1},
+ * max_0..max_{s-1}}. */
+int fitsne_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, void* stream);
+int fitsne_grid_from_bbox(fitsne_ctx* ctx, const double* bbox_host, fitsne_grid* grid_host);
+/* Install an explicit grid (nbody.InterpGrid built by the caller). */
+int fitsne_set_grid(fitsne_ctx* ctx, const fitsne_grid* grid_host);
+
+/* --- a2: _point_interp (nbody.py:201-230): node_index (n, p^s) int64 and
+ * weights (n, p^s) in ctx dtype.  Bit-exact node indices. */
+int fitsne_point_interp(fitsne_ctx* ctx, const void* Y, int64_t n, int64_t* node_index,
+                        void* weights, void* stream);
+
+/* --- a3: spread_charges (nbody.py:233-251).  charges (n, ncharge) row-major
+ * ctx dtype; coeffs out (ncharge, G) ctx dtype. */
+int fitsne_spread(fitsne_ctx* ctx, const void* Y, int64_t n, const void* charges,
+                  int ncharge, void* coeffs, void* stream);
+
+/* --- a4/a5: kernel_matvec_fft (nbody.py:262-311): v = Toeplitz(K) w on the
+ * current grid for `ncol` coefficient vectors (ncol, G). */
+int fitsne_kernel_matvec(fitsne_ctx* ctx, int kernel, const void* coeffs, int ncol,
+                         void* out, void* stream);
+
+/* --- a6: gather_potentials (nbody.py:344-350): values (ncol, G) -> out (n, ncol). */
+int fitsne_gather(fitsne_ctx* ctx, const void* Y, int64_t n, const void* values, int ncol,
+                  void* out, void* stream);
+
+/* --- a16: evaluate_nbody (nbody.py:353-399): builds the grid from the points,
+ * charges (n, ncharge) -> out (n, ncharge). */
+int fitsne_evaluate_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* charges,
+                          int ncharge, int kernel, int include_self, void* out, void* stream);
+
+/* --- a7/a8: compute_repulsive(method="fft") (optimizer.py:193-245).
+ * forces (n, s); z_host gets Z; k1 (n,) and k2 (n, s+1) optional (NULL). */
+int fitsne_repulsive(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces, double* z_host,
+                     void* k1, void* k2, void* stream);
+/* --- a14: compute_repulsive(method="exact") (optimizer.py:169-190, 236). */
+int fitsne_repulsive_exact(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces,
+                           double* z_host, void* k1, void* k2, void* stream);
+
+/* --- a15 -> CSR: the symmetric affinities (both triangles) of
+ * affinities.SparseAffinities (affinities.py:78-104).  Registers device
+ * arrays (kept alive by the caller): rows [row_begin, row_begin+n_rows) of the
+ * full matrix; col indices are global point indices. */
+int fitsne_set_affinities(fitsne_ctx* ctx, const int64_t* rowptr, const int32_t* col,
+                          const void* val, int64_t n_rows, int64_t row_begin, int64_t n_total,
+                          int64_t nnz);
+
+/* --- a9: compute_attractive (optimizer.py:150-166) over the registered rows.
+ * Y_full (n_total, s); out (n_rows, s). */
+int fitsne_attractive(fitsne_ctx* ctx, const void* Y_full, void* out, void* stream);
+
+/* --- a10: gradient (optimizer.py:248-262), method="fft": 4(alpha F_attr - F_rep).
+ * Single-GPU (registered rows must be all rows).  grad (n, s); z_host optional. */
+int fitsne_gradient(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, double* z_host,
+                    void* stream);
+
+/* --- a12: _kl_given_z (optimizer.py:265-275) over the registered rows. */
+int fitsne_kl(fitsne_ctx* ctx, const void* Y_full, double z, double* kl_host, void* stream);
+
+/* --- a11: step (optimizer.py:299-323): in-place Y, velocity, gains update.
+ * FITSNE_ENONFINITE if grad has a non-finite entry (Y, state untouched). */
+int fitsne_step(fitsne_ctx* ctx, void* Y, const void* grad, void* velocity, void* gains,
+                int64_t n, double momentum, double learning_rate, void* stream);
+
+/* --- a13 inner loop (optimizer.py:383-413): one fused t-SNE iteration on the
+ * device: grid, spread, FFT, Z, gather, SpMV, KL, update.  kl_dev (double*)
+ * receives KL of the pre-step Y at kl_dev[0] (device pointer, may be NULL);
+ * status_dev (int32*, device) gets FITSNE_ENONFINITE if the gradient or the new Y
+ * is non-finite (sticky, may be NULL).  One host sync (grid size). */
+int fitsne_iterate(fitsne_ctx* ctx, const void* Y, void* Y_out, void* velocity, void* gains,
+                   double alpha, double momentum, double learning_rate, double* kl_dev,
+                   int32_t* status_dev, void* stream);
+
+/* --- a16 helper: brute_force_nbody (nbody.py:402-419) on the device. */
+int fitsne_exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* charges,
+                       int ncharge, int kernel, int include_self, void* out, void* stream);
+
+/* Stage entry points for the sharded (multi-GPU) gradient: the host performs
+ * the NCCL collectives between them (parallel.py).  The grid accumulator holds
+ * 4 slots per node in the context dtype, fitsne_grid_accum_len() elements, and
+ * must be zero before the first spread (it is cleared again by fitsne_fft_tsne). */
+int64_t fitsne_grid_accum_len(fitsne_ctx* ctx);
+int fitsne_spread_tsne(fitsne_ctx* ctx, const void* Y_local, int64_t n_local, void* accum,
+                       void* stream);
+int fitsne_fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, int with_k1,
+                    double* z_host, void* stream);
+int fitsne_gather_tsne(fitsne_ctx* ctx, const void* Y_local, int64_t n_local, void* forces,
+                       void* k1, void* k2, void* stream);
+int fitsne_gradient_rows(fitsne_ctx* ctx, const void* Y_full, const void* forces_local,
+                         double alpha, void* grad_local, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* FITSNE_B200_H */

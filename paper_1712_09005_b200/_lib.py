@@ -1,0 +1,202 @@
+"""ctypes binding of libfitsne_b200.so (include/fitsne_b200.h).
+
+The library is the only compute path: if it cannot be loaded, or no CUDA
+device is visible, every call raises instead of falling back to the CPU.
+Device memory and streams come from torch (plumbing only); the kernels are the
+library's own sm_100a code.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+import threading
+from pathlib import Path
+
+import torch
+
+_PKG = Path(__file__).resolve().parent
+LIB_PATH = _PKG / "libfitsne_b200.so"
+
+OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG = range(8)
+F32, F64 = 0, 1
+CAUCHY, CAUCHY_SQUARED = 0, 1
+
+
+class FitsneError(RuntimeError):
+    """CUDA-level failure inside libfitsne_b200 (not a user error)."""
+
+
+class Grid(C.Structure):
+    _fields_ = [
+        ("lo", C.c_double * 2),
+        ("hi", C.c_double * 2),
+        ("spacing", C.c_double * 2),
+        ("dims", C.c_int32),
+        ("n_intervals", C.c_int32),
+        ("points_per_interval", C.c_int32),
+        ("nodes_per_dim", C.c_int32),
+        ("fft_len", C.c_int32),
+        ("status", C.c_int32),
+    ]
+
+
+_vp = C.c_void_p
+_i64 = C.c_int64
+_int = C.c_int
+_dbl = C.c_double
+
+_SIGS = {
+    "fitsne_last_error": (C.c_char_p, []),
+    "fitsne_abi_version": (_int, []),
+    "fitsne_create": (_int, [C.POINTER(_vp), _int, _int, _int, _int, _int, _dbl]),
+    "fitsne_destroy": (_int, [_vp]),
+    "fitsne_set_interp": (_int, [_vp, _int, _int, _dbl]),
+    "fitsne_make_grid": (_int, [_vp, _vp, _i64, C.POINTER(Grid), _vp]),
+    "fitsne_bbox": (_int, [_vp, _vp, _i64, C.POINTER(_dbl), _vp]),
+    "fitsne_grid_from_bbox": (_int, [_vp, C.POINTER(_dbl), C.POINTER(Grid)]),
+    "fitsne_set_grid": (_int, [_vp, C.POINTER(Grid)]),
+    "fitsne_point_interp": (_int, [_vp, _vp, _i64, _vp, _vp, _vp]),
+    "fitsne_spread": (_int, [_vp, _vp, _i64, _vp, _int, _vp, _vp]),
+    "fitsne_kernel_matvec": (_int, [_vp, _int, _vp, _int, _vp, _vp]),
+    "fitsne_gather": (_int, [_vp, _vp, _i64, _vp, _int, _vp, _vp]),
+    "fitsne_evaluate_nbody": (_int, [_vp, _vp, _i64, _vp, _int, _int, _int, _vp, _vp]),
+    "fitsne_exact_nbody": (_int, [_vp, _vp, _i64, _vp, _int, _int, _int, _vp, _vp]),
+    "fitsne_repulsive": (_int, [_vp, _vp, _i64, _vp, C.POINTER(_dbl), _vp, _vp, _vp]),
+    "fitsne_repulsive_exact": (_int, [_vp, _vp, _i64, _vp, C.POINTER(_dbl), _vp, _vp, _vp]),
+    "fitsne_set_affinities": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64]),
+    "fitsne_attractive": (_int, [_vp, _vp, _vp, _vp]),
+    "fitsne_gradient": (_int, [_vp, _vp, _dbl, _vp, C.POINTER(_dbl), _vp]),
+    "fitsne_kl": (_int, [_vp, _vp, _dbl, C.POINTER(_dbl), _vp]),
+    "fitsne_step": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp]),
+    "fitsne_iterate": (_int, [_vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp]),
+    "fitsne_grid_accum_len": (_i64, [_vp]),
+    "fitsne_spread_tsne": (_int, [_vp, _vp, _i64, _vp, _vp]),
+    "fitsne_fft_tsne": (_int, [_vp, _vp, _i64, _int, C.POINTER(_dbl), _vp]),
+    "fitsne_gather_tsne": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "fitsne_gradient_rows": (_int, [_vp, _vp, _vp, _dbl, _vp, _vp]),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+_lock = threading.Lock()
+
+
+def load(path: Path | str = LIB_PATH):
+    """Load the shared library and declare every prototype (no GPU needed)."""
+    global _lib
+    with _lock:
+        if _lib is not None:
+            return _lib
+        p = Path(path)
+        if not p.exists():
+            raise ImportError(
+                f"{p} is missing: build it with `python -m paper_1712_09005_b200.build` "
+                "(there is no CPU fallback)"
+            )
+        lib = C.CDLL(str(p))
+        for name, (res, args) in _SIGS.items():
+            fn = getattr(lib, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = lib
+        return lib
+
+
+def lib():
+    return _lib if _lib is not None else load()
+
+
+def last_error() -> str:
+    msg = lib().fitsne_last_error()
+    return msg.decode() if msg else ""
+
+
+def check(rc: int, what: str = "") -> None:
+    """Map a status code to the reference's exception types."""
+    if rc == OK:
+        return
+    msg = last_error() or what
+    if rc in (EINVAL, EOUTSIDE, EZ, ETOOBIG):
+        raise ValueError(msg)
+    if rc == ENONFINITE:
+        raise FloatingPointError(msg)
+    if rc == ENOMEM:
+        raise MemoryError(msg)
+    raise FitsneError(f"{what}: {msg}" if what else msg)
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise RuntimeError(
+            "paper_1712_09005_b200 runs only on a CUDA (sm_100a) device; none is visible "
+            "and there is no CPU fallback"
+        )
+
+
+def ptr(t: torch.Tensor | None):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+def stream_handle(device: int | None = None):
+    return C.c_void_p(torch.cuda.current_stream(device).cuda_stream)
+
+
+class Context:
+    """One libfitsne context: (device, dims, dtype, interpolation options)."""
+
+    def __init__(self, device: int, dims: int, dtype: torch.dtype, p: int, min_intervals: int,
+                 intervals_per_integer: float = 1.0):
+        require_cuda()
+        self.lib = lib()
+        self.device = device
+        self.dims = dims
+        self.dtype = dtype
+        self.code = F64 if dtype == torch.float64 else F32
+        self.p = p
+        self.min_intervals = min_intervals
+        self.ipi = float(intervals_per_integer)
+        h = C.c_void_p()
+        with torch.cuda.device(device):
+            check(self.lib.fitsne_create(C.byref(h), device, dims, self.code, p, min_intervals,
+                                         self.ipi), "fitsne_create")
+        self.h = h
+        self._P_key = None
+        self._P_refs = None
+
+    def __del__(self):
+        try:
+            if getattr(self, "h", None) and _lib is not None:
+                _lib.fitsne_destroy(self.h)
+                self.h = None
+        except Exception:
+            pass
+
+    @property
+    def stream(self):
+        return stream_handle(self.device)
+
+    def set_affinities(self, csr, key=None):
+        """Register a device CSR (rowptr int64, col int32, val) with this context."""
+        if key is not None and key == self._P_key:
+            return
+        rowptr, col, val, row_begin, n_total = csr
+        check(self.lib.fitsne_set_affinities(self.h, ptr(rowptr), ptr(col), ptr(val),
+                                             rowptr.numel() - 1, row_begin, n_total, col.numel()),
+              "fitsne_set_affinities")
+        self._P_key = key
+        self._P_refs = csr  # keep the device arrays alive while registered
+
+
+_contexts: dict = {}
+
+
+def context(device: int, dims: int, dtype: torch.dtype, p: int = 3, min_intervals: int = 20,
+            intervals_per_integer: float = 1.0) -> Context:
+    key = (device, dims, dtype, p, min_intervals, float(intervals_per_integer),
+           threading.get_ident())
+    ctx = _contexts.get(key)
+    if ctx is None:
+        ctx = Context(device, dims, dtype, p, min_intervals, intervals_per_integer)
+        _contexts[key] = ctx
+    return ctx

@@ -1,0 +1,164 @@
+"""Affinity input type and its device CSR form.
+
+``SparseAffinities`` mirrors the reference type (affinities.py:78-104): the
+symmetric P stored once per unordered pair (rows < cols, int64) with float64
+values whose ordered-pair total is 2 * sum(values) = 1.  The gradient kernels
+read P as the FULL symmetric CSR (both triangles, int64 row pointers, int32
+column indices, values in the compute dtype), built once on the device and
+cached on the P object -- the "P-matrix CSR input" of the north star.
+
+Any object with ``n``, ``rows``, ``cols``, ``values`` (e.g. the reference's
+own SparseAffinities) and a symmetric ``scipy.sparse`` matrix (full, both
+triangles) are accepted too.
+
+The data -> affinities pipeline (kNN, perplexity calibration, symmetrize) of
+the reference is outside this path (P is precomputed and held fixed).
+"""
+
+from __future__ import annotations
+
+import weakref
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+__all__ = ["SparseAffinities", "DeviceCSR", "device_csr", "csr_from_full"]
+
+
+@dataclass
+class SparseAffinities:
+    n: int
+    rows: np.ndarray
+    cols: np.ndarray
+    values: np.ndarray
+
+    def __post_init__(self):
+        self.rows = np.asarray(self.rows, dtype=np.int64)
+        self.cols = np.asarray(self.cols, dtype=np.int64)
+        self.values = np.asarray(self.values, dtype=float)
+        if not (self.rows.shape == self.cols.shape == self.values.shape):
+            raise ValueError("rows, cols, values must share a shape")
+        if np.any(self.rows >= self.cols):
+            raise ValueError("entries must be stored with row < col")
+        if np.any(self.values < 0):
+            raise ValueError("affinities must be nonnegative")
+
+    @property
+    def ordered_total(self) -> float:
+        return 2.0 * float(self.values.sum())
+
+
+@dataclass
+class DeviceCSR:
+    """Rows [row_begin, row_begin + n_rows) of the full symmetric P."""
+
+    rowptr: torch.Tensor   # (n_rows+1,) int64, rowptr[0] == 0
+    col: torch.Tensor      # (nnz,) int32 global column indices
+    val: torch.Tensor      # (nnz,) compute dtype
+    row_begin: int
+    n_total: int
+    ordered_total: float   # sum of all stored values (both triangles)
+
+    @property
+    def n_rows(self) -> int:
+        return self.rowptr.numel() - 1
+
+    def as_tuple(self):
+        return (self.rowptr, self.col, self.val, self.row_begin, self.n_total)
+
+
+def _coo_full(P, device):
+    """(rows, cols, vals) of the full symmetric matrix on the device."""
+    if hasattr(P, "rows") and hasattr(P, "cols") and hasattr(P, "values"):
+        n = int(P.n)
+        r = torch.as_tensor(np.asarray(P.rows, dtype=np.int64)).to(device)
+        c = torch.as_tensor(np.asarray(P.cols, dtype=np.int64)).to(device)
+        v = torch.as_tensor(np.asarray(P.values, dtype=np.float64)).to(device)
+        return n, torch.cat([r, c]), torch.cat([c, r]), torch.cat([v, v])
+    try:
+        import scipy.sparse as sp
+    except ImportError:  # pragma: no cover
+        sp = None
+    if sp is not None and sp.issparse(P):
+        coo = P.tocoo()
+        if coo.shape[0] != coo.shape[1]:
+            raise ValueError("affinity matrix must be square")
+        n = coo.shape[0]
+        return (n, torch.as_tensor(coo.row.astype(np.int64)).to(device),
+                torch.as_tensor(coo.col.astype(np.int64)).to(device),
+                torch.as_tensor(coo.data.astype(np.float64)).to(device))
+    raise TypeError("affinities must be a SparseAffinities-like object or a scipy.sparse matrix")
+
+
+def csr_from_full(n, r, c, v, dtype, row_begin=0, row_end=None) -> DeviceCSR:
+    """Sort device COO (full matrix) into CSR rows [row_begin, row_end)."""
+    if row_end is None:
+        row_end = n
+    total = float(v.sum().item()) if v.numel() else 0.0
+    if row_begin != 0 or row_end != n:
+        keep = (r >= row_begin) & (r < row_end)
+        r, c, v = r[keep], c[keep], v[keep]
+    order = torch.argsort(r * n + c)
+    r, c, v = r[order], c[order], v[order]
+    counts = torch.bincount(r - row_begin, minlength=row_end - row_begin)
+    rowptr = torch.zeros(row_end - row_begin + 1, dtype=torch.int64, device=r.device)
+    torch.cumsum(counts, 0, out=rowptr[1:])
+    return DeviceCSR(rowptr.contiguous(), c.to(torch.int32).contiguous(), v.to(dtype).contiguous(),
+                     int(row_begin), int(n), total)
+
+
+_side_cache: dict = {}
+
+
+def _cache_slot(P):
+    try:
+        d = P.__dict__
+        return d.setdefault("_fitsne_csr", {})
+    except AttributeError:
+        key = id(P)
+        slot = _side_cache.get(key)
+        if slot is None:
+            slot = {}
+            _side_cache[key] = slot
+            try:
+                weakref.finalize(P, _side_cache.pop, key, None)
+            except TypeError:
+                pass
+        return slot
+
+
+def _fingerprint(P):
+    if hasattr(P, "rows"):
+        return (int(P.n), len(P.rows), id(P.rows), id(P.cols), id(P.values))
+    return (P.shape, P.nnz, id(P))
+
+
+def device_csr(P, dtype: torch.dtype, device: int, row_begin: int = 0, row_end=None) -> DeviceCSR:
+    """Device CSR of P in ``dtype``, built once and cached on the P object."""
+    slot = _cache_slot(P)
+    key = (dtype, device, row_begin, row_end, _fingerprint(P))
+    hit = slot.get(key)
+    if hit is not None:
+        return hit
+    with torch.cuda.device(device):
+        n, r, c, v = _coo_full(P, torch.device("cuda", device))
+        csr = csr_from_full(n, r, c, v, dtype, row_begin, n if row_end is None else row_end)
+        del r, c, v
+    # keep one entry per (dtype, device, rows): drop stale fingerprints
+    for k in [k for k in slot if k[:4] == key[:4]]:
+        del slot[k]
+    slot[key] = csr
+    return csr
+
+
+def n_points(P) -> int:
+    if hasattr(P, "n"):
+        return int(P.n)
+    return int(P.shape[0])
+
+
+def ordered_total(P) -> float:
+    if hasattr(P, "ordered_total"):
+        return float(P.ordered_total)
+    return float(P.sum())

@@ -1,0 +1,572 @@
+// Attractive half of the gradient, KL, the momentum/gains update and the
+// exact O(N^2) sums, on sm_100a.
+//
+//   compute_attractive (optimizer.py:150-166): the reference applies every
+//   stored upper-triangle pair in both directions with two bincounts; here P
+//   is the full symmetric CSR (both triangles) and each row is reduced by one
+//   warp: F_i = sum_j p_ij / (1 + |y_i - y_j|^2) (y_i - y_j).
+//   _kl_given_z (optimizer.py:265-275): KL = 2 sum_{upper, p>0} p (log p - log q)
+//   with q = 1/((1+d^2) Z) equals, over the full matrix,
+//   sum p log p + sum p log1p(d^2) + (sum p) log Z; the first sum is fixed and
+//   precomputed once, the second is fused into the SpMV row loop.
+//   step (optimizer.py:299-323).
+//   _exact_repulsion_sums (optimizer.py:169-190).
+#include <cmath>
+#include <algorithm>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace fitsne {
+
+static constexpr int kBlock = 256;
+
+static inline int nblocks(int64_t n, int block = kBlock) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (1LL << 30)) g = (1LL << 30);
+  return (int)g;
+}
+
+template <typename T>
+__device__ __forceinline__ T fast_log1p(T x);
+template <>
+__device__ __forceinline__ float fast_log1p<float>(float x) { return log1pf(x); }
+template <>
+__device__ __forceinline__ double fast_log1p<double>(double x) { return log1p(x); }
+
+// ---------------------------------------------------------------------------
+// warp-per-row CSR SpMV.  MODE 0: F_attr out.  MODE 1: gradient
+// 4 (alpha F_attr - F_rep).  KL: per-block partial of sum p log1p(d^2).
+// ---------------------------------------------------------------------------
+template <typename T, int S, int MODE, bool KL>
+__global__ void __launch_bounds__(kBlock)
+k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+          const T* __restrict__ val, const T* __restrict__ Y, int64_t n_rows, int64_t row_begin,
+          const T* __restrict__ frep, T alpha, T* __restrict__ out, double* __restrict__ klpart) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double kl = 0.0;
+  for (int64_t r = warp; r < n_rows; r += nwarps) {
+    const int64_t i = row_begin + r;
+    T yi[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) yi[d] = Y[i * S + d];
+    const int64_t beg = rowptr[r], end = rowptr[r + 1];
+    T acc[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) acc[d] = 0;
+    T klr = 0;
+    for (int64_t k = beg + lane; k < end; k += 32) {
+      const int32_t j = __ldg(col + k);
+      const T p = __ldg(val + k);
+      T d2 = 0;
+      T df[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        df[d] = yi[d] - __ldg(Y + (int64_t)j * S + d);
+        d2 += df[d] * df[d];
+      }
+      const T w = p / ((T)1 + d2);
+#pragma unroll
+      for (int d = 0; d < S; ++d) acc[d] += w * df[d];
+      if (KL) {
+        if (p > (T)0) klr += p * fast_log1p<T>(d2);
+      }
+    }
+#pragma unroll
+    for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
+    if (KL) kl += (double)klr;
+    if (lane == 0) {
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        if (MODE == 0) out[r * S + d] = acc[d];
+        else out[r * S + d] = (T)4 * (alpha * acc[d] - frep[r * S + d]);
+      }
+    }
+  }
+  if (KL) {
+    __shared__ double red[kBlock / 32];
+    kl = warp_sum(kl);
+    if (lane == 0) red[threadIdx.x >> 5] = kl;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0;
+      for (int w = 0; w < kBlock / 32; ++w) s += red[w];
+      klpart[blockIdx.x] = s;
+    }
+  }
+}
+
+// deterministic fold of per-block partials into dst[0]
+__global__ void k_fold(const double* __restrict__ part, int n, double* __restrict__ dst) {
+  __shared__ double red[32];
+  double s = 0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) s += part[k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+    dst[0] = t;
+  }
+}
+
+static int attract_grid(fitsne_ctx* ctx) {
+  int64_t warps_needed = ctx->n_rows;
+  int64_t blocks = (warps_needed * 32 + kBlock - 1) / kBlock;
+  int64_t cap = (int64_t)ctx->num_sms * 16;  // persistent-ish: 16 blocks of 8 warps per SM
+  if (blocks > cap) blocks = cap;
+  if (blocks < 1) blocks = 1;
+  return (int)blocks;
+}
+
+template <typename T>
+static int launch_attract(fitsne_ctx* ctx, const T* Y, const T* frep, T alpha, T* out, int mode,
+                          bool kl, double* klpart, int blocks, cudaStream_t st) {
+  const T* val = (const T*)ctx->val;
+#define ATT(S, M, K)                                                                          \
+  k_attract<T, S, M, K><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, val, Y, ctx->n_rows, \
+                                                   ctx->row_begin, frep, alpha, out, klpart)
+  if (ctx->dims == 1) {
+    if (mode == 0) { if (kl) ATT(1, 0, true); else ATT(1, 0, false); }
+    else { if (kl) ATT(1, 1, true); else ATT(1, 1, false); }
+  } else {
+    if (mode == 0) { if (kl) ATT(2, 0, true); else ATT(2, 0, false); }
+    else { if (kl) ATT(2, 1, true); else ATT(2, 1, false); }
+  }
+#undef ATT
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double alpha, void* out,
+               bool grad, bool kl, cudaStream_t st) {
+  if (!ctx->rowptr) { set_error("no affinities registered"); return FITSNE_EINVAL; }
+  FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  double* part = (double*)ctx->part.ptr;
+  const int blocks = attract_grid(ctx);
+  if (ctx->dtype == FITSNE_F32)
+    FITSNE_TRY(launch_attract<float>(ctx, (const float*)Yfull, (const float*)forces, (float)alpha,
+                                     (float*)out, grad ? 1 : 0, kl, part, blocks, st));
+  else
+    FITSNE_TRY(launch_attract<double>(ctx, (const double*)Yfull, (const double*)forces, alpha,
+                                      (double*)out, grad ? 1 : 0, kl, part, blocks, st));
+  if (kl) {
+    k_fold<<<1, 256, 0, st>>>(part, blocks, (double*)ctx->scal.ptr + 1);
+    FITSNE_CHECK_LAUNCH();
+  }
+  return FITSNE_OK;
+}
+
+int kl_sum(fitsne_ctx* ctx, const void* Yfull, cudaStream_t st) {
+  // F_attr is computed as a by-product into scratch; only the KL partial is kept
+  size_t es = dsize(ctx->dtype);
+  FITSNE_TRY(ensure(ctx->gtmp, es * (size_t)std::max<int64_t>(ctx->n_rows, 1) * ctx->dims));
+  return attractive(ctx, Yfull, nullptr, 1.0, ctx->gtmp.ptr, false, true, st);
+}
+
+// sum over stored p>0 of p log p and of p (fixed per affinity matrix)
+template <typename T>
+__global__ void k_plogp(const T* __restrict__ val, int64_t nnz, double* __restrict__ part) {
+  double s = 0, m = 0;
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < nnz;
+       k += (int64_t)gridDim.x * blockDim.x) {
+    double p = (double)val[k];
+    if (p > 0) { s += p * log(p); m += p; }
+  }
+  __shared__ double r1[32], r2[32];
+  s = warp_sum(s);
+  m = warp_sum(m);
+  if ((threadIdx.x & 31) == 0) { r1[threadIdx.x >> 5] = s; r2[threadIdx.x >> 5] = m; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < (int)blockDim.x / 32; ++w) { a += r1[w]; b += r2[w]; }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void k_fold2(const double* __restrict__ part, int n, double* __restrict__ dst) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int k = 0; k < n; ++k) { a += part[2 * k]; b += part[2 * k + 1]; }
+    dst[0] = a;
+    dst[1] = b;
+  }
+}
+
+int compute_plogp(fitsne_ctx* ctx, cudaStream_t st) {
+  FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  int blocks = std::min<int64_t>(nblocks(std::max<int64_t>(ctx->nnz, 1)), ctx->num_sms * 4);
+  double* part = (double*)ctx->part.ptr;
+  double* sc = (double*)ctx->scal.ptr;
+  if (ctx->dtype == FITSNE_F32) k_plogp<float><<<blocks, kBlock, 0, st>>>((const float*)ctx->val, ctx->nnz, part);
+  else k_plogp<double><<<blocks, kBlock, 0, st>>>((const double*)ctx->val, ctx->nnz, part);
+  FITSNE_CHECK_LAUNCH();
+  k_fold2<<<1, 32, 0, st>>>(part, blocks, sc + 4);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 4, sc + 4, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  ctx->plogp = ctx->h_scal[4];
+  ctx->psum = ctx->h_scal[5];
+  ctx->plogp_valid = true;
+  return FITSNE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// step (optimizer.py:299-323)
+// ---------------------------------------------------------------------------
+template <typename T>
+__device__ __forceinline__ int npsign(T v) { return (v > 0) - (v < 0); }
+
+template <typename T>
+__global__ void k_step(T* __restrict__ Y, const T* __restrict__ g, T* __restrict__ vel,
+                       T* __restrict__ gains, int64_t m, T momentum, T lr) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= m) return;
+  T gi = g[i], v = vel[i], gn = gains[i];
+  bool agree = npsign(gi) == npsign(v);
+  T vn = momentum * v - lr * gn * gi;
+  vel[i] = vn;
+  Y[i] = Y[i] + vn;
+  T ng = agree ? gn * (T)0.8 : gn + (T)0.2;
+  gains[i] = ng < (T)0.01 ? (T)0.01 : ng;
+}
+
+template <typename T>
+__global__ void k_nonfinite(const T* __restrict__ x, int64_t m, int* __restrict__ flag) {
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m;
+       i += (int64_t)gridDim.x * blockDim.x)
+    if (!isfinite(x[i])) bad = 1;
+  if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flag, 1);
+}
+
+int nonfinite_count(fitsne_ctx* ctx, const void* x, int64_t count, int* out_host, cudaStream_t st) {
+  FITSNE_TRY(ensure(ctx->counter, 64 * sizeof(int)));
+  int* flag = (int*)ctx->counter.ptr + 1;
+  FITSNE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  int blocks = std::min<int64_t>(nblocks(std::max<int64_t>(count, 1)), ctx->num_sms * 8);
+  if (ctx->dtype == FITSNE_F32) k_nonfinite<float><<<blocks, kBlock, 0, st>>>((const float*)x, count, flag);
+  else k_nonfinite<double><<<blocks, kBlock, 0, st>>>((const double*)x, count, flag);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_status + 1, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  *out_host = ctx->h_status[1];
+  return FITSNE_OK;
+}
+
+int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gains, int64_t n,
+                double momentum, double lr, cudaStream_t st) {
+  int64_t m = n * ctx->dims;
+  int bad = 0;
+  FITSNE_TRY(nonfinite_count(ctx, grad, m, &bad, st));
+  if (bad) {
+    set_error("non-finite gradient");
+    return FITSNE_ENONFINITE;
+  }
+  if (m == 0) return FITSNE_OK;
+  if (ctx->dtype == FITSNE_F32)
+    k_step<float><<<nblocks(m), kBlock, 0, st>>>((float*)Y, (const float*)grad, (float*)vel,
+                                                 (float*)gains, m, (float)momentum, (float)lr);
+  else
+    k_step<double><<<nblocks(m), kBlock, 0, st>>>((double*)Y, (const double*)grad, (double*)vel,
+                                                  (double*)gains, m, momentum, lr);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// fused iteration: SpMV + KL partial + gradient + update + next-Y finiteness
+// ---------------------------------------------------------------------------
+template <typename T, int S>
+__global__ void __launch_bounds__(kBlock)
+k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+          const T* __restrict__ val, const T* __restrict__ Y, int64_t n, const T* __restrict__ frep,
+          T alpha, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel, T* __restrict__ gains,
+          double* __restrict__ klpart, int32_t* __restrict__ status) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  double kl = 0.0;
+  int bad = 0;
+  for (int64_t i = warp; i < n; i += nwarps) {
+    T yi[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) yi[d] = Y[i * S + d];
+    const int64_t beg = rowptr[i], end = rowptr[i + 1];
+    T acc[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) acc[d] = 0;
+    T klr = 0;
+    for (int64_t k = beg + lane; k < end; k += 32) {
+      const int32_t j = __ldg(col + k);
+      const T p = __ldg(val + k);
+      T d2 = 0;
+      T df[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        df[d] = yi[d] - __ldg(Y + (int64_t)j * S + d);
+        d2 += df[d] * df[d];
+      }
+      const T w = p / ((T)1 + d2);
+#pragma unroll
+      for (int d = 0; d < S; ++d) acc[d] += w * df[d];
+      if (p > (T)0) klr += p * fast_log1p<T>(d2);
+    }
+#pragma unroll
+    for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
+    kl += (double)klr;
+    if (lane < S) {
+      const int d = lane;
+      T a = acc[0];
+#pragma unroll
+      for (int e = 1; e < S; ++e) if (d == e) a = acc[e];
+      const int64_t o = i * S + d;
+      T g = (T)4 * (alpha * a - frep[o]);
+      if (!isfinite(g)) bad |= 1;
+      T v = vel[o], gn = gains[o];
+      bool agree = npsign(g) == npsign(v);
+      T vn = momentum * v - lr * gn * g;
+      T ynew = yi[d] + vn;
+      if (!isfinite(ynew)) bad |= 2;
+      vel[o] = vn;
+      Yout[o] = ynew;
+      T ng = agree ? gn * (T)0.8 : gn + (T)0.2;
+      gains[o] = ng < (T)0.01 ? (T)0.01 : ng;
+    }
+  }
+  __shared__ double red[kBlock / 32];
+  kl = warp_sum(kl);
+  if (lane == 0) red[threadIdx.x >> 5] = kl;
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < kBlock / 32; ++w) s += red[w];
+    klpart[blockIdx.x] = s;
+    if (bad && status) atomicOr(status, bad);
+  }
+}
+
+// KL = plogp + sum p log1p(d^2) + psum log Z  -> dst
+__global__ void k_kl_final(const double* __restrict__ part, int n, const double* __restrict__ scal,
+                           double plogp, double psum, double* __restrict__ dst) {
+  __shared__ double red[32];
+  double s = 0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) s += part[k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+    dst[0] = plogp + t + psum * log(scal[0]);
+  }
+}
+
+int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
+                  double momentum, double lr, double* kl_dev, int32_t* status_dev, cudaStream_t st) {
+  const int64_t n = ctx->n_total;
+  size_t es = dsize(ctx->dtype);
+  FITSNE_TRY(ensure(ctx->forces, es * (size_t)n * ctx->dims));
+  FITSNE_TRY(make_grid(ctx, Yin, n, st));
+  FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
+  FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
+  FITSNE_TRY(gather_tsne(ctx, Yin, n, ctx->forces.ptr, nullptr, nullptr, st));
+  if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
+  FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
+  double* part = (double*)ctx->part.ptr;
+  int blocks = attract_grid(ctx);
+#define IT(T, S)                                                                                  \
+  k_iterate<T, S><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, (const T*)ctx->val,           \
+                                             (const T*)Yin, n, (const T*)ctx->forces.ptr, (T)alpha, \
+                                             (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains,    \
+                                             part, status_dev)
+  if (ctx->dtype == FITSNE_F32) { if (ctx->dims == 1) IT(float, 1); else IT(float, 2); }
+  else { if (ctx->dims == 1) IT(double, 1); else IT(double, 2); }
+#undef IT
+  FITSNE_CHECK_LAUNCH();
+  if (kl_dev) {
+    k_kl_final<<<1, 256, 0, st>>>(part, blocks, (const double*)ctx->scal.ptr, ctx->plogp, ctx->psum,
+                                  kl_dev);
+    FITSNE_CHECK_LAUNCH();
+  }
+  return FITSNE_OK;
+}
+
+// ---------------------------------------------------------------------------
+// exact O(N^2) sums (optimizer.py:169-190): k1_i = sum_{j!=i} q_ij,
+// k2_i = sum_{j!=i} q_ij^2 (y_j, 1), q_ij = 1/(1+d^2)
+// ---------------------------------------------------------------------------
+template <typename T, int S>
+__global__ void k_exact(const T* __restrict__ Y, int64_t n, T* __restrict__ k1, T* __restrict__ k2) {
+  constexpr int TILE = 256;
+  __shared__ T ys[TILE * S];
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  T yi[S];
+#pragma unroll
+  for (int d = 0; d < S; ++d) yi[d] = (i < n) ? Y[i * S + d] : (T)0;
+  double a1 = 0, a2[S + 1];
+#pragma unroll
+  for (int d = 0; d <= S; ++d) a2[d] = 0;
+  for (int64_t t0 = 0; t0 < n; t0 += TILE) {
+    __syncthreads();
+    for (int k = threadIdx.x; k < TILE * S; k += blockDim.x) {
+      int64_t j = t0 + k / S;
+      ys[k] = (j < n) ? Y[j * S + (k % S)] : (T)0;
+    }
+    __syncthreads();
+    int lim = (n - t0 < TILE) ? (int)(n - t0) : TILE;
+    if (i < n) {
+      for (int jj = 0; jj < lim; ++jj) {
+        int64_t j = t0 + jj;
+        if (j == i) continue;
+        T d2 = 0;
+#pragma unroll
+        for (int d = 0; d < S; ++d) {
+          T df = yi[d] - ys[jj * S + d];
+          d2 += df * df;
+        }
+        T a = (T)1 / ((T)1 + d2);
+        T b = a * a;
+        a1 += (double)a;
+#pragma unroll
+        for (int d = 0; d < S; ++d) a2[d] += (double)(b * ys[jj * S + d]);
+        a2[S] += (double)b;
+      }
+    }
+  }
+  if (i < n) {
+    k1[i] = (T)a1;
+#pragma unroll
+    for (int d = 0; d <= S; ++d) k2[i * (S + 1) + d] = (T)a2[d];
+  }
+}
+
+template <typename T>
+__global__ void k_sum(const T* __restrict__ x, int64_t n, double* __restrict__ dst) {
+  // single block deterministic sum
+  __shared__ double red[32];
+  double s = 0;
+  for (int64_t k = threadIdx.x; k < n; k += blockDim.x) s += (double)x[k];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+    dst[0] = t;
+  }
+}
+
+int exact_sums(fitsne_ctx* ctx, const void* Y, int64_t n, void* k1, void* k2, cudaStream_t st) {
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  if (ctx->dtype == FITSNE_F32) {
+    if (ctx->dims == 1) k_exact<float, 1><<<nblocks(n), 256, 0, st>>>((const float*)Y, n, (float*)k1, (float*)k2);
+    else k_exact<float, 2><<<nblocks(n), 256, 0, st>>>((const float*)Y, n, (float*)k1, (float*)k2);
+    FITSNE_CHECK_LAUNCH();
+    k_sum<float><<<1, 1024, 0, st>>>((const float*)k1, n, (double*)ctx->scal.ptr);
+  } else {
+    if (ctx->dims == 1) k_exact<double, 1><<<nblocks(n), 256, 0, st>>>((const double*)Y, n, (double*)k1, (double*)k2);
+    else k_exact<double, 2><<<nblocks(n), 256, 0, st>>>((const double*)Y, n, (double*)k1, (double*)k2);
+    FITSNE_CHECK_LAUNCH();
+    k_sum<double><<<1, 1024, 0, st>>>((const double*)k1, n, (double*)ctx->scal.ptr);
+  }
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+// forces = (y * k2[:, s] - k2[:, :s]) / Z   (optimizer.py:244)
+template <typename T, int S>
+__global__ void k_forces(const T* __restrict__ Y, int64_t n, const T* __restrict__ k2,
+                         const double* __restrict__ scal, T* __restrict__ f) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T z = (T)scal[0];
+#pragma unroll
+  for (int d = 0; d < S; ++d) f[i * S + d] = (Y[i * S + d] * k2[i * (S + 1) + S] - k2[i * (S + 1) + d]) / z;
+}
+
+int forces_from_sums(fitsne_ctx* ctx, const void* Y, int64_t n, const void* k2, void* forces,
+                     cudaStream_t st) {
+  const double* sc = (const double*)ctx->scal.ptr;
+  if (ctx->dtype == FITSNE_F32) {
+    if (ctx->dims == 1) k_forces<float, 1><<<nblocks(n), kBlock, 0, st>>>((const float*)Y, n, (const float*)k2, sc, (float*)forces);
+    else k_forces<float, 2><<<nblocks(n), kBlock, 0, st>>>((const float*)Y, n, (const float*)k2, sc, (float*)forces);
+  } else {
+    if (ctx->dims == 1) k_forces<double, 1><<<nblocks(n), kBlock, 0, st>>>((const double*)Y, n, (const double*)k2, sc, (double*)forces);
+    else k_forces<double, 2><<<nblocks(n), kBlock, 0, st>>>((const double*)Y, n, (const double*)k2, sc, (double*)forces);
+  }
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+// brute_force_nbody (nbody.py:402-419): out[i, c] = sum_j K(d2_ij) q[j, c]
+template <typename T, int S>
+__global__ void k_exact_nbody(const T* __restrict__ Y, int64_t n, const T* __restrict__ q, int nq,
+                              int kern, int include_self, T* __restrict__ out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  T yi[S];
+#pragma unroll
+  for (int d = 0; d < S; ++d) yi[d] = Y[i * S + d];
+  for (int c = 0; c < nq; ++c) {
+    double acc = 0;
+    for (int64_t j = 0; j < n; ++j) {
+      double d2 = 0;
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        double df = (double)yi[d] - (double)Y[j * S + d];
+        d2 += df * df;
+      }
+      double b = 1.0 / (1.0 + d2);
+      if (kern == FITSNE_CAUCHY_SQUARED) b = b * b;
+      acc += b * (double)q[j * nq + c];
+    }
+    if (!include_self) acc -= (double)q[i * nq + c];
+    out[i * nq + c] = (T)acc;
+  }
+}
+
+int exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* q, int nq, int kernel,
+                int include_self, void* out, cudaStream_t st) {
+  if (n <= 0 || nq <= 0) return FITSNE_OK;
+  if (ctx->dtype == FITSNE_F32) {
+    if (ctx->dims == 1) k_exact_nbody<float, 1><<<nblocks(n), kBlock, 0, st>>>((const float*)Y, n, (const float*)q, nq, kernel, include_self, (float*)out);
+    else k_exact_nbody<float, 2><<<nblocks(n), kBlock, 0, st>>>((const float*)Y, n, (const float*)q, nq, kernel, include_self, (float*)out);
+  } else {
+    if (ctx->dims == 1) k_exact_nbody<double, 1><<<nblocks(n), kBlock, 0, st>>>((const double*)Y, n, (const double*)q, nq, kernel, include_self, (double*)out);
+    else k_exact_nbody<double, 2><<<nblocks(n), kBlock, 0, st>>>((const double*)Y, n, (const double*)q, nq, kernel, include_self, (double*)out);
+  }
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+template <typename T>
+__global__ void k_sub(T* __restrict__ out, const T* __restrict__ q, int64_t m) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) out[i] -= q[i];
+}
+
+// out -= q (self-term removal, K(y, y) = 1: nbody.py:374-375)
+int sub_inplace(fitsne_ctx* ctx, void* out, const void* q, int64_t count, cudaStream_t st) {
+  if (count <= 0) return FITSNE_OK;
+  if (ctx->dtype == FITSNE_F32) k_sub<float><<<nblocks(count), kBlock, 0, st>>>((float*)out, (const float*)q, count);
+  else k_sub<double><<<nblocks(count), kBlock, 0, st>>>((double*)out, (const double*)q, count);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+int read_scalars(fitsne_ctx* ctx, int count, cudaStream_t st) {
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal, ctx->scal.ptr, sizeof(double) * count, cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  return FITSNE_OK;
+}
+
+}  // namespace fitsne

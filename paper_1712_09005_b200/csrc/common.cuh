@@ -1,0 +1,228 @@
+// Shared definitions of the sm_100a FIt-SNE library: context, grid arguments,
+// status handling, complex arithmetic and the bit-exact box/weight helpers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <cstddef>
+#include <string>
+
+#include "../../include/fitsne_b200.h"
+
+namespace fitsne {
+
+// ----------------------------------------------------------------------------
+// error handling
+// ----------------------------------------------------------------------------
+void set_error(const std::string& msg);
+
+struct Status {
+  int code;
+  Status(int c = FITSNE_OK) : code(c) {}
+  bool ok() const { return code == FITSNE_OK; }
+};
+
+#define FITSNE_CUDA(expr)                                                          \
+  do {                                                                             \
+    cudaError_t _e = (expr);                                                       \
+    if (_e != cudaSuccess) {                                                       \
+      ::fitsne::set_error(std::string("CUDA error: ") + cudaGetErrorString(_e) +   \
+                          " at " __FILE__ ":" + std::to_string(__LINE__));         \
+      return FITSNE_ECUDA;                                                         \
+    }                                                                              \
+  } while (0)
+
+#define FITSNE_CHECK_LAUNCH() FITSNE_CUDA(cudaGetLastError())
+
+#define FITSNE_TRY(expr)              \
+  do {                                \
+    int _s = (expr);                  \
+    if (_s != FITSNE_OK) return _s;   \
+  } while (0)
+
+// ----------------------------------------------------------------------------
+// grid arguments passed by value to kernels (the device twin of InterpGrid)
+// ----------------------------------------------------------------------------
+struct GridArgs {
+  double lo[2];
+  double hi[2];
+  double h[2];
+  int dims;
+  int n_int;
+  int p;
+  int n;   // nodes per dim
+  int L;   // FFT length
+};
+
+inline GridArgs grid_args(const fitsne_grid& g) {
+  GridArgs a;
+  for (int d = 0; d < 2; ++d) {
+    a.lo[d] = g.lo[d];
+    a.hi[d] = g.hi[d];
+    a.h[d] = g.spacing[d];
+  }
+  a.dims = g.dims;
+  a.n_int = g.n_intervals;
+  a.p = g.points_per_interval;
+  a.n = g.nodes_per_dim;
+  a.L = g.fft_len;
+  return a;
+}
+
+// nodes in a box per point: p^dims
+constexpr int kMaxP = 8;
+
+// Channel layout of the t-SNE spread / potentials: one 4-slot record per node.
+//   spread:     [0] unit charge, [1] y_0, [2] y_1, [3] unused
+//   potentials: [0] K2*1, [1] K2*y_0, [2] K2*y_1, [3] K1*1
+constexpr int kNodeSlots = 4;
+
+// ----------------------------------------------------------------------------
+// the context
+// ----------------------------------------------------------------------------
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t cap = 0;
+};
+
+}  // namespace fitsne
+
+struct fitsne_ctx {
+  int device = 0;
+  int dims = 2;
+  int dtype = FITSNE_F32;
+  int p = 3;
+  int min_intervals = 20;
+  double intervals_per_integer = 1.0;
+
+  fitsne_grid grid{};
+  bool grid_valid = false;
+
+  // scratch (grow-only)
+  fitsne::DevBuf accum;     // spread accumulator, kNodeSlots per node, ctx dtype
+  bool accum_clean = false; // accum holds zeros over its whole capacity
+  fitsne::DevBuf fbuf;      // FFT work: 2 pairs x n x L complex
+  fitsne::DevBuf sbuf;      // kernel spectrum rows: n x (L/2+1) complex
+  fitsne::DevBuf pot;       // potentials: kNodeSlots per node
+  fitsne::DevBuf tw;        // twiddles exp(-2 pi i m / L)
+  int tw_len = 0;
+  fitsne::DevBuf zpart;     // Parseval partials (double), L/2+1
+  fitsne::DevBuf bbox_part; // per-block bbox partials (double)
+  fitsne::DevBuf scal;      // device scalars (double): [0] Z, [1] KL sum, [2..] misc
+  fitsne::DevBuf counter;   // int32 counters / status words
+  fitsne::DevBuf forces;    // (N, s) repulsive forces scratch
+  fitsne::DevBuf gtmp;      // (N, s) gradient scratch
+  fitsne::DevBuf part;      // per-block partial sums (double)
+  fitsne::DevBuf gen;       // generic scratch
+
+  fitsne_grid* h_grid = nullptr;  // pinned mirror
+  double* h_scal = nullptr;       // pinned scalars
+  int32_t* h_status = nullptr;    // pinned status
+
+  // affinities (borrowed device pointers)
+  const int64_t* rowptr = nullptr;
+  const int32_t* col = nullptr;
+  const void* val = nullptr;
+  int64_t n_rows = 0, row_begin = 0, n_total = 0, nnz = 0;
+  bool plogp_valid = false;
+  double plogp = 0.0;   // sum over stored (full, both triangles) p>0 of p log p
+  double psum = 0.0;    // sum over stored p>0 entries
+
+  int num_sms = 148;
+};
+
+namespace fitsne {
+
+int ensure(DevBuf& b, size_t bytes);
+inline size_t dsize(int dtype) { return dtype == FITSNE_F64 ? 8 : 4; }
+
+// ----------------------------------------------------------------------------
+// complex helpers
+// ----------------------------------------------------------------------------
+template <typename T> struct C2;
+template <> struct C2<float> { using type = float2; };
+template <> struct C2<double> { using type = double2; };
+
+template <typename V>
+__device__ __forceinline__ V cmul(V a, V b) {
+  V r;
+  r.x = a.x * b.x - a.y * b.y;
+  r.y = a.x * b.y + a.y * b.x;
+  return r;
+}
+template <typename V>
+__device__ __forceinline__ V cadd(V a, V b) { V r; r.x = a.x + b.x; r.y = a.y + b.y; return r; }
+template <typename V>
+__device__ __forceinline__ V csub(V a, V b) { V r; r.x = a.x - b.x; r.y = a.y - b.y; return r; }
+template <typename V>
+__device__ __forceinline__ V cconj(V a) { a.y = -a.y; return a; }
+
+// ----------------------------------------------------------------------------
+// Bit-exact box assignment + Lagrange weights (nbody.py:201-230).
+//
+// Follows numpy's arithmetic: t = (x - lo)/h (IEEE double), cell =
+// clip(floor_divide(t, p), 0, n_int-1) with numpy's npy_divmod semantics,
+// u = (t - cell*p) - 0.5, w_j = prod_{i != j}(u - i) / prod_{i != j}(j - i)
+// multiplied left to right (nbody.py:183-190).  All in double with explicit
+// _rn intrinsics so that no FMA contraction can change a rounding.
+// ----------------------------------------------------------------------------
+__device__ __forceinline__ double npy_floor_divide(double a, double b) {
+  // numpy/_core/src/npymath/npy_math_internal.h.src : npy_divmod
+  double mod = fmod(a, b);
+  double div = __ddiv_rn(__dsub_rn(a, mod), b);
+  if (mod != 0.0) {
+    if ((b < 0) != (mod < 0)) {
+      div = __dsub_rn(div, 1.0);
+    }
+  }
+  double floordiv;
+  if (div != 0.0) {
+    floordiv = floor(div);
+    if (__dsub_rn(div, floordiv) > 0.5) floordiv = __dadd_rn(floordiv, 1.0);
+  } else {
+    floordiv = copysign(0.0, __ddiv_rn(a, b));
+  }
+  return floordiv;
+}
+
+// returns the cell (box) index along one dimension and fills w[0..p-1]
+__device__ __forceinline__ int box_weights(double x, double lo, double h, int n_int, int p,
+                                           double* w) {
+  double t = __ddiv_rn(__dsub_rn(x, lo), h);
+  double q = npy_floor_divide(t, (double)p);
+  long long c = (long long)q;
+  if (c < 0) c = 0;
+  if (c > n_int - 1) c = n_int - 1;
+  double u = __dsub_rn(__dsub_rn(t, (double)(c * p)), 0.5);
+  if (p == 3) {
+    // denominators 2, -1, 2 (nbody.py:176-180)
+    double d0 = u, d1 = __dsub_rn(u, 1.0), d2 = __dsub_rn(u, 2.0);
+    w[0] = __ddiv_rn(__dmul_rn(d1, d2), 2.0);
+    w[1] = __ddiv_rn(__dmul_rn(d0, d2), -1.0);
+    w[2] = __ddiv_rn(__dmul_rn(d0, d1), 2.0);
+  } else {
+    for (int j = 0; j < p; ++j) {
+      double num = 1.0, den = 1.0;
+      bool first = true;
+      for (int i = 0; i < p; ++i) {
+        if (i == j) continue;
+        double di = __dsub_rn(u, (double)i);
+        num = first ? di : __dmul_rn(num, di);
+        den = __dmul_rn(den, (double)(j - i));
+        first = false;
+      }
+      w[j] = __ddiv_rn(num, den);
+    }
+  }
+  return (int)c;
+}
+
+// block-wide reductions ------------------------------------------------------
+template <typename V>
+__device__ __forceinline__ V warp_sum(V v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+}  // namespace fitsne

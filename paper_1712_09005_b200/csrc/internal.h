@@ -1,0 +1,57 @@
+// Host-side orchestration functions shared by the C-ABI translation unit.
+#pragma once
+
+#include "common.cuh"
+
+namespace fitsne {
+
+// grid ------------------------------------------------------------------------
+int grid_from_bbox(fitsne_ctx* ctx, const double* bbox, fitsne_grid* out);
+int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host,
+                 cudaStream_t st);
+int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st);
+int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
+
+// repulsion pipeline ------------------------------------------------------------
+// spread of the t-SNE charges (1, y_0[, y_1]) into ctx->accum (or `accum`)
+int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
+// FFT stage: accum -> ctx->pot, Z -> ctx->scal[0] (needs n_total for Z)
+int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st);
+// gather: pot -> forces (n, s) [+ k1 (n,), k2 (n, s+1)]
+int gather_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces, void* k1, void* k2,
+                cudaStream_t st);
+
+// general n-body pieces (nbody.py public API) ------------------------------------
+int point_interp(fitsne_ctx* ctx, const void* Y, int64_t n, int64_t* idx, void* w,
+                 cudaStream_t st);
+int spread_general(fitsne_ctx* ctx, const void* Y, int64_t n, const void* q, int nq,
+                   void* coeffs, cudaStream_t st);
+int matvec_general(fitsne_ctx* ctx, int kernel, const void* coeffs, int ncol, void* out,
+                   cudaStream_t st);
+int gather_general(fitsne_ctx* ctx, const void* Y, int64_t n, const void* vals, int ncol,
+                   void* out, cudaStream_t st);
+
+// exact O(N^2) sums: k1 (n,), k2 (n, s+1) both ctx dtype; Z -> scal[0]
+int exact_sums(fitsne_ctx* ctx, const void* Y, int64_t n, void* k1, void* k2, cudaStream_t st);
+int forces_from_sums(fitsne_ctx* ctx, const void* Y, int64_t n, const void* k2, void* forces,
+                     cudaStream_t st);
+int exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* q, int nq, int kernel,
+                int include_self, void* out, cudaStream_t st);
+
+// attractive / KL / step ------------------------------------------------------------
+int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double alpha,
+               void* out, bool grad, bool kl, cudaStream_t st);
+int kl_sum(fitsne_ctx* ctx, const void* Yfull, cudaStream_t st);  // -> scal[1] = sum p log1p(d2)
+int compute_plogp(fitsne_ctx* ctx, cudaStream_t st);
+int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gains, int64_t n,
+                double momentum, double lr, cudaStream_t st);
+int nonfinite_count(fitsne_ctx* ctx, const void* x, int64_t count, int* out_host,
+                    cudaStream_t st);
+int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains,
+                  double alpha, double momentum, double lr, double* kl_dev, int32_t* status_dev,
+                  cudaStream_t st);
+
+int read_scalars(fitsne_ctx* ctx, int count, cudaStream_t st);  // scal[0..count) -> h_scal
+int sub_inplace(fitsne_ctx* ctx, void* out, const void* q, int64_t count, cudaStream_t st);
+
+}  // namespace fitsne

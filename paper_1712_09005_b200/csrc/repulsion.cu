@@ -1,0 +1,1027 @@
+// Repulsive half of the t-SNE gradient on sm_100a: bounding box + grid
+// (nbody.py:118-150), box/weights (nbody.py:201-230), charge spreading
+// (nbody.py:233-251), circulant-FFT convolution with the Cauchy kernels
+// (nbody.py:262-311), gather (nbody.py:344-350) and the t-SNE assembly of
+// optimizer.py:193-245.
+//
+// 2-D convolution layout (all intermediate buffers are L2 resident):
+//   accum  : spread charges, kNodeSlots (=4) per node, node-major (x*n + y)
+//   F      : [pair][x][k]  complex, x in [0,n), k in [0,L)   (row-FFT output)
+//   S      : [i][ky]       complex, i in [0,n), ky in [0,L/2] (kernel row FFT;
+//            .x = row transform of K1, .y = of K2, both real-even)
+//   pot    : potentials, 4 slots per node
+// Two real signals are packed per complex signal ("pairs"): convolving
+// a + i b with a real kernel gives K*a + i K*b, so no Hermitian split is
+// needed.  t-SNE pairs: A = y_0 + i y_1 (-> K2), B = unit (-> K2 + i K1).
+// Z comes from Parseval on B: Z = sum_k K1hat |Bhat|^2 / L^2 - N, equal to
+// the reference's sum of K1 potentials (optimizer.py:206, 241).
+#include <cmath>
+#include <algorithm>
+
+#include "common.cuh"
+#include "fft.cuh"
+#include "internal.h"
+
+namespace fitsne {
+
+static constexpr int kBlock = 256;
+
+static inline int grid_for(int64_t n, int block = kBlock) {
+  int64_t g = (n + block - 1) / block;
+  if (g < 1) g = 1;
+  if (g > (1LL << 30)) g = (1LL << 30);
+  return (int)g;
+}
+
+// =============================================================================
+// a1: bounding box (nbody.py:131-133) and grid formulas (nbody.py:134-143)
+// =============================================================================
+template <typename T, int S>
+__global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ part,
+                       int* __restrict__ nonfinite) {
+  double mn[S], mx[S];
+#pragma unroll
+  for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
+  int bad = 0;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      double v = (double)Y[i * S + d];
+      if (!isfinite(v)) bad = 1;
+      mn[d] = fmin(mn[d], v);
+      mx[d] = fmax(mx[d], v);
+    }
+  }
+  __shared__ double smn[32][S], smx[32][S];
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+  }
+  int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0) {
+#pragma unroll
+    for (int d = 0; d < S; ++d) { smn[wid][d] = mn[d]; smx[wid][d] = mx[d]; }
+  }
+  bad = __syncthreads_or(bad);
+  if (threadIdx.x == 0) {
+    int nw = (blockDim.x + 31) / 32;
+    for (int w = 1; w < nw; ++w)
+#pragma unroll
+      for (int d = 0; d < S; ++d) { mn[d] = fmin(mn[d], smn[w][d]); mx[d] = fmax(mx[d], smx[w][d]); }
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      part[blockIdx.x * 2 * S + d] = mn[d];
+      part[blockIdx.x * 2 * S + S + d] = mx[d];
+    }
+    if (bad) atomicOr(nonfinite, 1);
+  }
+}
+
+template <int S>
+__global__ void k_bbox_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
+  // one warp: deterministic fixed-order fold per lane then shuffle
+  double mn[S], mx[S];
+#pragma unroll
+  for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
+  for (int b = threadIdx.x; b < nblk; b += 32) {
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      mn[d] = fmin(mn[d], part[b * 2 * S + d]);
+      mx[d] = fmax(mx[d], part[b * 2 * S + S + d]);
+    }
+  }
+#pragma unroll
+  for (int d = 0; d < S; ++d)
+    for (int o = 16; o > 0; o >>= 1) {
+      mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
+      mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
+    }
+  if (threadIdx.x == 0)
+#pragma unroll
+    for (int d = 0; d < S; ++d) { out[d] = mn[d]; out[S + d] = mx[d]; }
+}
+
+int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, cudaStream_t st) {
+  const int S = ctx->dims;
+  int nblk = (int)std::min<int64_t>(std::max<int64_t>((n + kBlock - 1) / kBlock, 1), 4 * ctx->num_sms);
+  FITSNE_TRY(ensure(ctx->bbox_part, sizeof(double) * (size_t)nblk * 2 * S + 64));
+  FITSNE_TRY(ensure(ctx->counter, 64 * sizeof(int)));
+  double* part = (double*)ctx->bbox_part.ptr;
+  double* outd = part + (size_t)nblk * 2 * S;
+  int* flag = (int*)ctx->counter.ptr;
+  FITSNE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  if (ctx->dtype == FITSNE_F32) {
+    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag);
+    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag);
+  } else {
+    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag);
+    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag);
+  }
+  FITSNE_CHECK_LAUNCH();
+  if (S == 1) k_bbox_final<1><<<1, 32, 0, st>>>(part, nblk, outd);
+  else k_bbox_final<2><<<1, 32, 0, st>>>(part, nblk, outd);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * 2 * S, cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_status, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  if (ctx->h_status[0]) {
+    set_error("points must be finite");
+    return FITSNE_ENONFINITE;
+  }
+  for (int d = 0; d < 2 * S; ++d) bbox_host[d] = ctx->h_scal[8 + d];
+  return FITSNE_OK;
+}
+
+// Exact restatement of make_grid's scalar formulas (nbody.py:131-143).  Host
+// code compiled with -ffp-contract=off so each operation rounds like numpy.
+int grid_from_bbox(fitsne_ctx* ctx, const double* bbox, fitsne_grid* out) {
+  const int S = ctx->dims;
+  double lo[2] = {0, 0}, hi[2] = {0, 0}, span[2] = {0, 0};
+  double widest = -INFINITY;
+  for (int d = 0; d < S; ++d) {
+    lo[d] = bbox[d];
+    hi[d] = bbox[S + d];
+    if (!std::isfinite(lo[d]) || !std::isfinite(hi[d])) {
+      set_error("points must be finite");
+      return FITSNE_ENONFINITE;
+    }
+    span[d] = hi[d] - lo[d];
+    widest = std::max(widest, span[d]);
+  }
+  double cells = (ctx->intervals_per_integer == 1.0) ? std::ceil(widest)
+                                                     : std::ceil(widest * ctx->intervals_per_integer);
+  if (cells > 1e7) {
+    set_error("embedding span too large for the interpolation grid");
+    return FITSNE_ETOOBIG;
+  }
+  int n_int = std::max(ctx->min_intervals, (int)cells);
+  for (int d = 0; d < S; ++d) {
+    if (span[d] < 1.0) {
+      double c = 0.5 * (lo[d] + hi[d]);
+      lo[d] = c - 0.5;
+      hi[d] = c + 0.5;
+    } else {
+      double pad = 1e-6 * span[d];
+      lo[d] -= pad;
+      hi[d] += pad;
+    }
+  }
+  fitsne_grid g{};
+  g.dims = S;
+  g.n_intervals = n_int;
+  g.points_per_interval = ctx->p;
+  long long nn = (long long)n_int * ctx->p;
+  if (nn > (1 << 20)) {
+    set_error("interpolation grid too large");
+    return FITSNE_ETOOBIG;
+  }
+  g.nodes_per_dim = (int)nn;
+  for (int d = 0; d < S; ++d) {
+    g.lo[d] = lo[d];
+    g.hi[d] = hi[d];
+    g.spacing[d] = (hi[d] - lo[d]) / (double)nn;
+  }
+  g.fft_len = smooth23_at_least(2 * (int)nn - 1);
+  g.status = 0;
+  *out = g;
+  return FITSNE_OK;
+}
+
+template <typename T>
+__global__ void k_twiddles(typename C2<T>::type* tw, int L) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < L; m += gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi(2.0 * (double)m / (double)L, &s, &c);
+    typename C2<T>::type w;
+    w.x = (T)c;
+    w.y = (T)(-s);
+    tw[m] = w;
+  }
+}
+
+int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
+  if (g.dims != ctx->dims) {
+    set_error("grid dims do not match the context");
+    return FITSNE_EINVAL;
+  }
+  const int L = g.fft_len;
+  // rows stage holds 2 pairs x 2 ping-pong buffers of L complex in shared memory
+  const int lmax = (ctx->dtype == FITSNE_F32) ? 6912 : 3456;
+  if (L > lmax || (g.dims == 1 && L > (ctx->dtype == FITSNE_F32 ? 5184 : 2592))) {
+    set_error("interpolation grid needs an FFT longer than supported (L=" + std::to_string(L) + ")");
+    return FITSNE_ETOOBIG;
+  }
+  ctx->grid = g;
+  ctx->grid_valid = true;
+  if (ctx->tw_len != L) {
+    size_t es = 2 * dsize(ctx->dtype);
+    FITSNE_TRY(ensure(ctx->tw, es * (size_t)L));
+    if (ctx->dtype == FITSNE_F32)
+      k_twiddles<float><<<grid_for(L), kBlock, 0, st>>>((float2*)ctx->tw.ptr, L);
+    else
+      k_twiddles<double><<<grid_for(L), kBlock, 0, st>>>((double2*)ctx->tw.ptr, L);
+    FITSNE_CHECK_LAUNCH();
+    ctx->tw_len = L;
+  }
+  return FITSNE_OK;
+}
+
+int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
+  double bbox[4];
+  FITSNE_TRY(compute_bbox(ctx, Y, n, bbox, st));
+  fitsne_grid g;
+  FITSNE_TRY(grid_from_bbox(ctx, bbox, &g));
+  return install_grid(ctx, g, st);
+}
+
+// =============================================================================
+// a2/a3: box assignment + Lagrange weights, spreading
+// =============================================================================
+template <typename T, int S>
+struct PointInterp {
+  int cell[S];
+  double w[S][kMaxP];
+};
+
+template <typename T, int S>
+__device__ __forceinline__ void interp_point(const T* __restrict__ Y, int64_t i, const GridArgs& g,
+                                             PointInterp<T, S>& pi, double* y) {
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    y[d] = (double)Y[i * S + d];
+    pi.cell[d] = box_weights(y[d], g.lo[d], g.h[d], g.n_int, g.p, pi.w[d]);
+  }
+}
+
+// t-SNE charges (1, y_0[, y_1]) of each point into 4-slot node records.
+template <typename T, int S, int P>
+__global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T* __restrict__ acc) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = (P > 0) ? P : g.p;
+  PointInterp<T, S> pi;
+  double y[S];
+  interp_point<T, S>(Y, i, g, pi, y);
+  if (S == 1) {
+    for (int a = 0; a < p; ++a) {
+      int64_t node = (int64_t)pi.cell[0] * p + a;
+      double w = pi.w[0][a];
+      T* dst = acc + node * kNodeSlots;
+      if constexpr (sizeof(T) == 4) {
+        atomicAdd(reinterpret_cast<float2*>(dst), make_float2((float)w, (float)(w * y[0])));
+      } else {
+        atomicAdd((double*)dst, w);
+        atomicAdd((double*)dst + 1, w * y[0]);
+      }
+    }
+  } else {
+    const int64_t nn = g.n;
+    for (int a = 0; a < p; ++a) {
+      int64_t rowbase = ((int64_t)pi.cell[0] * p + a) * nn + (int64_t)pi.cell[1] * p;
+      for (int b = 0; b < p; ++b) {
+        double w = pi.w[0][a] * pi.w[1][b];
+        T* dst = acc + (rowbase + b) * kNodeSlots;
+        if constexpr (sizeof(T) == 4) {
+          atomicAdd(reinterpret_cast<float4*>(dst),
+                    make_float4((float)w, (float)(w * y[0]), (float)(w * y[1]), 0.f));
+        } else {
+          atomicAdd((double*)dst, w);
+          atomicAdd((double*)dst + 1, w * y[0]);
+          atomicAdd((double*)dst + 2, w * y[1]);
+        }
+      }
+    }
+  }
+}
+
+template <typename T, int S>
+static void launch_spread_tsne(const T* Y, int64_t n, const GridArgs& g, T* acc, cudaStream_t st) {
+  if (g.p == 3) k_spread_tsne<T, S, 3><<<grid_for(n), kBlock, 0, st>>>(Y, n, g, acc);
+  else k_spread_tsne<T, S, 0><<<grid_for(n), kBlock, 0, st>>>(Y, n, g, acc);
+}
+
+static size_t accum_elems(const fitsne_grid& g) {
+  size_t G = 1;
+  for (int d = 0; d < g.dims; ++d) G *= (size_t)g.nodes_per_dim;
+  return G * kNodeSlots;
+}
+
+static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
+  size_t bytes = accum_elems(ctx->grid) * dsize(ctx->dtype);
+  if (ctx->accum.cap < bytes) {
+    FITSNE_TRY(ensure(ctx->accum, bytes));
+    ctx->accum_clean = false;
+  }
+  if (!ctx->accum_clean) {
+    FITSNE_CUDA(cudaMemsetAsync(ctx->accum.ptr, 0, ctx->accum.cap, st));
+    ctx->accum_clean = true;
+  }
+  return FITSNE_OK;
+}
+
+int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
+  if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  GridArgs g = grid_args(ctx->grid);
+  if (accum == nullptr) {
+    FITSNE_TRY(ensure_accum(ctx, st));
+    accum = ctx->accum.ptr;
+  }
+  if (n > 0) {
+    if (ctx->dtype == FITSNE_F32) {
+      if (ctx->dims == 1) launch_spread_tsne<float, 1>((const float*)Y, n, g, (float*)accum, st);
+      else launch_spread_tsne<float, 2>((const float*)Y, n, g, (float*)accum, st);
+    } else {
+      if (ctx->dims == 1) launch_spread_tsne<double, 1>((const double*)Y, n, g, (double*)accum, st);
+      else launch_spread_tsne<double, 2>((const double*)Y, n, g, (double*)accum, st);
+    }
+    FITSNE_CHECK_LAUNCH();
+  }
+  ctx->accum_clean = false;
+  return FITSNE_OK;
+}
+
+// general charges (N, nq) row-major -> coeffs (nq, G) planar
+template <typename T, int S>
+__global__ void k_spread_general(const T* __restrict__ Y, int64_t n, GridArgs g,
+                                 const T* __restrict__ q, int nq, T* __restrict__ coeffs,
+                                 int* __restrict__ outside) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  PointInterp<T, S> pi;
+  double y[S];
+  bool out = false;
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    double v = (double)Y[i * S + d];
+    if (v < g.lo[d] || v > g.hi[d]) out = true;
+  }
+  if (out) { atomicOr(outside, 1); return; }
+  interp_point<T, S>(Y, i, g, pi, y);
+  const int p = g.p;
+  const int64_t nn = g.n;
+  const int64_t G = (S == 1) ? nn : nn * nn;
+  const int cnt = (S == 1) ? p : p * p;
+  for (int k = 0; k < cnt; ++k) {
+    int a = (S == 1) ? k : k / p, b = (S == 1) ? 0 : k % p;
+    int64_t node = (S == 1) ? ((int64_t)pi.cell[0] * p + a)
+                            : (((int64_t)pi.cell[0] * p + a) * nn + (int64_t)pi.cell[1] * p + b);
+    double w = (S == 1) ? pi.w[0][a] : pi.w[0][a] * pi.w[1][b];
+    for (int c = 0; c < nq; ++c) {
+      double v = w * (double)q[i * nq + c];
+      atomicAdd(&coeffs[(int64_t)c * G + node], (T)v);
+    }
+  }
+}
+
+template <typename T, int S>
+__global__ void k_point_interp(const T* __restrict__ Y, int64_t n, GridArgs g,
+                               int64_t* __restrict__ idx, T* __restrict__ wout,
+                               int* __restrict__ outside) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool out = false;
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    double v = (double)Y[i * S + d];
+    if (v < g.lo[d] || v > g.hi[d]) out = true;
+  }
+  if (out) atomicOr(outside, 1);
+  PointInterp<T, S> pi;
+  double y[S];
+  interp_point<T, S>(Y, i, g, pi, y);
+  const int p = g.p;
+  const int64_t nn = g.n;
+  const int cnt = (S == 1) ? p : p * p;
+  for (int k = 0; k < cnt; ++k) {
+    int a = (S == 1) ? k : k / p, b = (S == 1) ? 0 : k % p;
+    int64_t node = (S == 1) ? ((int64_t)pi.cell[0] * p + a)
+                            : (((int64_t)pi.cell[0] * p + a) * nn + (int64_t)pi.cell[1] * p + b);
+    double w = (S == 1) ? pi.w[0][a] : pi.w[0][a] * pi.w[1][b];
+    idx[i * cnt + k] = node;
+    wout[i * cnt + k] = (T)w;
+  }
+}
+
+static int check_outside(fitsne_ctx* ctx, cudaStream_t st) {
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_status, ctx->counter.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  if (ctx->h_status[0]) {
+    set_error("point outside grid bounds");
+    return FITSNE_EOUTSIDE;
+  }
+  return FITSNE_OK;
+}
+
+int point_interp(fitsne_ctx* ctx, const void* Y, int64_t n, int64_t* idx, void* w, cudaStream_t st) {
+  if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  GridArgs g = grid_args(ctx->grid);
+  FITSNE_TRY(ensure(ctx->counter, 64 * sizeof(int)));
+  FITSNE_CUDA(cudaMemsetAsync(ctx->counter.ptr, 0, sizeof(int), st));
+  if (n > 0) {
+    int* flag = (int*)ctx->counter.ptr;
+    if (ctx->dtype == FITSNE_F32) {
+      if (ctx->dims == 1) k_point_interp<float, 1><<<grid_for(n), kBlock, 0, st>>>((const float*)Y, n, g, idx, (float*)w, flag);
+      else k_point_interp<float, 2><<<grid_for(n), kBlock, 0, st>>>((const float*)Y, n, g, idx, (float*)w, flag);
+    } else {
+      if (ctx->dims == 1) k_point_interp<double, 1><<<grid_for(n), kBlock, 0, st>>>((const double*)Y, n, g, idx, (double*)w, flag);
+      else k_point_interp<double, 2><<<grid_for(n), kBlock, 0, st>>>((const double*)Y, n, g, idx, (double*)w, flag);
+    }
+    FITSNE_CHECK_LAUNCH();
+  }
+  return check_outside(ctx, st);
+}
+
+int spread_general(fitsne_ctx* ctx, const void* Y, int64_t n, const void* q, int nq, void* coeffs,
+                   cudaStream_t st) {
+  if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  GridArgs g = grid_args(ctx->grid);
+  size_t G = accum_elems(ctx->grid) / kNodeSlots;
+  FITSNE_CUDA(cudaMemsetAsync(coeffs, 0, G * nq * dsize(ctx->dtype), st));
+  FITSNE_TRY(ensure(ctx->counter, 64 * sizeof(int)));
+  FITSNE_CUDA(cudaMemsetAsync(ctx->counter.ptr, 0, sizeof(int), st));
+  int* flag = (int*)ctx->counter.ptr;
+  if (n > 0) {
+    if (ctx->dtype == FITSNE_F32) {
+      if (ctx->dims == 1) k_spread_general<float, 1><<<grid_for(n), kBlock, 0, st>>>((const float*)Y, n, g, (const float*)q, nq, (float*)coeffs, flag);
+      else k_spread_general<float, 2><<<grid_for(n), kBlock, 0, st>>>((const float*)Y, n, g, (const float*)q, nq, (float*)coeffs, flag);
+    } else {
+      if (ctx->dims == 1) k_spread_general<double, 1><<<grid_for(n), kBlock, 0, st>>>((const double*)Y, n, g, (const double*)q, nq, (double*)coeffs, flag);
+      else k_spread_general<double, 2><<<grid_for(n), kBlock, 0, st>>>((const double*)Y, n, g, (const double*)q, nq, (double*)coeffs, flag);
+    }
+    FITSNE_CHECK_LAUNCH();
+  }
+  return check_outside(ctx, st);
+}
+
+// =============================================================================
+// a4/a5: kernel spectrum + circulant convolution (2-D: row / column / row)
+// =============================================================================
+enum ConvMode { MODE_TSNE = 0, MODE_GENERAL = 1 };
+
+template <typename T>
+__device__ __forceinline__ void kernel_pair(int i, int j, double hx, double hy, T& k1, T& k2) {
+  // first[i, j] = K((i hx)^2 + (j hy)^2), nbody.py:272-275
+  double dx = (double)i * hx, dy = (double)j * hy;
+  double d2 = __dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy));
+  double base = 1.0 / (1.0 + d2);
+  k1 = (T)base;
+  k2 = (T)(base * base);
+}
+
+// Row stage.  Blocks [0, n): data rows (forward FFT of the packed pairs).
+// Blocks [n, 2n): kernel-spectrum rows.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int pair0, int npair,
+               typename C2<T>::type* __restrict__ F, typename C2<T>::type* __restrict__ Sbuf,
+               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  V* a = reinterpret_cast<V*>(smem_raw);
+  const int L = g.L, n = g.n;
+  const int H = L / 2 + 1;
+  if ((int)blockIdx.x < n) {
+    const int x = blockIdx.x;
+    const int ns = (MODE == MODE_TSNE) ? 2 : npair;
+    V* b = a + (size_t)ns * L;
+    for (int y = threadIdx.x; y < L; y += blockDim.x) {
+      if (MODE == MODE_TSNE) {
+        V A = {0, 0}, B = {0, 0};
+        if (y < n) {
+          T* rec = acc + ((size_t)x * n + y) * kNodeSlots;
+          B.x = rec[0];
+          A.x = rec[1];
+          A.y = rec[2];
+          // consume-and-clear: leaves the accumulator zeroed for the next spread
+          rec[0] = 0; rec[1] = 0; rec[2] = 0;
+        }
+        a[y] = A;
+        a[L + y] = B;
+      } else {
+        const size_t G = (size_t)n * n;
+        for (int q = 0; q < npair; ++q) {
+          V v = {0, 0};
+          if (y < n) {
+            int c0 = 2 * (pair0 + q), c1 = c0 + 1;
+            v.x = coeffs[(size_t)c0 * G + (size_t)x * n + y];
+            if (c1 < ncol) v.y = coeffs[(size_t)c1 * G + (size_t)x * n + y];
+          }
+          a[(size_t)q * L + y] = v;
+        }
+      }
+    }
+    V* r = block_fft<V, T>(a, b, pl, ns, L, tw, false);
+    for (int q = 0; q < ns; ++q)
+      for (int k = threadIdx.x; k < L; k += blockDim.x)
+        F[((size_t)q * n + x) * L + k] = r[(size_t)q * L + k];
+  } else {
+    const int i = blockIdx.x - n;
+    V* b = a + L;
+    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+      V z = {0, 0};
+      int jj = (j < n) ? j : ((j > L - n) ? L - j : -1);
+      if (jj >= 0) {
+        T k1, k2;
+        kernel_pair<T>(i, jj, g.h[0], g.h[1], k1, k2);
+        z.x = k1;
+        z.y = k2;
+      }
+      a[j] = z;
+    }
+    V* r = block_fft<V, T>(a, b, pl, 1, L, tw, false);
+    for (int k = threadIdx.x; k < H; k += blockDim.x) Sbuf[(size_t)i * H + k] = r[k];
+  }
+}
+
+// Column stage: one block per column pair (ky, L-ky).  Builds the kernel
+// spectrum column, then forward FFT, multiply, Parseval (t-SNE), inverse FFT.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restrict__ Sbuf,
+       GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int kern,
+       int with_k1, double* __restrict__ zpart) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L = g.L, n = g.n, H = L / 2 + 1;
+  V* K = reinterpret_cast<V*>(smem_raw);
+  V* a = K + L;
+  V* b = a + L;
+  const int ky = blockIdx.x;
+  // spectrum column: rows mirrored (circulant embedding, nbody.py:278-281)
+  for (int i = threadIdx.x; i < L; i += blockDim.x) {
+    V z = {0, 0};
+    int ii = (i < n) ? i : ((i > L - n) ? L - i : -1);
+    if (ii >= 0) z = Sbuf[(size_t)ii * H + ky];
+    a[i] = z;
+  }
+  V* r = block_fft<V, T>(a, b, pl, 1, L, tw, false);
+  const T scale = (T)(1.0 / ((double)L * (double)L));
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    V v = r[k];
+    V kk;
+    kk.x = v.x * scale;  // K1hat / L^2 (real)
+    kk.y = v.y * scale;  // K2hat / L^2 (real)
+    K[k] = kk;
+  }
+  double zacc = 0.0;
+  const int ncolumns = (ky == 0 || 2 * ky == L) ? 1 : 2;
+  for (int cc = 0; cc < ncolumns; ++cc) {
+    const int col = (cc == 0) ? ky : L - ky;
+    for (int q = 0; q < npair; ++q) {
+      __syncthreads();
+      for (int x = threadIdx.x; x < L; x += blockDim.x) {
+        V z = {0, 0};
+        if (x < n) z = F[((size_t)q * n + x) * L + col];
+        a[x] = z;
+      }
+      V* fr = block_fft<V, T>(a, b, pl, 1, L, tw, false);
+      V* other = (fr == a) ? b : a;
+      for (int k = threadIdx.x; k < L; k += blockDim.x) {
+        V v = fr[k];
+        V kk = K[k];
+        V o;
+        if (MODE == MODE_TSNE) {
+          if (q == 0) {
+            o.x = v.x * kk.y;
+            o.y = v.y * kk.y;
+          } else {
+            zacc += (double)kk.x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
+            if (with_k1) {
+              // v * (K2 + i K1)
+              o.x = v.x * kk.y - v.y * kk.x;
+              o.y = v.x * kk.x + v.y * kk.y;
+            } else {
+              o.x = v.x * kk.y;
+              o.y = v.y * kk.y;
+            }
+          }
+        } else {
+          T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
+          o.x = v.x * m;
+          o.y = v.y * m;
+        }
+        fr[k] = o;
+      }
+      V* ir = block_fft<V, T>(fr, other, pl, 1, L, tw, true);
+      for (int x = threadIdx.x; x < n; x += blockDim.x) F[((size_t)q * n + x) * L + col] = ir[x];
+    }
+  }
+  if (MODE == MODE_TSNE) {
+    __shared__ double red[32];
+    zacc = warp_sum(zacc);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = zacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += red[w];
+      zpart[ky] = s;
+    }
+  }
+}
+
+// Row inverse stage: one block per row x.  Block 0 also folds the Parseval
+// partials into Z (deterministic order).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+k_rows_inverse(const typename C2<T>::type* __restrict__ F, GridArgs g,
+               const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int ncol,
+               int pair0, T* __restrict__ pot, T* __restrict__ out, const double* __restrict__ zpart,
+               double* __restrict__ scal, double n_total) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L = g.L, n = g.n, H = L / 2 + 1;
+  V* a = reinterpret_cast<V*>(smem_raw);
+  V* b = a + (size_t)npair * L;
+  const int x = blockIdx.x;
+  for (int q = 0; q < npair; ++q)
+    for (int k = threadIdx.x; k < L; k += blockDim.x) a[(size_t)q * L + k] = F[((size_t)q * n + x) * L + k];
+  V* r = block_fft<V, T>(a, b, pl, npair, L, tw, true);
+  if (MODE == MODE_TSNE) {
+    for (int y = threadIdx.x; y < n; y += blockDim.x) {
+      V A = r[y], B = r[L + y];
+      T* rec = pot + ((size_t)x * n + y) * kNodeSlots;
+      rec[0] = B.x;  // K2 * 1
+      rec[1] = A.x;  // K2 * y_0
+      rec[2] = A.y;  // K2 * y_1
+      rec[3] = B.y;  // K1 * 1 (only with_k1)
+    }
+    if (x == 0) {
+      __shared__ double red[32];
+      double s = 0;
+      for (int k = threadIdx.x; k < H; k += blockDim.x) s += zpart[k];
+      s = warp_sum(s);
+      if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        double t = 0;
+        for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) t += red[w];
+        scal[0] = t - n_total;  // Z
+      }
+    }
+  } else {
+    const size_t G = (size_t)n * n;
+    for (int q = 0; q < npair; ++q) {
+      int c0 = 2 * (pair0 + q), c1 = c0 + 1;
+      for (int y = threadIdx.x; y < n; y += blockDim.x) {
+        V v = r[(size_t)q * L + y];
+        out[(size_t)c0 * G + (size_t)x * n + y] = v.x;
+        if (c1 < ncol) out[(size_t)c1 * G + (size_t)x * n + y] = v.y;
+      }
+    }
+  }
+}
+
+// 1-D convolution: a single block holds the whole transform (L <= 5184 f32).
+template <typename T, int MODE>
+__global__ void __launch_bounds__(1024)
+k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g,
+         const typename C2<T>::type* __restrict__ tw, FftPlan pl, int kern, int with_k1,
+         T* __restrict__ pot, T* __restrict__ out, double* __restrict__ scal, double n_total) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L = g.L, n = g.n;
+  V* K = reinterpret_cast<V*>(smem_raw);
+  V* a = K + L;
+  V* b = a + 2 * L;
+  // spectrum: circ[:n] = first, circ[L-n+1:] = mirror (nbody.py:264-271)
+  for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    V z = {0, 0};
+    int jj = (j < n) ? j : ((j > L - n) ? L - j : -1);
+    if (jj >= 0) {
+      double d = (double)jj * g.h[0];
+      double base = 1.0 / (1.0 + __dmul_rn(d, d));
+      z.x = (T)base;
+      z.y = (T)(base * base);
+    }
+    a[j] = z;
+  }
+  V* r = block_fft<V, T>(a, b, pl, 1, L, tw, false);
+  const T scale = (T)(1.0 / (double)L);
+  for (int k = threadIdx.x; k < L; k += blockDim.x) {
+    V v = r[k];
+    V kk;
+    kk.x = v.x * scale;
+    kk.y = v.y * scale;
+    K[k] = kk;
+  }
+  __syncthreads();
+  const int npair = (MODE == MODE_TSNE) ? 2 : (ncol + 1) / 2;
+  double zacc = 0.0;
+  for (int q0 = 0; q0 < npair; q0 += 2) {
+    const int ns = min(2, npair - q0);
+    for (int y = threadIdx.x; y < L; y += blockDim.x) {
+      for (int s = 0; s < ns; ++s) {
+        V v = {0, 0};
+        if (y < n) {
+          if (MODE == MODE_TSNE) {
+            T* rec = acc + (size_t)y * kNodeSlots;
+            if (s == 0) v.x = rec[1]; else v.x = rec[0];
+          } else {
+            int c0 = 2 * (q0 + s), c1 = c0 + 1;
+            v.x = coeffs[(size_t)c0 * n + y];
+            if (c1 < ncol) v.y = coeffs[(size_t)c1 * n + y];
+          }
+        }
+        a[(size_t)s * L + y] = v;
+      }
+    }
+    if (MODE == MODE_TSNE) {
+      __syncthreads();
+      for (int y = threadIdx.x; y < n; y += blockDim.x) {
+        T* rec = acc + (size_t)y * kNodeSlots;
+        rec[0] = 0; rec[1] = 0;
+      }
+    }
+    V* fr = block_fft<V, T>(a, b, pl, ns, L, tw, false);
+    V* other = (fr == a) ? b : a;
+    for (int t = threadIdx.x; t < ns * L; t += blockDim.x) {
+      int s = t / L, k = t - s * L;
+      V v = fr[t];
+      V kk = K[k];
+      V o;
+      if (MODE == MODE_TSNE) {
+        if (s == 0) {
+          o.x = v.x * kk.y; o.y = v.y * kk.y;
+        } else {
+          zacc += (double)kk.x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
+          if (with_k1) {
+            o.x = v.x * kk.y - v.y * kk.x;
+            o.y = v.x * kk.x + v.y * kk.y;
+          } else {
+            o.x = v.x * kk.y; o.y = v.y * kk.y;
+          }
+        }
+      } else {
+        T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
+        o.x = v.x * m; o.y = v.y * m;
+      }
+      fr[t] = o;
+    }
+    V* ir = block_fft<V, T>(fr, other, pl, ns, L, tw, true);
+    for (int y = threadIdx.x; y < n; y += blockDim.x) {
+      if (MODE == MODE_TSNE) {
+        V A = ir[y], B = ir[L + y];
+        T* rec = pot + (size_t)y * kNodeSlots;
+        rec[0] = B.x; rec[1] = A.x; rec[2] = 0; rec[3] = B.y;
+      } else {
+        for (int s = 0; s < ns; ++s) {
+          V v = ir[(size_t)s * L + y];
+          int c0 = 2 * (q0 + s), c1 = c0 + 1;
+          out[(size_t)c0 * n + y] = v.x;
+          if (c1 < ncol) out[(size_t)c1 * n + y] = v.y;
+        }
+      }
+    }
+    __syncthreads();
+  }
+  if (MODE == MODE_TSNE) {
+    __shared__ double red[32];
+    zacc = warp_sum(zacc);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = zacc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double s = 0;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += red[w];
+      scal[0] = s - n_total;
+    }
+  }
+}
+
+template <typename T>
+static int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) {
+    FITSNE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  }
+  return FITSNE_OK;
+}
+
+// Runs the convolution pipeline.  MODE_TSNE: input accum (4-slot records,
+// cleared on the way), output ctx->pot, Z -> scal[0].  MODE_GENERAL: coeffs
+// (ncol, G) -> out (ncol, G) with kernel `kern`.
+template <typename T, int MODE>
+static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int kern, bool with_k1,
+                    T* out, int64_t n_total, cudaStream_t st) {
+  using V = typename C2<T>::type;
+  const fitsne_grid& gr = ctx->grid;
+  GridArgs g = grid_args(gr);
+  const int L = g.L, n = g.n, H = L / 2 + 1;
+  FftPlan pl;
+  make_plan(pl, L);
+  const V* tw = (const V*)ctx->tw.ptr;
+  double* scal = (double*)ctx->scal.ptr;
+  T* pot = (T*)ctx->pot.ptr;
+  if (gr.dims == 1) {
+    size_t smem = sizeof(V) * (size_t)L * 5;
+    FITSNE_TRY(set_smem<T>((const void*)k_conv1d<T, MODE>, smem));
+    k_conv1d<T, MODE><<<1, 1024, smem, st>>>(accum, coeffs, ncol, g, tw, pl, kern, with_k1 ? 1 : 0,
+                                             pot, out, scal, (double)n_total);
+    FITSNE_CHECK_LAUNCH();
+    return FITSNE_OK;
+  }
+  const int maxpair = 2;
+  FITSNE_TRY(ensure(ctx->fbuf, sizeof(V) * (size_t)maxpair * n * L));
+  FITSNE_TRY(ensure(ctx->sbuf, sizeof(V) * (size_t)n * H));
+  FITSNE_TRY(ensure(ctx->zpart, sizeof(double) * (size_t)H));
+  V* F = (V*)ctx->fbuf.ptr;
+  V* Sb = (V*)ctx->sbuf.ptr;
+  double* zp = (double*)ctx->zpart.ptr;
+  const int npair_total = (MODE == MODE_TSNE) ? 2 : (ncol + 1) / 2;
+  for (int pair0 = 0; pair0 < npair_total; pair0 += maxpair) {
+    const int npair = std::min(maxpair, npair_total - pair0);
+    // the spectrum rows are recomputed per pair group (one group for t-SNE)
+    size_t smem_r = sizeof(V) * (size_t)2 * npair * L;
+    FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
+    k_rows_forward<T, MODE><<<2 * n, 256, smem_r, st>>>(accum, coeffs, ncol, pair0, npair, F, Sb, g,
+                                                        tw, pl);
+    FITSNE_CHECK_LAUNCH();
+    size_t smem_c = sizeof(V) * (size_t)3 * L;
+    FITSNE_TRY(set_smem<T>((const void*)k_cols<T, MODE>, smem_c));
+    k_cols<T, MODE><<<H, 256, smem_c, st>>>(F, Sb, g, tw, pl, npair, kern, with_k1 ? 1 : 0, zp);
+    FITSNE_CHECK_LAUNCH();
+    size_t smem_i = sizeof(V) * (size_t)2 * npair * L;
+    FITSNE_TRY(set_smem<T>((const void*)k_rows_inverse<T, MODE>, smem_i));
+    k_rows_inverse<T, MODE><<<n, 256, smem_i, st>>>(F, g, tw, pl, npair, ncol, pair0, pot, out, zp,
+                                                    scal, (double)n_total);
+    FITSNE_CHECK_LAUNCH();
+  }
+  return FITSNE_OK;
+}
+
+int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st) {
+  if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  if (accum == nullptr) accum = ctx->accum.ptr;
+  size_t G = accum_elems(ctx->grid) / kNodeSlots;
+  FITSNE_TRY(ensure(ctx->pot, G * kNodeSlots * dsize(ctx->dtype)));
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  int rc;
+  if (ctx->dtype == FITSNE_F32)
+    rc = run_conv<float, MODE_TSNE>(ctx, (float*)accum, nullptr, 3, 0, with_k1, nullptr, n_total, st);
+  else
+    rc = run_conv<double, MODE_TSNE>(ctx, (double*)accum, nullptr, 3, 0, with_k1, nullptr, n_total, st);
+  if (rc == FITSNE_OK && accum == ctx->accum.ptr) ctx->accum_clean = true;  // consumed + cleared
+  return rc;
+}
+
+int matvec_general(fitsne_ctx* ctx, int kernel, const void* coeffs, int ncol, void* out,
+                   cudaStream_t st) {
+  if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  if (kernel != FITSNE_CAUCHY && kernel != FITSNE_CAUCHY_SQUARED) {
+    set_error("unknown kernel");
+    return FITSNE_EINVAL;
+  }
+  FITSNE_TRY(ensure(ctx->pot, 64));
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  if (ncol <= 0) return FITSNE_OK;
+  if (ctx->dtype == FITSNE_F32)
+    return run_conv<float, MODE_GENERAL>(ctx, nullptr, (const float*)coeffs, ncol, kernel, false,
+                                         (float*)out, 0, st);
+  return run_conv<double, MODE_GENERAL>(ctx, nullptr, (const double*)coeffs, ncol, kernel, false,
+                                        (double*)out, 0, st);
+}
+
+// =============================================================================
+// a6/a7/a8: gather + t-SNE assembly
+//   k1 = phi_K1(1) - 1, k2[:, c] = phi_K2(y_c) - y_c, k2[:, s] = phi_K2(1) - 1
+//   F_rep = (y * k2[:, s] - k2[:, :s]) / Z           (optimizer.py:206-210, 244)
+// =============================================================================
+template <typename T>
+__device__ __forceinline__ void load_slots(const T* p, T (&v)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+    double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+
+template <typename T, int S, int P>
+__global__ void k_gather_tsne(const T* __restrict__ Y, int64_t n, GridArgs g,
+                              const T* __restrict__ pot, const double* __restrict__ scal,
+                              T* __restrict__ forces, T* __restrict__ k1out, T* __restrict__ k2out) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int p = (P > 0) ? P : g.p;
+  PointInterp<T, S> pi;
+  double y[S];
+  interp_point<T, S>(Y, i, g, pi, y);
+  T phi[4] = {0, 0, 0, 0};
+  if (S == 1) {
+    for (int a = 0; a < p; ++a) {
+      T v[4];
+      load_slots<T>(pot + ((int64_t)pi.cell[0] * p + a) * kNodeSlots, v);
+      T w = (T)pi.w[0][a];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) phi[c] += v[c] * w;
+    }
+  } else {
+    const int64_t nn = g.n;
+    for (int a = 0; a < p; ++a) {
+      int64_t rowbase = ((int64_t)pi.cell[0] * p + a) * nn + (int64_t)pi.cell[1] * p;
+      for (int b = 0; b < p; ++b) {
+        T v[4];
+        load_slots<T>(pot + (rowbase + b) * kNodeSlots, v);
+        T w = (T)(pi.w[0][a] * pi.w[1][b]);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) phi[c] += v[c] * w;
+      }
+    }
+  }
+  const T Z = (T)scal[0];
+  T h4 = phi[0] - (T)1;
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    T yc = (T)y[d];
+    T hc = phi[1 + d] - yc;
+    forces[i * S + d] = (yc * h4 - hc) / Z;
+    if (k2out) k2out[i * (S + 1) + d] = hc;
+  }
+  if (k2out) k2out[i * (S + 1) + S] = h4;
+  if (k1out) k1out[i] = phi[3] - (T)1;
+}
+
+int gather_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces, void* k1, void* k2,
+                cudaStream_t st) {
+  GridArgs g = grid_args(ctx->grid);
+  if (n <= 0) return FITSNE_OK;
+  const double* scal = (const double*)ctx->scal.ptr;
+#define GATHER_LAUNCH(T, S)                                                                  \
+  do {                                                                                       \
+    if (g.p == 3)                                                                            \
+      k_gather_tsne<T, S, 3><<<grid_for(n), kBlock, 0, st>>>((const T*)Y, n, g,              \
+          (const T*)ctx->pot.ptr, scal, (T*)forces, (T*)k1, (T*)k2);                         \
+    else                                                                                     \
+      k_gather_tsne<T, S, 0><<<grid_for(n), kBlock, 0, st>>>((const T*)Y, n, g,              \
+          (const T*)ctx->pot.ptr, scal, (T*)forces, (T*)k1, (T*)k2);                         \
+  } while (0)
+  if (ctx->dtype == FITSNE_F32) {
+    if (ctx->dims == 1) GATHER_LAUNCH(float, 1); else GATHER_LAUNCH(float, 2);
+  } else {
+    if (ctx->dims == 1) GATHER_LAUNCH(double, 1); else GATHER_LAUNCH(double, 2);
+  }
+#undef GATHER_LAUNCH
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+// values (ncol, G) planar -> out (n, ncol)
+template <typename T, int S>
+__global__ void k_gather_general(const T* __restrict__ Y, int64_t n, GridArgs g,
+                                 const T* __restrict__ vals, int ncol, T* __restrict__ out,
+                                 int* __restrict__ outside) {
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  bool o = false;
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    double v = (double)Y[i * S + d];
+    if (v < g.lo[d] || v > g.hi[d]) o = true;
+  }
+  if (o) { atomicOr(outside, 1); return; }
+  PointInterp<T, S> pi;
+  double y[S];
+  interp_point<T, S>(Y, i, g, pi, y);
+  const int p = g.p;
+  const int64_t nn = g.n;
+  const int64_t G = (S == 1) ? nn : nn * nn;
+  const int cnt = (S == 1) ? p : p * p;
+  for (int c = 0; c < ncol; ++c) {
+    double acc = 0.0;
+    for (int k = 0; k < cnt; ++k) {
+      int a = (S == 1) ? k : k / p, b = (S == 1) ? 0 : k % p;
+      int64_t node = (S == 1) ? ((int64_t)pi.cell[0] * p + a)
+                              : (((int64_t)pi.cell[0] * p + a) * nn + (int64_t)pi.cell[1] * p + b);
+      double w = (S == 1) ? pi.w[0][a] : pi.w[0][a] * pi.w[1][b];
+      acc += (double)vals[(int64_t)c * G + node] * w;
+    }
+    out[i * ncol + c] = (T)acc;
+  }
+}
+
+int gather_general(fitsne_ctx* ctx, const void* Y, int64_t n, const void* vals, int ncol, void* out,
+                   cudaStream_t st) {
+  if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  GridArgs g = grid_args(ctx->grid);
+  FITSNE_TRY(ensure(ctx->counter, 64 * sizeof(int)));
+  FITSNE_CUDA(cudaMemsetAsync(ctx->counter.ptr, 0, sizeof(int), st));
+  int* flag = (int*)ctx->counter.ptr;
+  if (n > 0) {
+    if (ctx->dtype == FITSNE_F32) {
+      if (ctx->dims == 1) k_gather_general<float, 1><<<grid_for(n), kBlock, 0, st>>>((const float*)Y, n, g, (const float*)vals, ncol, (float*)out, flag);
+      else k_gather_general<float, 2><<<grid_for(n), kBlock, 0, st>>>((const float*)Y, n, g, (const float*)vals, ncol, (float*)out, flag);
+    } else {
+      if (ctx->dims == 1) k_gather_general<double, 1><<<grid_for(n), kBlock, 0, st>>>((const double*)Y, n, g, (const double*)vals, ncol, (double*)out, flag);
+      else k_gather_general<double, 2><<<grid_for(n), kBlock, 0, st>>>((const double*)Y, n, g, (const double*)vals, ncol, (double*)out, flag);
+    }
+    FITSNE_CHECK_LAUNCH();
+  }
+  return check_outside(ctx, st);
+}
+
+}  // namespace fitsne
