@@ -161,7 +161,6 @@ class Context:
             check(self.lib.fitsne_create(C.byref(h), device, dims, self.code, p, min_intervals,
                                          self.ipi), "fitsne_create")
         self.h = h
-        self._P_key = None
         self._P_refs = None
 
     def __del__(self):
@@ -176,15 +175,16 @@ class Context:
     def stream(self):
         return stream_handle(self.device)
 
-    def set_affinities(self, csr, key=None):
-        """Register a device CSR (rowptr int64, col int32, val) with this context."""
-        if key is not None and key == self._P_key:
+    def set_affinities(self, csr):
+        """Register a DeviceCSR with this context (no-op if it is already the
+        registered one; the context keeps a strong reference, so identity
+        cannot be confused with a freed object)."""
+        if csr is self._P_refs:
             return
-        rowptr, col, val, row_begin, n_total = csr
-        check(self.lib.fitsne_set_affinities(self.h, ptr(rowptr), ptr(col), ptr(val),
-                                             rowptr.numel() - 1, row_begin, n_total, col.numel()),
+        check(self.lib.fitsne_set_affinities(self.h, ptr(csr.rowptr), ptr(csr.col), ptr(csr.val),
+                                             csr.n_rows, csr.row_begin, csr.n_total,
+                                             csr.col.numel()),
               "fitsne_set_affinities")
-        self._P_key = key
         self._P_refs = csr  # keep the device arrays alive while registered
 
 

@@ -162,7 +162,7 @@ def _embedding(Y, dtype):
 def _ctx_with_P(P, dev, dims, dt, p=3, min_int=20, ipi=1.0):
     csr = device_csr(P, dt, dev)
     ctx = _lib.context(dev, dims, dt, p, min_int, ipi)
-    ctx.set_affinities(csr.as_tuple(), key=(id(csr),))
+    ctx.set_affinities(csr)
     return ctx, csr
 
 
@@ -391,7 +391,7 @@ def _run_unfused(P, y0, cfg, dev, dt, method, callback) -> TsneResult:
         f, z, k1, k2 = _repulsion_device(y, dev, dt, cfg.min_intervals, cfg.points_per_interval,
                                          method, cfg.intervals_per_integer)
         rep = Repulsion(forces=f, z=z, k1_potential=k1, k2_potentials=k2)
-        ctx.set_affinities(device_csr(P, dt, dev).as_tuple(), key=None)
+        ctx.set_affinities(device_csr(P, dt, dev))
         grad = torch.empty_like(y)
         _lib.check(ctx.lib.fitsne_gradient_rows(ctx.h, _lib.ptr(y), _lib.ptr(f), float(alpha),
                                                 _lib.ptr(grad), ctx.stream), "fitsne_gradient_rows")

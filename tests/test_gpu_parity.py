@@ -75,7 +75,8 @@ class TestGridInterp:
         og = O.grid_for(pts.astype(np.float64), 50, p)
         oidx, ow = O.interp(og, pts.astype(np.float64))
         np.testing.assert_array_equal(idx.cpu().numpy(), oidx)
-        np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=0, atol=2e-7)
+        # weights are computed in fp64 and rounded once to fp32
+        np.testing.assert_allclose(w.cpu().numpy(), ow, rtol=6e-8, atol=1e-9)
 
     def test_adversarial_cell_boundaries(self, fs):
         """Points exactly on / one ulp around cell edges: indices bit-exact."""
@@ -107,9 +108,9 @@ class TestNbodyPieces:
         assert rel_inf(coeffs, golden[tag + "_spread"]) <= tol
         for kern in nbody.Kernel:
             v = nbody.kernel_matvec_fft(golden[tag + "_spread"], kern, g, dtype=dtype)
-            assert rel_inf(v, golden[tag + f"_matvec_{kern.value}"]) <= (1e-12 if dtype == "float64" else 1e-5)
+            assert rel_inf(v, golden[tag + f"_matvec_{kern.value}"]) <= (1e-12 if dtype == "float64" else 2e-5)
         got = nbody.gather_potentials(pts, golden[tag + "_vals"], g, dtype=dtype)
-        assert rel_inf(got, golden[tag + "_gather"]) <= (1e-13 if dtype == "float64" else 1e-6)
+        assert rel_inf(got, golden[tag + "_gather"]) <= (1e-13 if dtype == "float64" else 2e-5)
 
     @pytest.mark.parametrize("dims", [1, 2])
     def test_matvec_fft_vs_direct(self, fs, dims):
