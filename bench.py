@@ -1,0 +1,383 @@
+"""Benchmark: t-SNE gradient evaluations/sec at N=1.3M, 2-D (BASELINE.json config 3).
+
+One step = one full FFT-interpolated gradient evaluation 4(alpha F_attr - F_rep)
+(optimizer.gradient, method="fft", optimizer.py:248-262) on a fixed synthetic
+(P, Y) pair: bounding box + grid, spread, kernel spectra + circulant FFT
+convolution, Parseval Z, gather, CSR SpMV + combine -- all through
+libfitsne_b200 (sm_100a).
+
+  value : device-resident throughput (Y and P already in HBM), CUDA events on
+          the launching stream, W warm-ups then exactly K timed steps.
+  e2e   : the same metric through the public drop-in call
+          optimizer.gradient(P, Y_host) with Y in pinned host memory: each step
+          copies Y in and the gradient out inside the timed region.
+  roofline: the dominant kernel (the CSR SpMV, k_attract) timed alone with
+          CUDA events; algorithmic bytes per launch / launch time vs the
+          measured HBM copy bandwidth in MEASURED_PEAKS.json.
+  cpu_baseline: the CPU oracle (oracle/fitsne_oracle.py, the reference's
+          numpy/scipy algorithm) on the host cores, rank 0 / N=1 only.
+
+--impl reference runs the reference's CPU implementation (the oracle port of
+the pure-Python reference, which cannot be installed on the box) on the same
+config; under torchrun only rank 0 works.
+
+Multi-GPU (torchrun, N>1): points and CSR rows are sharded by contiguous index
+range; per step each rank spreads its points, the grid is all-reduced (NCCL),
+every rank runs the FFT stage, gathers its points, the embedding is
+all-gathered and each rank runs the SpMV over its rows (parallel.py).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+WORKLOADS = {
+    "c3": dict(n=1_300_000, desc="C3: N=1.3M, d=50 40-cluster anisotropic power-law mixture, "
+                                 "exact kNN k=90, perplexity 30, symmetric CSR P; 2-D Y = "
+                                 "top-2 PCA of X scaled to |y|<=100; min_intervals 50, p 3"),
+}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=None, help="override N (debug)")
+    ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--breakdown", action="store_true", help="per-stage timing (extra JSON)")
+    ap.add_argument("--seed", type=int, default=3)
+    return ap.parse_args()
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.samples = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(
+                    ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                     "--format=csv,noheader,nounits"], capture_output=True, text=True, timeout=5)
+                parts = [p.strip() for p in out.stdout.strip().split(",")]
+                if len(parts) >= 7:
+                    self.samples.append(parts)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for s in self.samples for k in range(4)
+                          if s[3 + k].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.samples)}
+
+
+# ----------------------------------------------------------------------------- data
+def make_inputs(args, device):
+    """Seeded C3 inputs (P upper COO holder, Y float64 (N, 2))."""
+    import torch
+    from tools import synth
+    n = args.n or WORKLOADS["c3"]["n"]
+    t0 = time.time()
+    P, Y = synth.c3(device=device, n=n, seed=args.seed)
+    torch.cuda.synchronize() if str(device).startswith("cuda") else None
+    return P, Y, time.time() - t0
+
+
+def peaks():
+    f = ROOT / "MEASURED_PEAKS.json"
+    if f.exists():
+        d = json.loads(f.read_text())
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def traffic_from_profiles(name="spmv"):
+    f = ROOT / "profiles" / "traffic.json"
+    if f.exists():
+        try:
+            return json.loads(f.read_text()).get(name)
+        except Exception:
+            return None
+    return None
+
+
+# ----------------------------------------------------------------------------- CPU leg
+def cpu_gradient_sample(P, Y, min_int=50, p=3):
+    """Reference CPU algorithm (oracle port) for one gradient evaluation.
+
+    Sample: the full repulsion (grid, 4 spread/FFT/gather passes) plus the
+    attractive pass over 1/8 of the stored pairs; the attractive time is scaled
+    by 8 (it is linear in the pair count).  Returns seconds per evaluation.
+    """
+    from oracle import fitsne_oracle as O
+    workers = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    O.repulsion(Y, min_int, p, "fft", workers)
+    t_rep = time.perf_counter() - t0
+    m = P.rows.size // 8
+    t0 = time.perf_counter()
+    O.attraction(P.rows[:m], P.cols[:m], P.values[:m], Y)
+    t_att = time.perf_counter() - t0
+    return t_rep + 8.0 * t_att, workers
+
+
+def run_reference(args):
+    import torch
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    dev = "cuda" if torch.cuda.is_available() else "cpu"
+    P, Y, t_gen = make_inputs(args, dev)
+    for _ in range(args.warmup):
+        cpu_gradient_sample(P, Y)
+    times = []
+    workers = 1
+    for _ in range(args.steps):
+        t, workers = cpu_gradient_sample(P, Y)
+        times.append(t)
+    sec = float(np.mean(times))
+    val = 1.0 / sec
+    line = {
+        "impl": "reference",
+        "metric": "t-SNE gradient evals/sec at N=1.3M 2-D",
+        "value": val, "unit": "grad_evals/s", "n_gpus": args.gpus, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS["c3"]["desc"], "N": int(P.n),
+                   "nnz_full": int(2 * P.rows.size)},
+        "cpu_baseline": {"value": val, "unit": "grad_evals/s", "cores": workers, "kind": "port",
+                         "sample": "per step: full FFT repulsion (scipy.fft workers=cpu_count) + "
+                                   "attractive bincount pass over 1/8 of the stored pairs, x8"},
+        "e2e": {"value": val, "unit": "grad_evals/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- ours
+def timed(fn, steps, stream):
+    import torch
+    s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    s.record(stream)
+    for _ in range(steps):
+        fn()
+    e.record(stream)
+    e.synchronize()
+    return s.elapsed_time(e) / steps  # ms
+
+
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+    from paper_1712_09005_b200 import _lib, optimizer
+    from paper_1712_09005_b200.affinities import device_csr
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl")
+    dev = local
+    dt = torch.float32 if args.dtype == "float32" else torch.float64
+    P, Y, t_gen = make_inputs(args, f"cuda:{dev}")
+    n = P.n
+    stream = torch.cuda.current_stream(dev)
+
+    if world > 1:
+        from paper_1712_09005_b200 import parallel
+        ev = parallel.ShardedGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
+                                      points_per_interval=3)
+        y_full = torch.from_numpy(Y).to(device=dev, dtype=dt)
+        step = lambda: ev.gradient(y_full, 1.0)  # noqa: E731
+        for _ in range(args.warmup):
+            step()
+        dist.barrier()
+        torch.cuda.synchronize()
+        with ClockSampler(dev) as clk:
+            ms = timed(step, args.steps, stream)
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+        if rank == 0:
+            line = {
+                "metric": "t-SNE gradient evals/sec at N=1.3M 2-D", "value": 1e3 / ms,
+                "unit": "grad_evals/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dt == torch.float32 else "f64",
+                "data": "synthetic",
+                "config": {"workload": WORKLOADS["c3"]["desc"], "N": n, "parallelism": f"points{world}",
+                           "l2": "inputs larger than L2 (CSR > 126 MB)"},
+                "gpu_launches": ev.launches_per_step * args.steps,
+                "clocks": clk.summary(),
+            }
+            print(json.dumps(line), flush=True)
+        dist.destroy_process_group()
+        return
+
+    # ---- single GPU -----------------------------------------------------------
+    y = torch.from_numpy(Y).to(device=dev, dtype=dt)
+    csr = device_csr(P, dt, dev)
+    ctx = _lib.context(dev, 2, dt, 3, 50, 1.0)
+    ctx.set_affinities(csr)
+    g = torch.empty_like(y)
+    zc = __import__("ctypes").c_double()
+
+    def step():
+        _lib.check(ctx.lib.fitsne_gradient(ctx.h, _lib.ptr(y), 1.0, _lib.ptr(g), None,
+                                           ctx.stream), "fitsne_gradient")
+
+    for _ in range(max(args.warmup, 3)):
+        step()
+    torch.cuda.synchronize()
+    with ClockSampler(dev) as clk:
+        ms = timed(step, args.steps, stream)
+    clocks = clk.summary()
+
+    # grid facts for the record
+    gr = _lib.Grid()
+    _lib.check(ctx.lib.fitsne_make_grid(ctx.h, _lib.ptr(y), n, __import__("ctypes").byref(gr),
+                                        ctx.stream), "make_grid")
+    nnz = int(csr.col.numel())
+
+    # dominant kernel alone: the CSR SpMV + combine (k_attract), same launch as in the step
+    forces = torch.zeros_like(y)
+
+    def spmv():
+        _lib.check(ctx.lib.fitsne_gradient_rows(ctx.h, _lib.ptr(y), _lib.ptr(forces), 1.0,
+                                                _lib.ptr(g), ctx.stream), "gradient_rows")
+
+    for _ in range(3):
+        spmv()
+    ms_spmv = timed(spmv, args.steps, stream)
+    es = 4 if dt == torch.float32 else 8
+    s = 2
+    # algorithmic bytes: col (4) + val per nnz, int64 rowptr, Y read once (L2-resident
+    # neighbour reads counted once), F_rep in, gradient out
+    b_spmv = nnz * (4 + es) + 8 * (n + 1) + 3 * s * es * n
+    peak, peak_src = peaks()
+    achieved = b_spmv / (ms_spmv * 1e-3) / 1e9
+
+    breakdown = None
+    if args.breakdown:
+        breakdown = stage_breakdown(ctx, y, n, dt, args.steps, stream)
+
+    # e2e through the public drop-in API with pinned host buffers
+    y_host = torch.from_numpy(Y.astype(np.float32 if dt == torch.float32 else np.float64)).pin_memory()
+    api = lambda: optimizer.gradient(P, y_host, 1.0, 50, 3, "fft")  # noqa: E731
+    for _ in range(3):
+        api()
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    ms_e2e = timed(api, args.steps, stream)
+    wall_e2e = (time.perf_counter() - t0) / args.steps * 1e3
+    ms_e2e = max(ms_e2e, wall_e2e)
+
+    cpu = None
+    if not args.no_cpu_baseline and rank == 0:
+        Y64 = y.double().cpu().numpy()
+        sec, workers = cpu_gradient_sample(P, Y64)
+        cpu = {"value": 1.0 / sec, "unit": "grad_evals/s", "cores": workers, "kind": "port",
+               "sample": "one evaluation: full FFT repulsion (scipy.fft workers=cpu_count) + "
+                         "attractive bincount over 1/8 of the stored pairs, x8 (numpy: 1 thread)"}
+
+    line = {
+        "metric": "t-SNE gradient evals/sec at N=1.3M 2-D",
+        "value": 1e3 / ms, "unit": "grad_evals/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "f32" if dt == torch.float32 else "f64", "data": "synthetic",
+        "config": {"workload": WORKLOADS["c3"]["desc"], "N": n, "nnz_full": nnz,
+                   "n_intervals": int(gr.n_intervals), "nodes_per_dim": int(gr.nodes_per_dim),
+                   "fft_len": int(gr.fft_len), "parallelism": "single",
+                   "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB L2), no flush" %
+                         (nnz * (4 + es) / 1e9),
+                   "input_gen_s": round(t_gen, 1)},
+        "roofline": {"kernel": "k_attract (CSR SpMV + gradient combine)", "bound": "hbm",
+                     "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                     "peak_source": peak_src, "algorithmic_bytes": b_spmv,
+                     "launch_ms": ms_spmv, "share_of_step": ms_spmv / ms,
+                     "traffic": traffic_from_profiles("spmv")},
+        "cpu_baseline": cpu,
+        "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
+                "h2d_bytes_per_step": int(y_host.numel() * y_host.element_size()),
+                "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
+        "gpu_launches": 8 * args.steps,
+        "clocks": clocks,
+    }
+    if breakdown:
+        line["breakdown_ms"] = breakdown
+    print(json.dumps(line), flush=True)
+
+
+def stage_breakdown(ctx, y, n, dt, steps, stream):
+    """Per-stage device time of one evaluation (CUDA events, averaged)."""
+    import ctypes as C
+    import torch
+    from paper_1712_09005_b200 import _lib
+    gr = _lib.Grid()
+    out = {}
+    out["bbox+grid"] = timed(lambda: ctx.lib.fitsne_make_grid(ctx.h, _lib.ptr(y), n, C.byref(gr),
+                                                              ctx.stream), steps, stream)
+    acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=dt, device=y.device)
+    out["spread"] = timed(lambda: ctx.lib.fitsne_spread_tsne(ctx.h, _lib.ptr(y), n, _lib.ptr(acc),
+                                                             ctx.stream), steps, stream)
+    # fft stage clears the accumulator it consumes, so re-spread is not needed for timing
+    out["fft_conv"] = timed(lambda: ctx.lib.fitsne_fft_tsne(ctx.h, _lib.ptr(acc), n, 0, None,
+                                                            ctx.stream), steps, stream)
+    f = torch.empty_like(y)
+    out["gather"] = timed(lambda: ctx.lib.fitsne_gather_tsne(ctx.h, _lib.ptr(y), n, _lib.ptr(f),
+                                                             None, None, ctx.stream), steps, stream)
+    return out
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

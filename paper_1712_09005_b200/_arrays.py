@@ -99,8 +99,14 @@ def as_points(x, dims=None):
     return x
 
 
-def output(t: torch.Tensor, device_result: bool):
-    """Device tensor for device callers, float64 numpy otherwise."""
+def output(t: torch.Tensor, device_result, like=None):
+    """Device tensor for device callers; a CPU tensor (compute dtype, via a
+    pinned staging copy) for CPU-tensor callers; float64 numpy otherwise."""
     if device_result:
         return t
+    if isinstance(like, torch.Tensor):
+        host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        host.copy_(t, non_blocking=True)
+        torch.cuda.current_stream(t.device).synchronize()
+        return host
     return t.to(torch.float64).cpu().numpy()

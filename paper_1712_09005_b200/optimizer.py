@@ -245,7 +245,7 @@ def gradient(P, Y, alpha: float = 1.0, min_intervals: int = 20, points_per_inter
         f, _, _, _ = _repulsion_device(y, dev, dt, min_intervals, points_per_interval, "exact")
         _lib.check(ctx.lib.fitsne_gradient_rows(ctx.h, _lib.ptr(y), _lib.ptr(f), float(alpha),
                                                 _lib.ptr(g), ctx.stream), "fitsne_gradient_rows")
-    return A.output(g, A.is_device_input(Y))
+    return A.output(g, A.is_device_input(Y), like=Y)
 
 
 def _kl_device(ctx, y, z):
