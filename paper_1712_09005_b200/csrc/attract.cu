@@ -35,6 +35,55 @@ __device__ __forceinline__ float fast_log1p<float>(float x) { return log1pf(x); 
 template <>
 __device__ __forceinline__ double fast_log1p<double>(double x) { return log1p(x); }
 
+
+template <typename T, int S>
+__device__ __forceinline__ void load_point(const T* __restrict__ Y, int64_t j, T (&v)[S]) {
+  if constexpr (S == 2 && sizeof(T) == 4) {
+    float2 a = __ldg(reinterpret_cast<const float2*>(Y) + j);
+    v[0] = a.x; v[1] = a.y;
+  } else if constexpr (S == 2) {
+    double2 a = __ldg(reinterpret_cast<const double2*>(Y) + j);
+    v[0] = a.x; v[1] = a.y;
+  } else {
+    v[0] = __ldg(Y + j);
+  }
+}
+
+// One warp reduces CSR row [beg, end) against y_i: acc += sum_j w_ij (y_i - y_j),
+// w_ij = p_ij / (1 + d_ij^2), and (KL) klr += p_ij log1p(d_ij^2).  Two stored
+// entries per lane per trip keep two independent neighbour gathers in flight.
+template <typename T, int S, bool KL>
+__device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, const T* __restrict__ val,
+                                           const T* __restrict__ Y, int64_t beg, int64_t end,
+                                           int lane, const T (&yi)[S], T (&acc)[S], T& klr) {
+  for (int64_t k = beg + lane; k < end; k += 64) {
+    const bool two = k + 32 < end;
+    const int32_t j0 = __ldg(col + k);
+    const T p0 = __ldg(val + k);
+    const int32_t j1 = two ? __ldg(col + k + 32) : j0;
+    const T p1 = two ? __ldg(val + k + 32) : (T)0;
+    T y0[S], y1[S];
+    load_point<T, S>(Y, j0, y0);
+    load_point<T, S>(Y, j1, y1);
+    T d0[S], d1[S], s0 = 0, s1 = 0;
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      d0[d] = yi[d] - y0[d];
+      d1[d] = yi[d] - y1[d];
+      s0 += d0[d] * d0[d];
+      s1 += d1[d] * d1[d];
+    }
+    const T w0 = p0 / ((T)1 + s0);
+    const T w1 = p1 / ((T)1 + s1);
+#pragma unroll
+    for (int d = 0; d < S; ++d) acc[d] += w0 * d0[d] + w1 * d1[d];
+    if (KL) {
+      if (p0 > (T)0) klr += p0 * fast_log1p<T>(s0);
+      if (p1 > (T)0) klr += p1 * fast_log1p<T>(s1);
+    }
+  }
+}
+
 // ---------------------------------------------------------------------------
 // warp-per-row CSR SpMV.  MODE 0: F_attr out.  MODE 1: gradient
 // 4 (alpha F_attr - F_rep).  KL: per-block partial of sum p log1p(d^2).
@@ -51,30 +100,13 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
   for (int64_t r = warp; r < n_rows; r += nwarps) {
     const int64_t i = row_begin + r;
     T yi[S];
-#pragma unroll
-    for (int d = 0; d < S; ++d) yi[d] = Y[i * S + d];
+    load_point<T, S>(Y, i, yi);
     const int64_t beg = rowptr[r], end = rowptr[r + 1];
     T acc[S];
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = 0;
     T klr = 0;
-    for (int64_t k = beg + lane; k < end; k += 32) {
-      const int32_t j = __ldg(col + k);
-      const T p = __ldg(val + k);
-      T d2 = 0;
-      T df[S];
-#pragma unroll
-      for (int d = 0; d < S; ++d) {
-        df[d] = yi[d] - __ldg(Y + (int64_t)j * S + d);
-        d2 += df[d] * df[d];
-      }
-      const T w = p / ((T)1 + d2);
-#pragma unroll
-      for (int d = 0; d < S; ++d) acc[d] += w * df[d];
-      if (KL) {
-        if (p > (T)0) klr += p * fast_log1p<T>(d2);
-      }
-    }
+    row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr);
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
     if (KL) kl += (double)klr;
@@ -298,28 +330,13 @@ k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
   int bad = 0;
   for (int64_t i = warp; i < n; i += nwarps) {
     T yi[S];
-#pragma unroll
-    for (int d = 0; d < S; ++d) yi[d] = Y[i * S + d];
+    load_point<T, S>(Y, i, yi);
     const int64_t beg = rowptr[i], end = rowptr[i + 1];
     T acc[S];
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = 0;
     T klr = 0;
-    for (int64_t k = beg + lane; k < end; k += 32) {
-      const int32_t j = __ldg(col + k);
-      const T p = __ldg(val + k);
-      T d2 = 0;
-      T df[S];
-#pragma unroll
-      for (int d = 0; d < S; ++d) {
-        df[d] = yi[d] - __ldg(Y + (int64_t)j * S + d);
-        d2 += df[d] * df[d];
-      }
-      const T w = p / ((T)1 + d2);
-#pragma unroll
-      for (int d = 0; d < S; ++d) acc[d] += w * df[d];
-      if (p > (T)0) klr += p * fast_log1p<T>(d2);
-    }
+    row_reduce<T, S, true>(col, val, Y, beg, end, lane, yi, acc, klr);
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
     kl += (double)klr;

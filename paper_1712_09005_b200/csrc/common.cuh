@@ -186,20 +186,35 @@ __device__ __forceinline__ double npy_floor_divide(double a, double b) {
 }
 
 // returns the cell (box) index along one dimension and fills w[0..p-1]
+// floor_divide(t, p) for t >= 0 and integer p in [2, 8]: numpy's divmod
+// computes mod = fmod(t, p) exactly, then (t - mod) = k p and k p / p = k
+// exactly, i.e. the floor of the EXACT quotient.  The correctly rounded IEEE
+// quotient RN(t/p) has the same floor: it could only differ if t < k p while
+// RN(t/p) = k.  But t <= k p - d, with d the double spacing below k p, and
+// d >= 2^floor(log2 p) u_k (u_k the spacing below k), so k - t/p >=
+// (2^floor(log2 p) / p) u_k > u_k / 2 for p in {3, 5, 6, 7} (powers of two
+// divide exactly): RN(t/p) <= k - u_k.  Hence floor(t / p) == numpy's t // p
+// without the costly fmod.  Negative t (out-of-bounds points) keeps numpy's
+// algorithm verbatim.
+__device__ __forceinline__ double floor_div_small(double t, int p) {
+  if (t >= 0.0) return floor(__ddiv_rn(t, (double)p));
+  return npy_floor_divide(t, (double)p);
+}
+
 __device__ __forceinline__ int box_weights(double x, double lo, double h, int n_int, int p,
                                            double* w) {
   double t = __ddiv_rn(__dsub_rn(x, lo), h);
-  double q = npy_floor_divide(t, (double)p);
+  double q = floor_div_small(t, p);
   long long c = (long long)q;
   if (c < 0) c = 0;
   if (c > n_int - 1) c = n_int - 1;
   double u = __dsub_rn(__dsub_rn(t, (double)(c * p)), 0.5);
   if (p == 3) {
-    // denominators 2, -1, 2 (nbody.py:176-180)
+    // denominators 2, -1, 2 (nbody.py:176-180); x/2 == x*0.5 and x/-1 == -x exactly
     double d0 = u, d1 = __dsub_rn(u, 1.0), d2 = __dsub_rn(u, 2.0);
-    w[0] = __ddiv_rn(__dmul_rn(d1, d2), 2.0);
-    w[1] = __ddiv_rn(__dmul_rn(d0, d2), -1.0);
-    w[2] = __ddiv_rn(__dmul_rn(d0, d1), 2.0);
+    w[0] = __dmul_rn(__dmul_rn(d1, d2), 0.5);
+    w[1] = -__dmul_rn(d0, d2);
+    w[2] = __dmul_rn(__dmul_rn(d0, d1), 0.5);
   } else {
     for (int j = 0; j < p; ++j) {
       double num = 1.0, den = 1.0;

@@ -24,7 +24,16 @@ struct FftPlan {
   int radix[24];
   int ns[24];      // Ns before the stage
   int stride[24];  // L / (Ns * R): twiddle index multiplier
+  unsigned mlr[24];  // ceil(2^32 / (L/R)): exact x / (L/R) = umulhi(x, mlr) for x < 2^32/(L/R)
+  unsigned mns[24];  // ceil(2^32 / Ns)
 };
+
+__host__ __device__ inline unsigned magic_div(unsigned d) {
+  return (unsigned)((((unsigned long long)1 << 32) + d - 1) / d);
+}
+
+// exact for x * d < 2^32 (here x < 16 L <= 2^17 and d <= 2^13)
+__device__ __forceinline__ unsigned fast_div(unsigned x, unsigned m) { return __umulhi(x, m); }
 
 __host__ __device__ inline bool is_smooth23(int L) {
   if (L < 1) return false;
@@ -55,7 +64,11 @@ __host__ __device__ inline void make_plan(FftPlan& pl, int L) {
   for (int i = 0; i < b; ++i) { pl.radix[s] = 3; pl.ns[s] = ns; ns *= 3; ++s; }
   pl.nstage = s;
   pl.L = L;
-  for (int i = 0; i < s; ++i) pl.stride[i] = L / (pl.ns[i] * pl.radix[i]);
+  for (int i = 0; i < s; ++i) {
+    pl.stride[i] = L / (pl.ns[i] * pl.radix[i]);
+    pl.mlr[i] = magic_div((unsigned)(L / pl.radix[i]));
+    pl.mns[i] = magic_div((unsigned)pl.ns[i]);
+  }
 }
 
 template <typename V>
@@ -107,14 +120,14 @@ __device__ __forceinline__ void dft3(V& a0, V& a1, V& a2, bool inv) {
 // One Stockham stage over `nsig` signals laid out at in[s*sig + i].
 template <typename V, typename T>
 __device__ __forceinline__ void fft_stage(const V* __restrict__ in, V* __restrict__ out, int L,
-                                          int R, int Ns, int tstride, int nsig, int sig,
-                                          const V* __restrict__ tw, bool inv) {
+                                          int R, int Ns, int tstride, unsigned mlr, unsigned mns,
+                                          int nsig, int sig, const V* __restrict__ tw, bool inv) {
   const int LR = L / R;
   const int total = nsig * LR;
   for (int t = threadIdx.x; t < total; t += blockDim.x) {
-    int s = t / LR;
+    int s = (int)fast_div((unsigned)t, mlr);
     int j = t - s * LR;
-    int k = j % Ns;
+    int k = j - (int)fast_div((unsigned)j, mns) * Ns;
     const V* src = in + (size_t)s * sig;
     V* dst = out + (size_t)s * sig;
     int base = (j - k) * R + k;  // (j/Ns)*Ns*R + k
@@ -160,7 +173,8 @@ __device__ V* block_fft(V* a, V* b, const FftPlan& pl, int nsig, int sig,
                         const V* __restrict__ tw, bool inv) {
   __syncthreads();
   for (int st = 0; st < pl.nstage; ++st) {
-    fft_stage<V, T>(a, b, pl.L, pl.radix[st], pl.ns[st], pl.stride[st], nsig, sig, tw, inv);
+    fft_stage<V, T>(a, b, pl.L, pl.radix[st], pl.ns[st], pl.stride[st], pl.mlr[st], pl.mns[st],
+                    nsig, sig, tw, inv);
     __syncthreads();
     V* t = a; a = b; b = t;
   }

@@ -472,23 +472,27 @@ __device__ __forceinline__ void kernel_pair(int i, int j, double hx, double hy, 
   k2 = (T)(base * base);
 }
 
-// Row stage.  Blocks [0, n): data rows (forward FFT of the packed pairs).
-// Blocks [n, 2n): kernel-spectrum rows.
+// Row stage.  merged=1: block x transforms data row x (the packed pairs) and
+// kernel-spectrum row x in one batched FFT.  merged=0 (large L): blocks [0, n)
+// do the data rows, blocks [n, 2n) the spectrum rows.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int pair0, int npair,
                typename C2<T>::type* __restrict__ F, typename C2<T>::type* __restrict__ Sbuf,
-               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl) {
+               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int merged) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   V* a = reinterpret_cast<V*>(smem_raw);
   const int L = g.L, n = g.n;
   const int H = L / 2 + 1;
-  if ((int)blockIdx.x < n) {
-    const int x = blockIdx.x;
-    const int ns = (MODE == MODE_TSNE) ? 2 : npair;
-    V* b = a + (size_t)ns * L;
-    for (int y = threadIdx.x; y < L; y += blockDim.x) {
+  const bool do_data = merged || (int)blockIdx.x < n;
+  const bool do_spec = merged || (int)blockIdx.x >= n;
+  const int x = (merged || (int)blockIdx.x < n) ? (int)blockIdx.x : (int)blockIdx.x - n;
+  const int ns = do_data ? ((MODE == MODE_TSNE) ? 2 : npair) : 0;
+  const int nsig = ns + (do_spec ? 1 : 0);
+  V* b = a + (size_t)nsig * L;
+  for (int y = threadIdx.x; y < L; y += blockDim.x) {
+    if (do_data) {
       if (MODE == MODE_TSNE) {
         V A = {0, 0}, B = {0, 0};
         if (y < n) {
@@ -514,100 +518,113 @@ k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int 
         }
       }
     }
-    V* r = block_fft<V, T>(a, b, pl, ns, L, tw, false);
-    for (int q = 0; q < ns; ++q)
-      for (int k = threadIdx.x; k < L; k += blockDim.x)
-        F[((size_t)q * n + x) * L + k] = r[(size_t)q * L + k];
-  } else {
-    const int i = blockIdx.x - n;
-    V* b = a + L;
-    for (int j = threadIdx.x; j < L; j += blockDim.x) {
+    if (do_spec) {
+      // first[x, j] = K((x hx)^2 + (j hy)^2), columns mirrored (nbody.py:272-281)
       V z = {0, 0};
-      int jj = (j < n) ? j : ((j > L - n) ? L - j : -1);
+      int jj = (y < n) ? y : ((y > L - n) ? L - y : -1);
       if (jj >= 0) {
         T k1, k2;
-        kernel_pair<T>(i, jj, g.h[0], g.h[1], k1, k2);
+        kernel_pair<T>(x, jj, g.h[0], g.h[1], k1, k2);
         z.x = k1;
         z.y = k2;
       }
-      a[j] = z;
+      a[(size_t)ns * L + y] = z;
     }
-    V* r = block_fft<V, T>(a, b, pl, 1, L, tw, false);
-    for (int k = threadIdx.x; k < H; k += blockDim.x) Sbuf[(size_t)i * H + k] = r[k];
   }
+  V* r = block_fft<V, T>(a, b, pl, nsig, L, tw, false);
+  for (int t = threadIdx.x; t < ns * L; t += blockDim.x) {
+    const int q = t / L, k = t - q * L;
+    F[((size_t)q * n + x) * L + k] = r[t];
+  }
+  if (do_spec)
+    for (int k = threadIdx.x; k < H; k += blockDim.x) Sbuf[(size_t)x * H + k] = r[(size_t)ns * L + k];
 }
 
-// Column stage: one block per column pair (ky, L-ky).  Builds the kernel
-// spectrum column, then forward FFT, multiply, Parseval (t-SNE), inverse FFT.
+// Column stage: one block per column pair (ky, L-ky).  One batched forward FFT
+// transforms the kernel-spectrum column (slot 0, rows mirrored as in the
+// circulant embedding, nbody.py:278-281) together with the first `batch` data
+// columns; then multiply (+ Parseval for t-SNE) and one batched inverse FFT.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restrict__ Sbuf,
        GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int kern,
-       int with_k1, double* __restrict__ zpart) {
+       int with_k1, int batch, double* __restrict__ zpart) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = g.L, n = g.n, H = L / 2 + 1;
   V* K = reinterpret_cast<V*>(smem_raw);
   V* a = K + L;
-  V* b = a + L;
+  V* b = a + (size_t)(batch + 1) * L;
   const int ky = blockIdx.x;
-  // spectrum column: rows mirrored (circulant embedding, nbody.py:278-281)
-  for (int i = threadIdx.x; i < L; i += blockDim.x) {
-    V z = {0, 0};
-    int ii = (i < n) ? i : ((i > L - n) ? L - i : -1);
-    if (ii >= 0) z = Sbuf[(size_t)ii * H + ky];
-    a[i] = z;
-  }
-  V* r = block_fft<V, T>(a, b, pl, 1, L, tw, false);
-  const T scale = (T)(1.0 / ((double)L * (double)L));
-  for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    V v = r[k];
-    V kk;
-    kk.x = v.x * scale;  // K1hat / L^2 (real)
-    kk.y = v.y * scale;  // K2hat / L^2 (real)
-    K[k] = kk;
-  }
-  double zacc = 0.0;
   const int ncolumns = (ky == 0 || 2 * ky == L) ? 1 : 2;
-  for (int cc = 0; cc < ncolumns; ++cc) {
-    const int col = (cc == 0) ? ky : L - ky;
-    for (int q = 0; q < npair; ++q) {
-      __syncthreads();
-      for (int x = threadIdx.x; x < L; x += blockDim.x) {
-        V z = {0, 0};
-        if (x < n) z = F[((size_t)q * n + x) * L + col];
-        a[x] = z;
+  const int nsig = ncolumns * npair;  // data signal s -> column s / npair, pair s % npair
+  const T scale = (T)(1.0 / ((double)L * (double)L));
+  double zacc = 0.0;
+  for (int s0 = 0; s0 < nsig; s0 += batch) {
+    const int ns = min(batch, nsig - s0);
+    const bool first = (s0 == 0);
+    __syncthreads();
+    // slot 0: spectrum column (first group only); slots 1..ns: data columns
+    for (int t = threadIdx.x; t < (ns + 1) * L; t += blockDim.x) {
+      const int slot = t / L, x = t - slot * L;
+      V z = {0, 0};
+      if (slot == 0) {
+        if (first) {
+          int ii = (x < n) ? x : ((x > L - n) ? L - x : -1);
+          if (ii >= 0) z = Sbuf[(size_t)ii * H + ky];
+        }
+      } else if (x < n) {
+        const int s = s0 + slot - 1;
+        const int col = (s / npair == 0) ? ky : L - ky;
+        z = F[((size_t)(s % npair) * n + x) * L + col];
       }
-      V* fr = block_fft<V, T>(a, b, pl, 1, L, tw, false);
-      V* other = (fr == a) ? b : a;
+      a[t] = z;
+    }
+    V* fr = block_fft<V, T>(a, b, pl, ns + 1, L, tw, false);
+    V* other = (fr == a) ? b : a;
+    if (first) {
       for (int k = threadIdx.x; k < L; k += blockDim.x) {
         V v = fr[k];
-        V kk = K[k];
-        V o;
-        if (MODE == MODE_TSNE) {
-          if (q == 0) {
+        V kk;
+        kk.x = v.x * scale;  // K1hat / L^2 (real)
+        kk.y = v.y * scale;  // K2hat / L^2 (real)
+        K[k] = kk;
+      }
+      __syncthreads();
+    }
+    for (int t = threadIdx.x; t < ns * L; t += blockDim.x) {
+      const int sl = t / L, k = t - sl * L;
+      const int q = (s0 + sl) % npair;
+      V v = fr[L + t];
+      V kk = K[k];
+      V o;
+      if (MODE == MODE_TSNE) {
+        if (q == 0) {
+          o.x = v.x * kk.y;
+          o.y = v.y * kk.y;
+        } else {
+          zacc += (double)kk.x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
+          if (with_k1) {  // v * (K2 + i K1)
+            o.x = v.x * kk.y - v.y * kk.x;
+            o.y = v.x * kk.x + v.y * kk.y;
+          } else {
             o.x = v.x * kk.y;
             o.y = v.y * kk.y;
-          } else {
-            zacc += (double)kk.x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
-            if (with_k1) {
-              // v * (K2 + i K1)
-              o.x = v.x * kk.y - v.y * kk.x;
-              o.y = v.x * kk.x + v.y * kk.y;
-            } else {
-              o.x = v.x * kk.y;
-              o.y = v.y * kk.y;
-            }
           }
-        } else {
-          T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
-          o.x = v.x * m;
-          o.y = v.y * m;
         }
-        fr[k] = o;
+      } else {
+        T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
+        o.x = v.x * m;
+        o.y = v.y * m;
       }
-      V* ir = block_fft<V, T>(fr, other, pl, 1, L, tw, true);
-      for (int x = threadIdx.x; x < n; x += blockDim.x) F[((size_t)q * n + x) * L + col] = ir[x];
+      fr[L + t] = o;
+    }
+    V* ir = block_fft<V, T>(fr + L, other + L, pl, ns, L, tw, true);
+    for (int t = threadIdx.x; t < ns * n; t += blockDim.x) {
+      const int sl = t / n, x = t - sl * n;
+      const int s = s0 + sl;
+      const int col = (s / npair == 0) ? ky : L - ky;
+      F[((size_t)(s % npair) * n + x) * L + col] = ir[(size_t)sl * L + x];
     }
   }
   if (MODE == MODE_TSNE) {
@@ -834,14 +851,20 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
   for (int pair0 = 0; pair0 < npair_total; pair0 += maxpair) {
     const int npair = std::min(maxpair, npair_total - pair0);
     // the spectrum rows are recomputed per pair group (one group for t-SNE)
-    size_t smem_r = sizeof(V) * (size_t)2 * npair * L;
+    const int nd = (MODE == MODE_TSNE) ? 2 : npair;
+    const int merged = sizeof(V) * (size_t)2 * (nd + 1) * L <= 113 * 1024 ? 1 : 0;
+    size_t smem_r = sizeof(V) * (size_t)2 * (merged ? nd + 1 : std::max(nd, 1)) * L;
     FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
-    k_rows_forward<T, MODE><<<2 * n, 256, smem_r, st>>>(accum, coeffs, ncol, pair0, npair, F, Sb, g,
-                                                        tw, pl);
+    k_rows_forward<T, MODE><<<merged ? n : 2 * n, 256, smem_r, st>>>(accum, coeffs, ncol, pair0,
+                                                                     npair, F, Sb, g, tw, pl, merged);
     FITSNE_CHECK_LAUNCH();
-    size_t smem_c = sizeof(V) * (size_t)3 * L;
+    // data signals per batched FFT: as many as fit two blocks per SM (<= 113 KB)
+    int batch = 4;
+    while (batch > 1 && sizeof(V) * (size_t)(3 + 2 * batch) * L > 113 * 1024) batch /= 2;
+    size_t smem_c = sizeof(V) * (size_t)(3 + 2 * batch) * L;
     FITSNE_TRY(set_smem<T>((const void*)k_cols<T, MODE>, smem_c));
-    k_cols<T, MODE><<<H, 256, smem_c, st>>>(F, Sb, g, tw, pl, npair, kern, with_k1 ? 1 : 0, zp);
+    k_cols<T, MODE><<<H, 256, smem_c, st>>>(F, Sb, g, tw, pl, npair, kern, with_k1 ? 1 : 0, batch,
+                                            zp);
     FITSNE_CHECK_LAUNCH();
     size_t smem_i = sizeof(V) * (size_t)2 * npair * L;
     FITSNE_TRY(set_smem<T>((const void*)k_rows_inverse<T, MODE>, smem_i));
