@@ -28,12 +28,16 @@ struct FftPlan {
   unsigned mns[24];  // ceil(2^32 / Ns)
 };
 
+// m = ceil(2^32 / d) for d >= 2; d == 1 is encoded as m = 0 (2^32 does not fit)
 __host__ __device__ inline unsigned magic_div(unsigned d) {
+  if (d <= 1) return 0u;
   return (unsigned)((((unsigned long long)1 << 32) + d - 1) / d);
 }
 
-// exact for x * d < 2^32 (here x < 16 L <= 2^17 and d <= 2^13)
-__device__ __forceinline__ unsigned fast_div(unsigned x, unsigned m) { return __umulhi(x, m); }
+// exact x / d for x * d < 2^32 (here x < 16 L <= 2^17 and d <= 2^13)
+__device__ __forceinline__ unsigned fast_div(unsigned x, unsigned m) {
+  return m ? __umulhi(x, m) : x;
+}
 
 __host__ __device__ inline bool is_smooth23(int L) {
   if (L < 1) return false;
