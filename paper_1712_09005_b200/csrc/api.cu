@@ -282,7 +282,7 @@ int fitsne_set_affinities(fitsne_ctx* ctx, const int64_t* rowptr, const int32_t*
 
 int fitsne_attractive(fitsne_ctx* ctx, const void* Y_full, void* out, void* stream) {
   CTX_CHECK(ctx);
-  return attractive(ctx, Y_full, nullptr, 1.0, out, false, false, S_(stream));
+  return attractive(ctx, Y_full, nullptr, 1.0, out, 0, false, S_(stream));
 }
 
 int fitsne_gradient(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, double* z_host,
@@ -301,8 +301,8 @@ int fitsne_gradient(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, do
   FITSNE_TRY(make_grid(ctx, Y, n, st));
   FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
   FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
-  FITSNE_TRY(gather_tsne(ctx, Y, n, ctx->forces.ptr, nullptr, nullptr, st));
-  FITSNE_TRY(attractive(ctx, Y, ctx->forces.ptr, alpha, grad, true, false, st));
+  // gather of F_rep fused into the SpMV warps (k_attract MODE 2)
+  FITSNE_TRY(attractive(ctx, Y, nullptr, alpha, grad, 2, false, st));
   if (z_host) {
     FITSNE_TRY(read_scalars(ctx, 1, st));
     *z_host = ctx->h_scal[0];
@@ -377,7 +377,7 @@ int fitsne_gather_tsne(fitsne_ctx* ctx, const void* Y_local, int64_t n_local, vo
 int fitsne_gradient_rows(fitsne_ctx* ctx, const void* Y_full, const void* forces_local, double alpha,
                          void* grad_local, void* stream) {
   CTX_CHECK(ctx);
-  return attractive(ctx, Y_full, forces_local, alpha, grad_local, true, false, S_(stream));
+  return attractive(ctx, Y_full, forces_local, alpha, grad_local, 1, false, S_(stream));
 }
 
 int fitsne_exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* charges, int ncharge,

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "interp.cuh"
 #include "internal.h"
 
 namespace fitsne {
@@ -88,15 +89,21 @@ __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, cons
 // warp-per-row CSR SpMV.  MODE 0: F_attr out.  MODE 1: gradient
 // 4 (alpha F_attr - F_rep).  KL: per-block partial of sum p log1p(d^2).
 // ---------------------------------------------------------------------------
-template <typename T, int S, int MODE, bool KL>
+// MODE 2: the repulsive force of row i is gathered in the same warp from the
+// potential grid (lanes 0..p^s-1 each interpolate one node), so F_rep never
+// round-trips through HBM.
+template <typename T, int S, int MODE, bool KL, int P>
 __global__ void __launch_bounds__(kBlock)
 k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
           const T* __restrict__ val, const T* __restrict__ Y, int64_t n_rows, int64_t row_begin,
-          const T* __restrict__ frep, T alpha, T* __restrict__ out, double* __restrict__ klpart) {
+          const T* __restrict__ frep, T alpha, T* __restrict__ out, double* __restrict__ klpart,
+          GridArgs g, const T* __restrict__ pot, const double* __restrict__ scal) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
   double kl = 0.0;
+  T Z = (T)1;
+  if (MODE == 2) Z = (T)scal[0];
   for (int64_t r = warp; r < n_rows; r += nwarps) {
     const int64_t i = row_begin + r;
     T yi[S];
@@ -105,16 +112,24 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     T acc[S];
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = 0;
+    T phi[4];
+    if (MODE == 2) warp_gather_partial<T, S, P>(yi, g, pot, lane, phi);
     T klr = 0;
     row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr);
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
+    if (MODE == 2) {
+      phi[0] = warp_sum(phi[0]);
+#pragma unroll
+      for (int d = 0; d < S; ++d) phi[1 + d] = warp_sum(phi[1 + d]);
+    }
     if (KL) kl += (double)klr;
     if (lane == 0) {
 #pragma unroll
       for (int d = 0; d < S; ++d) {
         if (MODE == 0) out[r * S + d] = acc[d];
-        else out[r * S + d] = (T)4 * (alpha * acc[d] - frep[r * S + d]);
+        else if (MODE == 1) out[r * S + d] = (T)4 * (alpha * acc[d] - frep[r * S + d]);
+        else out[r * S + d] = (T)4 * (alpha * acc[d] - frep_from_phi<T, S>(yi, phi, Z, d));
       }
     }
   }
@@ -159,34 +174,43 @@ template <typename T>
 static int launch_attract(fitsne_ctx* ctx, const T* Y, const T* frep, T alpha, T* out, int mode,
                           bool kl, double* klpart, int blocks, cudaStream_t st) {
   const T* val = (const T*)ctx->val;
-#define ATT(S, M, K)                                                                          \
-  k_attract<T, S, M, K><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, val, Y, ctx->n_rows, \
-                                                   ctx->row_begin, frep, alpha, out, klpart)
-  if (ctx->dims == 1) {
-    if (mode == 0) { if (kl) ATT(1, 0, true); else ATT(1, 0, false); }
-    else { if (kl) ATT(1, 1, true); else ATT(1, 1, false); }
-  } else {
-    if (mode == 0) { if (kl) ATT(2, 0, true); else ATT(2, 0, false); }
-    else { if (kl) ATT(2, 1, true); else ATT(2, 1, false); }
-  }
+  GridArgs g = grid_args(ctx->grid);
+  const T* pot = (const T*)ctx->pot.ptr;
+  const double* scal = (const double*)ctx->scal.ptr;
+#define ATT(S, M, K, P)                                                                           \
+  k_attract<T, S, M, K, P><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, val, Y, ctx->n_rows,  \
+                                                      ctx->row_begin, frep, alpha, out, klpart, g, \
+                                                      pot, scal)
+#define ATT_K(S, M, P) do { if (kl) ATT(S, M, true, P); else ATT(S, M, false, P); } while (0)
+#define ATT_M(S)                                                    \
+  do {                                                              \
+    if (mode == 0) ATT_K(S, 0, 3);                                  \
+    else if (mode == 1) ATT_K(S, 1, 3);                             \
+    else if (g.p == 3) ATT_K(S, 2, 3);                              \
+    else ATT_K(S, 2, 0);                                            \
+  } while (0)
+  if (ctx->dims == 1) ATT_M(1); else ATT_M(2);
+#undef ATT_M
+#undef ATT_K
 #undef ATT
   FITSNE_CHECK_LAUNCH();
   return FITSNE_OK;
 }
 
 int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double alpha, void* out,
-               bool grad, bool kl, cudaStream_t st) {
+               int mode, bool kl, cudaStream_t st) {
   if (!ctx->rowptr) { set_error("no affinities registered"); return FITSNE_EINVAL; }
+  if (mode == 2 && !ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
   FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
   FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
   double* part = (double*)ctx->part.ptr;
   const int blocks = attract_grid(ctx);
   if (ctx->dtype == FITSNE_F32)
     FITSNE_TRY(launch_attract<float>(ctx, (const float*)Yfull, (const float*)forces, (float)alpha,
-                                     (float*)out, grad ? 1 : 0, kl, part, blocks, st));
+                                     (float*)out, mode, kl, part, blocks, st));
   else
     FITSNE_TRY(launch_attract<double>(ctx, (const double*)Yfull, (const double*)forces, alpha,
-                                      (double*)out, grad ? 1 : 0, kl, part, blocks, st));
+                                      (double*)out, mode, kl, part, blocks, st));
   if (kl) {
     k_fold<<<1, 256, 0, st>>>(part, blocks, (double*)ctx->scal.ptr + 1);
     FITSNE_CHECK_LAUNCH();
@@ -198,7 +222,7 @@ int kl_sum(fitsne_ctx* ctx, const void* Yfull, cudaStream_t st) {
   // F_attr is computed as a by-product into scratch; only the KL partial is kept
   size_t es = dsize(ctx->dtype);
   FITSNE_TRY(ensure(ctx->gtmp, es * (size_t)std::max<int64_t>(ctx->n_rows, 1) * ctx->dims));
-  return attractive(ctx, Yfull, nullptr, 1.0, ctx->gtmp.ptr, false, true, st);
+  return attractive(ctx, Yfull, nullptr, 1.0, ctx->gtmp.ptr, 0, true, st);
 }
 
 // sum over stored p>0 of p log p and of p (fixed per affinity matrix)
@@ -317,15 +341,17 @@ int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gai
 // ---------------------------------------------------------------------------
 // fused iteration: SpMV + KL partial + gradient + update + next-Y finiteness
 // ---------------------------------------------------------------------------
-template <typename T, int S>
+template <typename T, int S, int P>
 __global__ void __launch_bounds__(kBlock)
 k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-          const T* __restrict__ val, const T* __restrict__ Y, int64_t n, const T* __restrict__ frep,
+          const T* __restrict__ val, const T* __restrict__ Y, int64_t n, GridArgs gr,
+          const T* __restrict__ pot, const double* __restrict__ scal,
           T alpha, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel, T* __restrict__ gains,
           double* __restrict__ klpart, int32_t* __restrict__ status) {
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const T Z = (T)scal[0];
   double kl = 0.0;
   int bad = 0;
   for (int64_t i = warp; i < n; i += nwarps) {
@@ -335,10 +361,15 @@ k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     T acc[S];
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = 0;
+    T phi[4];
+    warp_gather_partial<T, S, P>(yi, gr, pot, lane, phi);
     T klr = 0;
     row_reduce<T, S, true>(col, val, Y, beg, end, lane, yi, acc, klr);
 #pragma unroll
     for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
+    phi[0] = warp_sum(phi[0]);
+#pragma unroll
+    for (int d = 0; d < S; ++d) phi[1 + d] = warp_sum(phi[1 + d]);
     kl += (double)klr;
     if (lane < S) {
       const int d = lane;
@@ -346,7 +377,7 @@ k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
 #pragma unroll
       for (int e = 1; e < S; ++e) if (d == e) a = acc[e];
       const int64_t o = i * S + d;
-      T g = (T)4 * (alpha * a - frep[o]);
+      T g = (T)4 * (alpha * a - frep_from_phi<T, S>(yi, phi, Z, d));
       if (!isfinite(g)) bad |= 1;
       T v = vel[o], gn = gains[o];
       bool agree = npsign(g) == npsign(v);
@@ -395,19 +426,22 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
   FITSNE_TRY(make_grid(ctx, Yin, n, st));
   FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
   FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
-  FITSNE_TRY(gather_tsne(ctx, Yin, n, ctx->forces.ptr, nullptr, nullptr, st));
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
   FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
   double* part = (double*)ctx->part.ptr;
   int blocks = attract_grid(ctx);
-#define IT(T, S)                                                                                  \
-  k_iterate<T, S><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, (const T*)ctx->val,           \
-                                             (const T*)Yin, n, (const T*)ctx->forces.ptr, (T)alpha, \
-                                             (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains,    \
-                                             part, status_dev)
+  GridArgs gr = grid_args(ctx->grid);
+#define IT2(T, S, P)                                                                              \
+  k_iterate<T, S, P><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, (const T*)ctx->val,        \
+                                                (const T*)Yin, n, gr, (const T*)ctx->pot.ptr,     \
+                                                (const double*)ctx->scal.ptr, (T)alpha,           \
+                                                (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, \
+                                                part, status_dev)
+#define IT(T, S) do { if (gr.p == 3) IT2(T, S, 3); else IT2(T, S, 0); } while (0)
   if (ctx->dtype == FITSNE_F32) { if (ctx->dims == 1) IT(float, 1); else IT(float, 2); }
   else { if (ctx->dims == 1) IT(double, 1); else IT(double, 2); }
 #undef IT
+#undef IT2
   FITSNE_CHECK_LAUNCH();
   if (kl_dev) {
     k_kl_final<<<1, 256, 0, st>>>(part, blocks, (const double*)ctx->scal.ptr, ctx->plogp, ctx->psum,

@@ -1,0 +1,105 @@
+// Per-point interpolation helpers shared by the spread, gather and fused
+// SpMV kernels (nbody.py:201-230, 344-350; optimizer.py:203-210, 244).
+#pragma once
+
+#include "common.cuh"
+
+namespace fitsne {
+
+template <typename T, int S>
+struct PointInterp {
+  int cell[S];
+  double w[S][kMaxP];
+};
+
+template <typename T, int S>
+__device__ __forceinline__ void interp_point(const T* __restrict__ Y, int64_t i, const GridArgs& g,
+                                             PointInterp<T, S>& pi, double* y) {
+#pragma unroll
+  for (int d = 0; d < S; ++d) {
+    y[d] = (double)Y[i * S + d];
+    pi.cell[d] = box_weights(y[d], g.lo[d], g.h[d], g.n_int, g.p, pi.w[d]);
+  }
+}
+
+// one 4-slot potential record (float4 / 2 x double2)
+template <typename T>
+__device__ __forceinline__ void load_slots(const T* p, T (&v)[4]) {
+  if constexpr (sizeof(T) == 4) {
+    float4 f = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
+  } else {
+    double2 a = __ldg(reinterpret_cast<const double2*>(p));
+    double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
+    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
+  }
+}
+
+// Warp-cooperative gather for point i: lane m < p^S interpolates node m of
+// the point's box; returns this lane's partial potentials phi[0..3] (to be
+// summed over the warp).  All lanes must call it (no divergence required).
+// P = 3: compile-time fast path (registers only); P = 0: any p in [2, 8].
+template <typename T, int S, int P>
+__device__ __forceinline__ void warp_gather_partial(const T (&yi)[S], const GridArgs& g,
+                                                    const T* __restrict__ pot, int lane,
+                                                    T (&phi)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) phi[c] = 0;
+  if constexpr (P == 3) {
+    // p = 3 fast path: everything in registers (no runtime-indexed arrays)
+    const int cnt = (S == 1) ? 3 : 9;
+    if (lane >= cnt) return;
+    const int a = (S == 1) ? lane : lane / 3, b = (S == 1) ? 0 : lane - (lane / 3) * 3;
+    double w0[3], w1[3];
+    const int c0 = box_weights((double)yi[0], g.lo[0], g.h[0], g.n_int, 3, w0);
+    int c1 = 0;
+    if (S == 2) c1 = box_weights((double)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.n_int, 3, w1);
+    const double wa = (a == 0) ? w0[0] : ((a == 1) ? w0[1] : w0[2]);
+    double wt = wa;
+    int64_t node = (int64_t)c0 * 3 + a;
+    if (S == 2) {
+      wt = wa * ((b == 0) ? w1[0] : ((b == 1) ? w1[1] : w1[2]));
+      node = node * g.n + (int64_t)c1 * 3 + b;
+    }
+    T v[4];
+    load_slots<T>(pot + node * kNodeSlots, v);
+    const T tw = (T)wt;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) phi[c] = v[c] * tw;
+    return;
+  } else {
+  const int p = g.p;
+  const int cnt = (S == 1) ? p : p * p;
+  if (lane >= cnt && cnt <= 32) return;
+  double w[S][kMaxP];
+  int cell[S];
+#pragma unroll
+  for (int d = 0; d < S; ++d) cell[d] = box_weights((double)yi[d], g.lo[d], g.h[d], g.n_int, p, w[d]);
+  for (int m = lane; m < cnt; m += 32) {
+    int64_t node;
+    double wt;
+    if (S == 1) {
+      node = (int64_t)cell[0] * p + m;
+      wt = w[0][m];
+    } else {
+      const int a = m / p, b = m - (m / p) * p;
+      node = ((int64_t)cell[0] * p + a) * g.n + (int64_t)cell[1] * p + b;
+      wt = w[0][a] * w[S - 1][b];
+    }
+    T v[4];
+    load_slots<T>(pot + node * kNodeSlots, v);
+    const T tw = (T)wt;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) phi[c] += v[c] * tw;
+  }
+  }
+}
+
+// F_rep_i = (y_i (phi_0 - 1) - (phi_{1+d} - y_d)) / Z  (optimizer.py:206-210, 244)
+template <typename T, int S>
+__device__ __forceinline__ T frep_from_phi(const T (&yi)[S], const T (&phi)[4], T Z, int d) {
+  const T h4 = phi[0] - (T)1;
+  return (yi[d] * h4 - (phi[1 + d] - yi[d])) / Z;
+}
+
+}  // namespace fitsne

@@ -20,6 +20,7 @@
 
 #include "common.cuh"
 #include "fft.cuh"
+#include "interp.cuh"
 #include "internal.h"
 
 namespace fitsne {
@@ -241,22 +242,6 @@ int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
 // =============================================================================
 // a2/a3: box assignment + Lagrange weights, spreading
 // =============================================================================
-template <typename T, int S>
-struct PointInterp {
-  int cell[S];
-  double w[S][kMaxP];
-};
-
-template <typename T, int S>
-__device__ __forceinline__ void interp_point(const T* __restrict__ Y, int64_t i, const GridArgs& g,
-                                             PointInterp<T, S>& pi, double* y) {
-#pragma unroll
-  for (int d = 0; d < S; ++d) {
-    y[d] = (double)Y[i * S + d];
-    pi.cell[d] = box_weights(y[d], g.lo[d], g.h[d], g.n_int, g.p, pi.w[d]);
-  }
-}
-
 // t-SNE charges (1, y_0[, y_1]) of each point into 4-slot node records.
 template <typename T, int S, int P>
 __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T* __restrict__ acc) {
@@ -912,18 +897,6 @@ int matvec_general(fitsne_ctx* ctx, int kernel, const void* coeffs, int ncol, vo
 //   k1 = phi_K1(1) - 1, k2[:, c] = phi_K2(y_c) - y_c, k2[:, s] = phi_K2(1) - 1
 //   F_rep = (y * k2[:, s] - k2[:, :s]) / Z           (optimizer.py:206-210, 244)
 // =============================================================================
-template <typename T>
-__device__ __forceinline__ void load_slots(const T* p, T (&v)[4]) {
-  if constexpr (sizeof(T) == 4) {
-    float4 f = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = f.x; v[1] = f.y; v[2] = f.z; v[3] = f.w;
-  } else {
-    double2 a = __ldg(reinterpret_cast<const double2*>(p));
-    double2 b = __ldg(reinterpret_cast<const double2*>(p) + 1);
-    v[0] = a.x; v[1] = a.y; v[2] = b.x; v[3] = b.y;
-  }
-}
-
 template <typename T, int S, int P>
 __global__ void k_gather_tsne(const T* __restrict__ Y, int64_t n, GridArgs g,
                               const T* __restrict__ pot, const double* __restrict__ scal,
