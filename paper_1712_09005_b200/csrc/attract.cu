@@ -93,45 +93,87 @@ __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, cons
 // potential grid (lanes 0..p^s-1 each interpolate one node), so F_rep never
 // round-trips through HBM.
 template <typename T, int S, int MODE, bool KL, int P>
-__global__ void __launch_bounds__(kBlock)
+__global__ void __launch_bounds__(kBlock, 6)
 k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
           const T* __restrict__ val, const T* __restrict__ Y, int64_t n_rows, int64_t row_begin,
           const T* __restrict__ frep, T alpha, T* __restrict__ out, double* __restrict__ klpart,
           GridArgs g, const T* __restrict__ pot, const double* __restrict__ scal) {
+  // Each warp owns tiles of 32 consecutive rows.  Per-row scalar work (y_i,
+  // row bounds, and for MODE 2 the p^s-node gather of F_rep) is done one row
+  // per lane with coalesced loads; the CSR reduction then walks the tile's
+  // rows one at a time with the whole warp, and lane m keeps row m's result.
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (n_rows + 31) >> 5;
+  // per-warp staging of the tile's row scalars (keeps them out of registers)
+  __shared__ int64_t s_rb[kBlock], s_re[kBlock];
+  __shared__ T s_y[kBlock * S], s_acc[kBlock * S];
+  const int wbase = threadIdx.x & ~31;
   double kl = 0.0;
   T Z = (T)1;
   if (MODE == 2) Z = (T)scal[0];
-  for (int64_t r = warp; r < n_rows; r += nwarps) {
-    const int64_t i = row_begin + r;
-    T yi[S];
-    load_point<T, S>(Y, i, yi);
-    const int64_t beg = rowptr[r], end = rowptr[r + 1];
-    T acc[S];
+  for (int64_t t = warp; t < ntiles; t += nwarps) {
+    const int64_t r_mine = t * 32 + lane;
+    const bool valid = r_mine < n_rows;
+    {
+      T ym[S];
 #pragma unroll
-    for (int d = 0; d < S; ++d) acc[d] = 0;
-    T phi[4];
-    if (MODE == 2) warp_gather_partial<T, S, P>(yi, g, pot, lane, phi);
-    T klr = 0;
-    row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr);
+      for (int d = 0; d < S; ++d) ym[d] = 0;
+      int64_t rb = 0, re = 0;
+      if (valid) {
+        load_point<T, S>(Y, row_begin + r_mine, ym);
+        rb = rowptr[r_mine];
+        re = rowptr[r_mine + 1];
+      }
+      s_rb[threadIdx.x] = rb;
+      s_re[threadIdx.x] = re;
 #pragma unroll
-    for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
-    if (MODE == 2) {
-      phi[0] = warp_sum(phi[0]);
-#pragma unroll
-      for (int d = 0; d < S; ++d) phi[1 + d] = warp_sum(phi[1 + d]);
+      for (int d = 0; d < S; ++d) s_y[threadIdx.x * S + d] = ym[d];
     }
-    if (KL) kl += (double)klr;
-    if (lane == 0) {
+    __syncwarp();
+    const int mcount = (n_rows - t * 32 < 32) ? (int)(n_rows - t * 32) : 32;
+    for (int m = 0; m < mcount; ++m) {
+      T yi[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) yi[d] = s_y[(wbase + m) * S + d];
+      const int64_t beg = s_rb[wbase + m];
+      const int64_t end = s_re[wbase + m];
+      T acc[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) acc[d] = 0;
+      T klr = 0;
+      row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr);
+#pragma unroll
+      for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
+      if (lane == m) {
+#pragma unroll
+        for (int d = 0; d < S; ++d) s_acc[threadIdx.x * S + d] = acc[d];
+      }
+      if (KL) kl += (double)klr;
+    }
+    __syncwarp();
+    if (valid) {
+      T ym[S], fr[S];
+#pragma unroll
+      for (int d = 0; d < S; ++d) { ym[d] = s_y[threadIdx.x * S + d]; fr[d] = 0; }
+      if (MODE == 1) {
+#pragma unroll
+        for (int d = 0; d < S; ++d) fr[d] = frep[r_mine * S + d];
+      } else if (MODE == 2) {
+        T phi[4];
+        point_gather<T, S, P>(ym, g, pot, phi);
+#pragma unroll
+        for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d);
+      }
 #pragma unroll
       for (int d = 0; d < S; ++d) {
-        if (MODE == 0) out[r * S + d] = acc[d];
-        else if (MODE == 1) out[r * S + d] = (T)4 * (alpha * acc[d] - frep[r * S + d]);
-        else out[r * S + d] = (T)4 * (alpha * acc[d] - frep_from_phi<T, S>(yi, phi, Z, d));
+        const T res = s_acc[threadIdx.x * S + d];
+        if (MODE == 0) out[r_mine * S + d] = res;
+        else out[r_mine * S + d] = (T)4 * (alpha * res - fr[d]);
       }
     }
+    __syncwarp();
   }
   if (KL) {
     __shared__ double red[kBlock / 32];
@@ -161,12 +203,12 @@ __global__ void k_fold(const double* __restrict__ part, int n, double* __restric
   }
 }
 
+// one 32-row tile per warp (the hardware scheduler balances the tiles)
 static int attract_grid(fitsne_ctx* ctx) {
-  int64_t warps_needed = ctx->n_rows;
-  int64_t blocks = (warps_needed * 32 + kBlock - 1) / kBlock;
-  int64_t cap = (int64_t)ctx->num_sms * 16;  // persistent-ish: 16 blocks of 8 warps per SM
-  if (blocks > cap) blocks = cap;
+  int64_t tiles = (ctx->n_rows + 31) / 32;
+  int64_t blocks = (tiles + kBlock / 32 - 1) / (kBlock / 32);
   if (blocks < 1) blocks = 1;
+  if (blocks > (1LL << 30)) blocks = (1LL << 30);
   return (int)blocks;
 }
 
@@ -201,10 +243,10 @@ int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double al
                int mode, bool kl, cudaStream_t st) {
   if (!ctx->rowptr) { set_error("no affinities registered"); return FITSNE_EINVAL; }
   if (mode == 2 && !ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
-  FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
+  const int blocks = attract_grid(ctx);
+  FITSNE_TRY(ensure(ctx->part, sizeof(double) * ((size_t)blocks + (size_t)ctx->num_sms * 16 + 64)));
   FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
   double* part = (double*)ctx->part.ptr;
-  const int blocks = attract_grid(ctx);
   if (ctx->dtype == FITSNE_F32)
     FITSNE_TRY(launch_attract<float>(ctx, (const float*)Yfull, (const float*)forces, (float)alpha,
                                      (float*)out, mode, kl, part, blocks, st));
@@ -339,7 +381,7 @@ int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gai
 }
 
 // ---------------------------------------------------------------------------
-// fused iteration: SpMV + KL partial + gradient + update + next-Y finiteness
+// fused iteration: gather + SpMV + KL partial + gradient + update + next-Y finiteness
 // ---------------------------------------------------------------------------
 template <typename T, int S, int P>
 __global__ void __launch_bounds__(kBlock)
@@ -351,43 +393,61 @@ k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
   const int lane = threadIdx.x & 31;
   const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  const int64_t ntiles = (n + 31) >> 5;
   const T Z = (T)scal[0];
   double kl = 0.0;
   int bad = 0;
-  for (int64_t i = warp; i < n; i += nwarps) {
-    T yi[S];
-    load_point<T, S>(Y, i, yi);
-    const int64_t beg = rowptr[i], end = rowptr[i + 1];
-    T acc[S];
+  for (int64_t t = warp; t < ntiles; t += nwarps) {
+    const int64_t i_mine = t * 32 + lane;
+    const bool valid = i_mine < n;
+    T ym[S], fr[S], res[S];
 #pragma unroll
-    for (int d = 0; d < S; ++d) acc[d] = 0;
-    T phi[4];
-    warp_gather_partial<T, S, P>(yi, gr, pot, lane, phi);
-    T klr = 0;
-    row_reduce<T, S, true>(col, val, Y, beg, end, lane, yi, acc, klr);
+    for (int d = 0; d < S; ++d) { ym[d] = 0; fr[d] = 0; res[d] = 0; }
+    int64_t rb = 0, re = 0;
+    if (valid) {
+      load_point<T, S>(Y, i_mine, ym);
+      rb = rowptr[i_mine];
+      re = rowptr[i_mine + 1];
+      T phi[4];
+      point_gather<T, S, P>(ym, gr, pot, phi);
 #pragma unroll
-    for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
-    phi[0] = warp_sum(phi[0]);
+      for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d);
+    }
+    const int mcount = (n - t * 32 < 32) ? (int)(n - t * 32) : 32;
+    for (int m = 0; m < mcount; ++m) {
+      T yi[S];
 #pragma unroll
-    for (int d = 0; d < S; ++d) phi[1 + d] = warp_sum(phi[1 + d]);
-    kl += (double)klr;
-    if (lane < S) {
-      const int d = lane;
-      T a = acc[0];
+      for (int d = 0; d < S; ++d) yi[d] = __shfl_sync(0xffffffffu, ym[d], m);
+      const int64_t beg = __shfl_sync(0xffffffffu, rb, m);
+      const int64_t end = __shfl_sync(0xffffffffu, re, m);
+      T acc[S];
 #pragma unroll
-      for (int e = 1; e < S; ++e) if (d == e) a = acc[e];
-      const int64_t o = i * S + d;
-      T g = (T)4 * (alpha * a - frep_from_phi<T, S>(yi, phi, Z, d));
-      if (!isfinite(g)) bad |= 1;
-      T v = vel[o], gn = gains[o];
-      bool agree = npsign(g) == npsign(v);
-      T vn = momentum * v - lr * gn * g;
-      T ynew = yi[d] + vn;
-      if (!isfinite(ynew)) bad |= 2;
-      vel[o] = vn;
-      Yout[o] = ynew;
-      T ng = agree ? gn * (T)0.8 : gn + (T)0.2;
-      gains[o] = ng < (T)0.01 ? (T)0.01 : ng;
+      for (int d = 0; d < S; ++d) acc[d] = 0;
+      T klr = 0;
+      row_reduce<T, S, true>(col, val, Y, beg, end, lane, yi, acc, klr);
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        acc[d] = warp_sum(acc[d]);
+        if (lane == m) res[d] = acc[d];
+      }
+      kl += (double)klr;
+    }
+    if (valid) {
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        const int64_t o = i_mine * S + d;
+        T g = (T)4 * (alpha * res[d] - fr[d]);
+        if (!isfinite(g)) bad |= 1;
+        T v = vel[o], gn = gains[o];
+        bool agree = npsign(g) == npsign(v);
+        T vn = momentum * v - lr * gn * g;
+        T ynew = ym[d] + vn;
+        if (!isfinite(ynew)) bad |= 2;
+        vel[o] = vn;
+        Yout[o] = ynew;
+        T ng = agree ? gn * (T)0.8 : gn + (T)0.2;
+        gains[o] = ng < (T)0.01 ? (T)0.01 : ng;
+      }
     }
   }
   __shared__ double red[kBlock / 32];
@@ -421,15 +481,13 @@ __global__ void k_kl_final(const double* __restrict__ part, int n, const double*
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
                   double momentum, double lr, double* kl_dev, int32_t* status_dev, cudaStream_t st) {
   const int64_t n = ctx->n_total;
-  size_t es = dsize(ctx->dtype);
-  FITSNE_TRY(ensure(ctx->forces, es * (size_t)n * ctx->dims));
   FITSNE_TRY(make_grid(ctx, Yin, n, st));
   FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
   FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
-  FITSNE_TRY(ensure(ctx->part, sizeof(double) * (size_t)ctx->num_sms * 16 + 64));
-  double* part = (double*)ctx->part.ptr;
   int blocks = attract_grid(ctx);
+  FITSNE_TRY(ensure(ctx->part, sizeof(double) * ((size_t)blocks + (size_t)ctx->num_sms * 16 + 64)));
+  double* part = (double*)ctx->part.ptr;
   GridArgs gr = grid_args(ctx->grid);
 #define IT2(T, S, P)                                                                              \
   k_iterate<T, S, P><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, (const T*)ctx->val,        \

@@ -47,6 +47,9 @@ struct GridArgs {
   double lo[2];
   double hi[2];
   double h[2];
+  float lo_f[2];    // fp32 copies for the guarded fp32 box estimate
+  float invh_f[2];
+  float guard[2];   // margin in units of t/p (>= 0.5 disables the fast path)
   int dims;
   int n_int;
   int p;
@@ -60,6 +63,17 @@ inline GridArgs grid_args(const fitsne_grid& g) {
     a.lo[d] = g.lo[d];
     a.hi[d] = g.hi[d];
     a.h[d] = g.spacing[d];
+    a.lo_f[d] = (float)g.lo[d];
+    a.invh_f[d] = g.spacing[d] > 0 ? (float)(1.0 / g.spacing[d]) : 0.f;
+    // |t32 - t| <= (|lo| 2^-24 + |x - lo| 2^-24) / h + t 2^-22 (rounding of
+    // lo, of x - lo, of 1/h and of the product); bound it with x - lo <= span
+    double span = g.hi[d] - g.lo[d];
+    double lo_abs = g.lo[d] < 0 ? -g.lo[d] : g.lo[d];
+    double et = g.spacing[d] > 0
+                    ? (lo_abs + span) * 5.96e-8 / g.spacing[d] + (double)g.nodes_per_dim * 2.4e-7
+                    : 1.0;
+    double gd = 4.0 * et / (g.points_per_interval > 0 ? g.points_per_interval : 3) + 1e-3;
+    a.guard[d] = gd > 0.5 ? 0.5f : (float)gd;
   }
   a.dims = g.dims;
   a.n_int = g.n_intervals;
@@ -230,6 +244,36 @@ __device__ __forceinline__ int box_weights(double x, double lo, double h, int n_
     }
   }
   return (int)c;
+}
+
+// fp32 fast path for p = 3 (fp32 mode): the box index must stay bit-exact,
+// the weights only need fp32 accuracy.  t is estimated in fp32; `guard` (set
+// by grid_args from a rounding-error bound, >= 1e-3) is a safe margin in
+// units of t/3: when t/3 lies within it of an integer the exact fp64 path
+// decides the cell.  Returns the cell and the three fp32 Lagrange weights.
+__device__ __forceinline__ int box_weights3_f32(float x, double lo, double h, float lo_f,
+                                                float invh_f, float guard, int n_int, float* w) {
+  const float t = (x - lo_f) * invh_f;
+  const float r = t * (1.0f / 3.0f);
+  const float q = floorf(r);
+  const float fr = r - q;
+  int c;
+  float u;
+  if (fr > guard && fr < 1.0f - guard && t >= 0.0f) {
+    c = (int)q;
+    if (c > n_int - 1) c = n_int - 1;
+    u = t - (float)(3 * c) - 0.5f;
+  } else {
+    double wd[3];
+    c = box_weights((double)x, lo, h, n_int, 3, wd);
+    double td = __ddiv_rn(__dsub_rn((double)x, lo), h);
+    u = (float)__dsub_rn(__dsub_rn(td, (double)(c * 3)), 0.5);
+  }
+  const float d1 = u - 1.0f, d2 = u - 2.0f;
+  w[0] = 0.5f * d1 * d2;
+  w[1] = -u * d2;
+  w[2] = 0.5f * u * d1;
+  return c;
 }
 
 // block-wide reductions ------------------------------------------------------

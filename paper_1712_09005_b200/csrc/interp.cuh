@@ -2,6 +2,8 @@
 // SpMV kernels (nbody.py:201-230, 344-350; optimizer.py:203-210, 244).
 #pragma once
 
+#include <type_traits>
+
 #include "common.cuh"
 
 namespace fitsne {
@@ -50,12 +52,21 @@ __device__ __forceinline__ void warp_gather_partial(const T (&yi)[S], const Grid
     const int cnt = (S == 1) ? 3 : 9;
     if (lane >= cnt) return;
     const int a = (S == 1) ? lane : lane / 3, b = (S == 1) ? 0 : lane - (lane / 3) * 3;
-    double w0[3], w1[3];
-    const int c0 = box_weights((double)yi[0], g.lo[0], g.h[0], g.n_int, 3, w0);
-    int c1 = 0;
-    if (S == 2) c1 = box_weights((double)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.n_int, 3, w1);
-    const double wa = (a == 0) ? w0[0] : ((a == 1) ? w0[1] : w0[2]);
-    double wt = wa;
+    using W = typename std::conditional<sizeof(T) == 4, float, double>::type;
+    W w0[3], w1[3];
+    int c0, c1 = 0;
+    if constexpr (sizeof(T) == 4) {
+      c0 = box_weights3_f32((float)yi[0], g.lo[0], g.h[0], g.lo_f[0], g.invh_f[0], g.guard[0],
+                            g.n_int, w0);
+      if (S == 2)
+        c1 = box_weights3_f32((float)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.lo_f[S - 1],
+                              g.invh_f[S - 1], g.guard[S - 1], g.n_int, w1);
+    } else {
+      c0 = box_weights((double)yi[0], g.lo[0], g.h[0], g.n_int, 3, w0);
+      if (S == 2) c1 = box_weights((double)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.n_int, 3, w1);
+    }
+    const W wa = (a == 0) ? w0[0] : ((a == 1) ? w0[1] : w0[2]);
+    W wt = wa;
     int64_t node = (int64_t)c0 * 3 + a;
     if (S == 2) {
       wt = wa * ((b == 0) ? w1[0] : ((b == 1) ? w1[1] : w1[2]));
@@ -92,6 +103,53 @@ __device__ __forceinline__ void warp_gather_partial(const T (&yi)[S], const Grid
 #pragma unroll
     for (int c = 0; c < 4; ++c) phi[c] += v[c] * tw;
   }
+  }
+}
+
+// Thread-per-point gather of the 4 potentials of point y (all p^S nodes).
+template <typename T, int S, int P>
+__device__ __forceinline__ void point_gather(const T (&yi)[S], const GridArgs& g,
+                                             const T* __restrict__ pot, T (&phi)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) phi[c] = 0;
+  if constexpr (P == 3 && sizeof(T) == 4) {
+    float w0[3], w1[3] = {1.f, 0.f, 0.f};
+    const int c0 = box_weights3_f32((float)yi[0], g.lo[0], g.h[0], g.lo_f[0], g.invh_f[0],
+                                    g.guard[0], g.n_int, w0);
+    int c1 = 0;
+    if (S == 2)
+      c1 = box_weights3_f32((float)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.lo_f[S - 1],
+                            g.invh_f[S - 1], g.guard[S - 1], g.n_int, w1);
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int64_t rowbase = (S == 1) ? ((int64_t)c0 * 3 + a)
+                                       : (((int64_t)c0 * 3 + a) * g.n + (int64_t)c1 * 3);
+#pragma unroll
+      for (int b = 0; b < ((S == 1) ? 1 : 3); ++b) {
+        T v[4];
+        load_slots<T>(pot + (rowbase + b) * kNodeSlots, v);
+        const float wt = w0[a] * w1[b];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) phi[c] += v[c] * wt;
+      }
+    }
+  } else {
+    const int p = (P > 0) ? P : g.p;
+    double w[S][kMaxP];
+    int cell[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) cell[d] = box_weights((double)yi[d], g.lo[d], g.h[d], g.n_int, p, w[d]);
+    const int cnt = (S == 1) ? p : p * p;
+    for (int m = 0; m < cnt; ++m) {
+      const int a = (S == 1) ? m : m / p, b = (S == 1) ? 0 : m - (m / p) * p;
+      const int64_t node = (S == 1) ? ((int64_t)cell[0] * p + a)
+                                    : (((int64_t)cell[0] * p + a) * g.n + (int64_t)cell[1] * p + b);
+      const double wt = (S == 1) ? w[0][a] : w[0][a] * w[S - 1][b];
+      T v[4];
+      load_slots<T>(pot + node * kNodeSlots, v);
+#pragma unroll
+      for (int c = 0; c < 4; ++c) phi[c] += v[c] * (T)wt;
+    }
   }
 }
 

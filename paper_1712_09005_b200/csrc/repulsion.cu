@@ -247,6 +247,27 @@ template <typename T, int S, int P>
 __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T* __restrict__ acc) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  if constexpr (sizeof(T) == 4 && P == 3 && S == 2) {
+    // fp32 mode, p = 3: guarded fp32 box estimate (exact indices), fp32 weights
+    const float2 yy = __ldg(reinterpret_cast<const float2*>(Y) + i);
+    float wx[3], wy[3];
+    const int cx = box_weights3_f32(yy.x, g.lo[0], g.h[0], g.lo_f[0], g.invh_f[0], g.guard[0],
+                                    g.n_int, wx);
+    const int cy = box_weights3_f32(yy.y, g.lo[1], g.h[1], g.lo_f[1], g.invh_f[1], g.guard[1],
+                                    g.n_int, wy);
+    const int64_t nn = g.n;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      const int64_t rowbase = ((int64_t)cx * 3 + a) * nn + (int64_t)cy * 3;
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const float w = wx[a] * wy[b];
+        atomicAdd(reinterpret_cast<float4*>(acc + (rowbase + b) * kNodeSlots),
+                  make_float4(w, w * yy.x, w * yy.y, 0.f));
+      }
+    }
+    return;
+  }
   const int p = (P > 0) ? P : g.p;
   PointInterp<T, S> pi;
   double y[S];
