@@ -78,6 +78,13 @@ int fitsne_destroy(fitsne_ctx* ctx);
 int fitsne_set_interp(fitsne_ctx* ctx, int points_per_interval, int min_intervals,
                       double intervals_per_integer);
 
+/* Implementation switches (no reference counterpart; for A/B tests).
+ *   FITSNE_OPT_SORTED_SPREAD: 0 = one atomic per point and node; 1 (default)
+ *   = box-sorted segmented spread (p = 3) when the points crowd into few boxes
+ *   (>= 128 points per occupied box); 2 = always box-sorted. */
+enum fitsne_option { FITSNE_OPT_SORTED_SPREAD = 1 };
+int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
+
 /* --- a1: make_grid (nbody.py:118-150).  Device bbox reduction + fp64 grid
  * formulas; the grid is copied to *grid_host (one host sync) and kept as the
  * context's current grid. */

@@ -99,14 +99,35 @@ def as_points(x, dims=None):
     return x
 
 
-def output(t: torch.Tensor, device_result, like=None):
-    """Device tensor for device callers; a CPU tensor (compute dtype, via a
-    pinned staging copy) for CPU-tensor callers; float64 numpy otherwise."""
+_pinned: dict = {}
+
+
+def _pinned_buffer(shape, dtype):
+    """Reusable pinned staging buffer (cudaHostAlloc is far too slow per call)."""
+    n = 1
+    for s in shape:
+        n *= int(s)
+    key = dtype
+    buf = _pinned.get(key)
+    if buf is None or buf.numel() < n:
+        buf = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
+        _pinned[key] = buf
+    return buf[:n].view(shape)
+
+
+def output(t: torch.Tensor, device_result, like=None, out=None):
+    """Result in the caller's convention: ``out`` (a caller-owned tensor, e.g.
+    pinned host memory, filled in place), else a device tensor for device
+    callers, a CPU tensor for CPU-tensor callers, float64 numpy otherwise."""
+    if out is not None:
+        if tuple(out.shape) != tuple(t.shape):
+            raise ValueError("out has the wrong shape")
+        out.copy_(t, non_blocking=True)
+        if not out.is_cuda:
+            torch.cuda.current_stream(t.device).synchronize()
+        return out
     if device_result:
         return t
     if isinstance(like, torch.Tensor):
-        host = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
-        host.copy_(t, non_blocking=True)
-        torch.cuda.current_stream(t.device).synchronize()
-        return host
+        return t.cpu()
     return t.to(torch.float64).cpu().numpy()

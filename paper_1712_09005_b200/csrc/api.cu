@@ -119,7 +119,7 @@ int fitsne_destroy(fitsne_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&c->accum, &c->fbuf, &c->sbuf, &c->pot, &c->tw, &c->zpart, &c->bbox_part,
-                    &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen};
+                    &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf};
   for (DevBuf* b : bufs) release(*b);
   if (c->h_grid) cudaFreeHost(c->h_grid);
   if (c->h_scal) cudaFreeHost(c->h_scal);
@@ -136,6 +136,17 @@ int fitsne_set_interp(fitsne_ctx* ctx, int p, int min_int, double ipi) {
   ctx->intervals_per_integer = ipi;
   ctx->grid_valid = false;
   return FITSNE_OK;
+}
+
+int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
+  CTX_CHECK(ctx);
+  if (option == FITSNE_OPT_SORTED_SPREAD) {
+    if (value < 0 || value > 2) { set_error("sorted spread mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    ctx->sorted_spread = value;
+    return FITSNE_OK;
+  }
+  set_error("unknown option");
+  return FITSNE_EINVAL;
 }
 
 int fitsne_make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, fitsne_grid* grid_host, void* stream) {

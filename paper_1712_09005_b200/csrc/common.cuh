@@ -128,6 +128,9 @@ struct fitsne_ctx {
   fitsne::DevBuf gtmp;      // (N, s) gradient scratch
   fitsne::DevBuf part;      // per-block partial sums (double)
   fitsne::DevBuf gen;       // generic scratch
+  fitsne::DevBuf sortbuf;   // box sort keys / values / histograms
+  int sorted_spread = 1;      // box-sorted spread (p = 3): 0 never, 1 when crowded, 2 always
+  double raw_bbox[4] = {0, 0, 0, 0};  // unpadded min/max of the last grid's points
 
   fitsne_grid* h_grid = nullptr;  // pinned mirror
   double* h_scal = nullptr;       // pinned scalars

@@ -15,6 +15,8 @@ int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
 // repulsion pipeline ------------------------------------------------------------
 // spread of the t-SNE charges (1, y_0[, y_1]) into ctx->accum (or `accum`)
 int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
+// box-sorted spread (p = 3); FITSNE_EINVAL when not applicable
+int spread_sorted(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
 // FFT stage: accum -> ctx->pot, Z -> ctx->scal[0] (needs n_total for Z)
 int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st);
 // gather: pot -> forces (n, s) [+ k1 (n,), k2 (n, s+1)]

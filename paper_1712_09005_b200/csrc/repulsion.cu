@@ -82,28 +82,41 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
   }
 }
 
+// min/max are order-independent, so the fold is deterministic; out[2S] gets
+// the non-finite flag so one D2H copy returns everything.
 template <int S>
-__global__ void k_bbox_final(const double* __restrict__ part, int nblk, double* __restrict__ out) {
-  // one warp: deterministic fixed-order fold per lane then shuffle
+__global__ void k_bbox_final(const double* __restrict__ part, int nblk, const int* __restrict__ flag,
+                             double* __restrict__ out) {
   double mn[S], mx[S];
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
-  for (int b = threadIdx.x; b < nblk; b += 32) {
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
 #pragma unroll
     for (int d = 0; d < S; ++d) {
       mn[d] = fmin(mn[d], part[b * 2 * S + d]);
       mx[d] = fmax(mx[d], part[b * 2 * S + S + d]);
     }
   }
+  __shared__ double smn[32][S], smx[32][S];
 #pragma unroll
   for (int d = 0; d < S; ++d)
     for (int o = 16; o > 0; o >>= 1) {
       mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
       mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
     }
-  if (threadIdx.x == 0)
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (lane == 0)
+#pragma unroll
+    for (int d = 0; d < S; ++d) { smn[wid][d] = mn[d]; smx[wid][d] = mx[d]; }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < (int)(blockDim.x + 31) / 32; ++w)
+#pragma unroll
+      for (int d = 0; d < S; ++d) { mn[d] = fmin(mn[d], smn[w][d]); mx[d] = fmax(mx[d], smx[w][d]); }
 #pragma unroll
     for (int d = 0; d < S; ++d) { out[d] = mn[d]; out[S + d] = mx[d]; }
+    out[2 * S] = (double)flag[0];
+  }
 }
 
 int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, cudaStream_t st) {
@@ -123,13 +136,13 @@ int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, c
     else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag);
   }
   FITSNE_CHECK_LAUNCH();
-  if (S == 1) k_bbox_final<1><<<1, 32, 0, st>>>(part, nblk, outd);
-  else k_bbox_final<2><<<1, 32, 0, st>>>(part, nblk, outd);
+  if (S == 1) k_bbox_final<1><<<1, 256, 0, st>>>(part, nblk, flag, outd);
+  else k_bbox_final<2><<<1, 256, 0, st>>>(part, nblk, flag, outd);
   FITSNE_CHECK_LAUNCH();
-  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * 2 * S, cudaMemcpyDeviceToHost, st));
-  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_status, flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * (2 * S + 1),
+                              cudaMemcpyDeviceToHost, st));
   FITSNE_CUDA(cudaStreamSynchronize(st));
-  if (ctx->h_status[0]) {
+  if (ctx->h_scal[8 + 2 * S] != 0.0) {
     set_error("points must be finite");
     return FITSNE_ENONFINITE;
   }
@@ -143,6 +156,7 @@ int grid_from_bbox(fitsne_ctx* ctx, const double* bbox, fitsne_grid* out) {
   const int S = ctx->dims;
   double lo[2] = {0, 0}, hi[2] = {0, 0}, span[2] = {0, 0};
   double widest = -INFINITY;
+  for (int d = 0; d < 2 * S; ++d) ctx->raw_bbox[d] = bbox[d];
   for (int d = 0; d < S; ++d) {
     lo[d] = bbox[d];
     hi[d] = bbox[S + d];
@@ -335,6 +349,22 @@ int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
   if (accum == nullptr) {
     FITSNE_TRY(ensure_accum(ctx, st));
     accum = ctx->accum.ptr;
+  }
+  // Box-sorted spread when points crowd into few boxes (same-address atomics
+  // would serialise): estimate the occupied boxes from the raw bounding box.
+  bool use_sorted = ctx->sorted_spread == 2;
+  if (ctx->sorted_spread == 1) {
+    double occ = 1.0;
+    for (int d = 0; d < ctx->dims; ++d) {
+      const double w = (ctx->grid.hi[d] - ctx->grid.lo[d]) / ctx->grid.n_intervals;
+      const double span = ctx->raw_bbox[ctx->dims + d] - ctx->raw_bbox[d];
+      occ *= (span >= 0 && w > 0) ? std::floor(span / w) + 2.0 : 1e30;
+    }
+    use_sorted = (double)n / occ >= 128.0;
+  }
+  if (n > 0 && use_sorted && spread_sorted(ctx, Y, n, accum, st) == FITSNE_OK) {
+    ctx->accum_clean = false;
+    return FITSNE_OK;
   }
   if (n > 0) {
     if (ctx->dtype == FITSNE_F32) {
@@ -817,7 +847,8 @@ k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g
 
 template <typename T>
 static int set_smem(const void* fn, size_t bytes) {
-  if (bytes > 48 * 1024) {
+  // the default 48 KB limit also covers the kernel's static shared memory
+  if (bytes > 40 * 1024) {
     FITSNE_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
   }
   return FITSNE_OK;

@@ -225,8 +225,12 @@ def compute_repulsive(Y, min_intervals: int = 20, points_per_interval: int = 3,
 
 def gradient(P, Y, alpha: float = 1.0, min_intervals: int = 20, points_per_interval: int = 3,
              method: str = "auto", workers: int = 1, *, dtype=None,
-             intervals_per_integer: float = 1.0):
-    """4 (alpha F_attr - F_rep) (optimizer.py:248-262)."""
+             intervals_per_integer: float = 1.0, out=None):
+    """4 (alpha F_attr - F_rep) (optimizer.py:248-262).
+
+    ``out`` (extension): a caller-owned tensor of Y's shape -- e.g. pinned host
+    memory -- that receives the gradient in place (and is returned).
+    """
     if alpha < 1.0:
         raise ValueError("exaggeration alpha must be >= 1")
     shp = _shape(Y)
@@ -237,7 +241,12 @@ def gradient(P, Y, alpha: float = 1.0, min_intervals: int = 20, points_per_inter
     y, dev, dt = _embedding(Y, dtype)
     ctx, _ = _ctx_with_P(P, dev, y.shape[1], dt, points_per_interval, min_intervals,
                          intervals_per_integer)
-    g = torch.empty_like(y)
+    if out is not None and out.is_cuda and out.dtype == dt and out.is_contiguous():
+        g = out
+    elif A.is_device_input(Y):
+        g = torch.empty_like(y)
+    else:
+        g = _scratch(ctx, "grad", y)   # result leaves the device: reuse the scratch
     if method == "fft":
         _lib.check(ctx.lib.fitsne_gradient(ctx.h, _lib.ptr(y), float(alpha), _lib.ptr(g), None,
                                            ctx.stream), "fitsne_gradient")
@@ -245,7 +254,19 @@ def gradient(P, Y, alpha: float = 1.0, min_intervals: int = 20, points_per_inter
         f, _, _, _ = _repulsion_device(y, dev, dt, min_intervals, points_per_interval, "exact")
         _lib.check(ctx.lib.fitsne_gradient_rows(ctx.h, _lib.ptr(y), _lib.ptr(f), float(alpha),
                                                 _lib.ptr(g), ctx.stream), "fitsne_gradient_rows")
-    return A.output(g, A.is_device_input(Y), like=Y)
+    if g is out:
+        return out
+    return A.output(g, A.is_device_input(Y) and out is None, like=Y, out=out)
+
+
+def _scratch(ctx, name, like):
+    """Per-context device scratch reused across calls (host-bound results only)."""
+    store = ctx.__dict__.setdefault("_scratch", {})
+    t = store.get(name)
+    if t is None or t.shape != like.shape or t.dtype != like.dtype or t.device != like.device:
+        t = torch.empty_like(like)
+        store[name] = t
+    return t
 
 
 def _kl_device(ctx, y, z):
