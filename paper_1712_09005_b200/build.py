@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfitsne_b200.so"
 SOURCES = ["api.cu", "repulsion.cu", "attract.cu", "sortspread.cu"]
-HEADERS = ["common.cuh", "fft.cuh", "interp.cuh", "internal.h"]
+HEADERS = ["common.cuh", "fft.cuh", "interp.cuh", "internal.h", "twiddles.cuh"]
 
 NVCC_FLAGS = [
     "-gencode", "arch=compute_100a,code=sm_100a",

@@ -225,8 +225,9 @@ int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
   }
   const int L = g.fft_len;
   // rows stage holds 2 pairs x 2 ping-pong buffers of L complex in shared memory
-  const int lmax = (ctx->dtype == FITSNE_F32) ? 6912 : 3456;
-  if (L > lmax || (g.dims == 1 && L > (ctx->dtype == FITSNE_F32 ? 5184 : 2592))) {
+  // column stage needs (L + 4 plen(L)) complex of shared memory at batch 1
+  const int lmax = (ctx->dtype == FITSNE_F32) ? 5184 : 2592;
+  if (L > lmax) {
     set_error("interpolation grid needs an FFT longer than supported (L=" + std::to_string(L) + ")");
     return FITSNE_ETOOBIG;
   }
@@ -510,7 +511,8 @@ __device__ __forceinline__ void kernel_pair(int i, int j, double hx, double hy, 
 
 // Row stage.  merged=1: block x transforms data row x (the packed pairs) and
 // kernel-spectrum row x in one batched FFT.  merged=0 (large L): blocks [0, n)
-// do the data rows, blocks [n, 2n) the spectrum rows.
+// do the data rows, blocks [n, 2n) the spectrum rows.  Shared memory: the
+// twiddle table (L) then the padded signals (stride plen(L), index pidx).
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int pair0, int npair,
@@ -518,161 +520,229 @@ k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int 
                GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int merged) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  V* a = reinterpret_cast<V*>(smem_raw);
   const int L = g.L, n = g.n;
+  const int PL = plen(L);
   const int H = L / 2 + 1;
+  V* s_tw = reinterpret_cast<V*>(smem_raw);
+  V* a = s_tw + L;
   const bool do_data = merged || (int)blockIdx.x < n;
   const bool do_spec = merged || (int)blockIdx.x >= n;
   const int x = (merged || (int)blockIdx.x < n) ? (int)blockIdx.x : (int)blockIdx.x - n;
   const int ns = do_data ? ((MODE == MODE_TSNE) ? 2 : npair) : 0;
   const int nsig = ns + (do_spec ? 1 : 0);
-  V* b = a + (size_t)nsig * L;
-  for (int y = threadIdx.x; y < L; y += blockDim.x) {
+  V* b = a + (size_t)nsig * PL;
+  stage_twiddles(s_tw, tw, L);
+  for (int y0 = threadIdx.x; y0 < L; y0 += 2 * blockDim.x) {
     if (do_data) {
       if (MODE == MODE_TSNE) {
-        V A = {0, 0}, B = {0, 0};
-        if (y < n) {
-          T* rec = acc + ((size_t)x * n + y) * kNodeSlots;
-          B.x = rec[0];
-          A.x = rec[1];
-          A.y = rec[2];
-          // consume-and-clear: leaves the accumulator zeroed for the next spread
-          rec[0] = 0; rec[1] = 0; rec[2] = 0;
+        T rv[2][3];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int y = y0 + u * blockDim.x;
+          rv[u][0] = rv[u][1] = rv[u][2] = 0;
+          if (y < n) {
+            T* rec = acc + ((size_t)x * n + y) * kNodeSlots;
+            if constexpr (sizeof(T) == 4) {
+              const float4 f = *reinterpret_cast<const float4*>(rec);
+              rv[u][0] = f.x; rv[u][1] = f.y; rv[u][2] = f.z;
+            } else {
+              const double2 f0 = *reinterpret_cast<const double2*>(rec);
+              rv[u][0] = f0.x; rv[u][1] = f0.y; rv[u][2] = rec[2];
+            }
+          }
         }
-        a[y] = A;
-        a[L + y] = B;
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int y = y0 + u * blockDim.x;
+          if (y >= L) continue;
+          V A, B;
+          B.x = rv[u][0]; B.y = 0;
+          A.x = rv[u][1]; A.y = rv[u][2];
+          a[pidx(y)] = A;
+          a[PL + pidx(y)] = B;
+          if (y < n) {
+            // consume-and-clear: leaves the accumulator zeroed for the next spread
+            T* rec = acc + ((size_t)x * n + y) * kNodeSlots;
+            if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(rec) = make_float4(0.f, 0.f, 0.f, 0.f);
+            else { rec[0] = 0; rec[1] = 0; rec[2] = 0; }
+          }
+        }
       } else {
         const size_t G = (size_t)n * n;
-        for (int q = 0; q < npair; ++q) {
-          V v = {0, 0};
-          if (y < n) {
-            int c0 = 2 * (pair0 + q), c1 = c0 + 1;
-            v.x = coeffs[(size_t)c0 * G + (size_t)x * n + y];
-            if (c1 < ncol) v.y = coeffs[(size_t)c1 * G + (size_t)x * n + y];
+        for (int u = 0; u < 2; ++u) {
+          const int y = y0 + u * blockDim.x;
+          if (y >= L) continue;
+          for (int q = 0; q < npair; ++q) {
+            V v = {0, 0};
+            if (y < n) {
+              int c0 = 2 * (pair0 + q), c1 = c0 + 1;
+              v.x = coeffs[(size_t)c0 * G + (size_t)x * n + y];
+              if (c1 < ncol) v.y = coeffs[(size_t)c1 * G + (size_t)x * n + y];
+            }
+            a[(size_t)q * PL + pidx(y)] = v;
           }
-          a[(size_t)q * L + y] = v;
         }
       }
     }
     if (do_spec) {
-      // first[x, j] = K((x hx)^2 + (j hy)^2), columns mirrored (nbody.py:272-281)
-      V z = {0, 0};
-      int jj = (y < n) ? y : ((y > L - n) ? L - y : -1);
-      if (jj >= 0) {
-        T k1, k2;
-        kernel_pair<T>(x, jj, g.h[0], g.h[1], k1, k2);
-        z.x = k1;
-        z.y = k2;
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int y = y0 + u * blockDim.x;
+        if (y >= L) continue;
+        // first[x, j] = K((x hx)^2 + (j hy)^2), columns mirrored (nbody.py:272-281)
+        V z = {0, 0};
+        int jj = (y < n) ? y : ((y > L - n) ? L - y : -1);
+        if (jj >= 0) {
+          T k1, k2;
+          kernel_pair<T>(x, jj, g.h[0], g.h[1], k1, k2);
+          z.x = k1;
+          z.y = k2;
+        }
+        a[(size_t)ns * PL + pidx(y)] = z;
       }
-      a[(size_t)ns * L + y] = z;
     }
   }
-  V* r = block_fft<V, T>(a, b, pl, nsig, L, tw, false);
-  for (int t = threadIdx.x; t < ns * L; t += blockDim.x) {
-    const int q = t / L, k = t - q * L;
-    F[((size_t)q * n + x) * L + k] = r[t];
-  }
+  V* r = block_fft<V, T>(a, b, pl, nsig, PL, s_tw, false);
+  for (int q = 0; q < ns; ++q)
+    for (int k = threadIdx.x; k < L; k += blockDim.x)
+      F[((size_t)q * n + x) * L + k] = r[(size_t)q * PL + pidx(k)];
   if (do_spec)
-    for (int k = threadIdx.x; k < H; k += blockDim.x) Sbuf[(size_t)x * H + k] = r[(size_t)ns * L + k];
+    for (int k = threadIdx.x; k < H; k += blockDim.x)
+      Sbuf[(size_t)x * H + k] = r[(size_t)ns * PL + pidx(k)];
 }
 
-// Column stage: one block per column pair (ky, L-ky).  One batched forward FFT
-// transforms the kernel-spectrum column (slot 0, rows mirrored as in the
-// circulant embedding, nbody.py:278-281) together with the first `batch` data
-// columns; then multiply (+ Parseval for t-SNE) and one batched inverse FFT.
-template <typename T, int MODE>
+// Kernel-spectrum column stage: block b transforms spectrum columns
+// ky = b*kSpecCols .. (rows mirrored as in the circulant embedding,
+// nbody.py:278-281) and stores Khat[ky][kx] = (K1hat, K2hat) / L^2 (real).
+constexpr int kSpecCols = 4;
+
+template <typename T>
 __global__ void __launch_bounds__(256)
-k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restrict__ Sbuf,
-       GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int kern,
-       int with_k1, int batch, double* __restrict__ zpart) {
+k_spec_cols(const typename C2<T>::type* __restrict__ Sbuf, GridArgs g,
+            const typename C2<T>::type* __restrict__ tw, FftPlan pl,
+            typename C2<T>::type* __restrict__ Khat) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = g.L, n = g.n, H = L / 2 + 1;
-  V* K = reinterpret_cast<V*>(smem_raw);
-  V* a = K + L;
-  V* b = a + (size_t)(batch + 1) * L;
-  const int ky = blockIdx.x;
-  const int ncolumns = (ky == 0 || 2 * ky == L) ? 1 : 2;
-  const int nsig = ncolumns * npair;  // data signal s -> column s / npair, pair s % npair
+  const int PL = plen(L);
+  V* s_tw = reinterpret_cast<V*>(smem_raw);
+  V* a = s_tw + L;
+  V* b = a + (size_t)kSpecCols * PL;
+  const int ky0 = blockIdx.x * kSpecCols;
+  const int nc = min(kSpecCols, H - ky0);
+  stage_twiddles(s_tw, tw, L);
+  // each row i contributes kSpecCols consecutive spectrum columns (32 B)
+  for (int x = threadIdx.x; x < L; x += blockDim.x) {
+    const int ii = (x < n) ? x : ((x > L - n) ? L - x : -1);
+    V z[kSpecCols];
+#pragma unroll
+    for (int c = 0; c < kSpecCols; ++c) {
+      z[c].x = 0; z[c].y = 0;
+      if (ii >= 0 && c < nc) z[c] = Sbuf[(size_t)ii * H + ky0 + c];
+    }
+#pragma unroll
+    for (int c = 0; c < kSpecCols; ++c)
+      if (c < nc) a[(size_t)c * PL + pidx(x)] = z[c];
+  }
+  V* r = block_fft<V, T>(a, b, pl, nc, PL, s_tw, false);
   const T scale = (T)(1.0 / ((double)L * (double)L));
+  for (int c = 0; c < nc; ++c)
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      V v = r[(size_t)c * PL + pidx(k)];
+      v.x *= scale;
+      v.y *= scale;
+      Khat[(size_t)(ky0 + c) * L + k] = v;
+    }
+}
+
+// Data column stage: one block per column c in [0, L): forward FFT of the
+// pairs, multiply by the kernel spectrum of column min(c, L-c) (+ Parseval
+// partial of the unit-charge pair for t-SNE), inverse FFT.
+template <typename T, int MODE>
+__global__ void __launch_bounds__(256)
+k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restrict__ Khat,
+       GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int kern,
+       int with_k1, double* __restrict__ zpart) {
+  using V = typename C2<T>::type;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int L = g.L, n = g.n;
+  const int PL = plen(L);
+  V* s_tw = reinterpret_cast<V*>(smem_raw);
+  V* a = s_tw + L;
+  V* b = a + (size_t)npair * PL;
+  const int col = blockIdx.x;
+  const V* Kc = Khat + (size_t)(col <= L - col ? col : L - col) * L;
+  stage_twiddles(s_tw, tw, L);
+  // strided column loads: 4 in flight per thread
+  for (int q = 0; q < npair; ++q)
+    for (int x0 = threadIdx.x; x0 < L; x0 += 4 * blockDim.x) {
+      V z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = x0 + u * blockDim.x;
+        z[u].x = 0; z[u].y = 0;
+        if (x < n) z[u] = F[((size_t)q * n + x) * L + col];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int x = x0 + u * blockDim.x;
+        if (x < L) a[(size_t)q * PL + pidx(x)] = z[u];
+      }
+    }
+  V* fr = block_fft<V, T>(a, b, pl, npair, PL, s_tw, false);
+  V* other = (fr == a) ? b : a;
   double zacc = 0.0;
-  for (int s0 = 0; s0 < nsig; s0 += batch) {
-    const int ns = min(batch, nsig - s0);
-    const bool first = (s0 == 0);
-    __syncthreads();
-    // slot 0: spectrum column (first group only); slots 1..ns: data columns
-    for (int t = threadIdx.x; t < (ns + 1) * L; t += blockDim.x) {
-      const int slot = t / L, x = t - slot * L;
-      V z = {0, 0};
-      if (slot == 0) {
-        if (first) {
-          int ii = (x < n) ? x : ((x > L - n) ? L - x : -1);
-          if (ii >= 0) z = Sbuf[(size_t)ii * H + ky];
-        }
-      } else if (x < n) {
-        const int s = s0 + slot - 1;
-        const int col = (s / npair == 0) ? ky : L - ky;
-        z = F[((size_t)(s % npair) * n + x) * L + col];
-      }
-      a[t] = z;
+  for (int k0 = threadIdx.x; k0 < L; k0 += 2 * blockDim.x) {
+    V kk[2];
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k < L) kk[u] = __ldg(Kc + k);
     }
-    V* fr = block_fft<V, T>(a, b, pl, ns + 1, L, tw, false);
-    V* other = (fr == a) ? b : a;
-    if (first) {
-      for (int k = threadIdx.x; k < L; k += blockDim.x) {
-        V v = fr[k];
-        V kk;
-        kk.x = v.x * scale;  // K1hat / L^2 (real)
-        kk.y = v.y * scale;  // K2hat / L^2 (real)
-        K[k] = kk;
-      }
-      __syncthreads();
-    }
-    for (int t = threadIdx.x; t < ns * L; t += blockDim.x) {
-      const int sl = t / L, k = t - sl * L;
-      const int q = (s0 + sl) % npair;
-      V v = fr[L + t];
-      V kk = K[k];
-      V o;
-      if (MODE == MODE_TSNE) {
-        if (q == 0) {
-          o.x = v.x * kk.y;
-          o.y = v.y * kk.y;
-        } else {
-          zacc += (double)kk.x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
-          if (with_k1) {  // v * (K2 + i K1)
-            o.x = v.x * kk.y - v.y * kk.x;
-            o.y = v.x * kk.x + v.y * kk.y;
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const int k = k0 + u * blockDim.x;
+      if (k >= L) continue;
+      for (int q = 0; q < npair; ++q) {
+        V* p = fr + (size_t)q * PL + pidx(k);
+        const V v = *p;
+        V o;
+        if (MODE == MODE_TSNE) {
+          if (q == 0) {
+            o.x = v.x * kk[u].y;
+            o.y = v.y * kk[u].y;
           } else {
-            o.x = v.x * kk.y;
-            o.y = v.y * kk.y;
+            zacc += (double)kk[u].x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
+            if (with_k1) {  // v * (K2 + i K1)
+              o.x = v.x * kk[u].y - v.y * kk[u].x;
+              o.y = v.x * kk[u].x + v.y * kk[u].y;
+            } else {
+              o.x = v.x * kk[u].y;
+              o.y = v.y * kk[u].y;
+            }
           }
+        } else {
+          const T m = (kern == FITSNE_CAUCHY) ? kk[u].x : kk[u].y;
+          o.x = v.x * m;
+          o.y = v.y * m;
         }
-      } else {
-        T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
-        o.x = v.x * m;
-        o.y = v.y * m;
+        *p = o;
       }
-      fr[L + t] = o;
-    }
-    V* ir = block_fft<V, T>(fr + L, other + L, pl, ns, L, tw, true);
-    for (int t = threadIdx.x; t < ns * n; t += blockDim.x) {
-      const int sl = t / n, x = t - sl * n;
-      const int s = s0 + sl;
-      const int col = (s / npair == 0) ? ky : L - ky;
-      F[((size_t)(s % npair) * n + x) * L + col] = ir[(size_t)sl * L + x];
     }
   }
+  V* ir = block_fft<V, T>(fr, other, pl, npair, PL, s_tw, true);
+  for (int q = 0; q < npair; ++q)
+    for (int x = threadIdx.x; x < n; x += blockDim.x)
+      F[((size_t)q * n + x) * L + col] = ir[(size_t)q * PL + pidx(x)];
   if (MODE == MODE_TSNE) {
     __shared__ double red[32];
     zacc = warp_sum(zacc);
-    __syncthreads();
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = zacc;
     __syncthreads();
     if (threadIdx.x == 0) {
       double s = 0;
       for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += red[w];
-      zpart[ky] = s;
+      zpart[col] = s;
     }
   }
 }
@@ -687,26 +757,44 @@ k_rows_inverse(const typename C2<T>::type* __restrict__ F, GridArgs g,
                double* __restrict__ scal, double n_total) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  const int L = g.L, n = g.n, H = L / 2 + 1;
-  V* a = reinterpret_cast<V*>(smem_raw);
-  V* b = a + (size_t)npair * L;
+  const int L = g.L, n = g.n;
+  const int PL = plen(L);
+  V* s_tw = reinterpret_cast<V*>(smem_raw);
+  V* a = s_tw + L;
+  V* b = a + (size_t)npair * PL;
   const int x = blockIdx.x;
+  stage_twiddles(s_tw, tw, L);
   for (int q = 0; q < npair; ++q)
-    for (int k = threadIdx.x; k < L; k += blockDim.x) a[(size_t)q * L + k] = F[((size_t)q * n + x) * L + k];
-  V* r = block_fft<V, T>(a, b, pl, npair, L, tw, true);
+    for (int k0 = threadIdx.x; k0 < L; k0 += 4 * blockDim.x) {
+      V z[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k < L) z[u] = F[((size_t)q * n + x) * L + k];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int k = k0 + u * blockDim.x;
+        if (k < L) a[(size_t)q * PL + pidx(k)] = z[u];
+      }
+    }
+  V* r = block_fft<V, T>(a, b, pl, npair, PL, s_tw, true);
   if (MODE == MODE_TSNE) {
     for (int y = threadIdx.x; y < n; y += blockDim.x) {
-      V A = r[y], B = r[L + y];
+      V A = r[pidx(y)], B = r[PL + pidx(y)];
       T* rec = pot + ((size_t)x * n + y) * kNodeSlots;
-      rec[0] = B.x;  // K2 * 1
-      rec[1] = A.x;  // K2 * y_0
-      rec[2] = A.y;  // K2 * y_1
-      rec[3] = B.y;  // K1 * 1 (only with_k1)
+      // slots: K2*1, K2*y_0, K2*y_1, K1*1 (the last only with_k1)
+      if constexpr (sizeof(T) == 4) {
+        *reinterpret_cast<float4*>(rec) = make_float4(B.x, A.x, A.y, B.y);
+      } else {
+        reinterpret_cast<double2*>(rec)[0] = make_double2(B.x, A.x);
+        reinterpret_cast<double2*>(rec)[1] = make_double2(A.y, B.y);
+      }
     }
     if (x == 0) {
       __shared__ double red[32];
       double s = 0;
-      for (int k = threadIdx.x; k < H; k += blockDim.x) s += zpart[k];
+      for (int k = threadIdx.x; k < L; k += blockDim.x) s += zpart[k];
       s = warp_sum(s);
       if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
       __syncthreads();
@@ -721,7 +809,7 @@ k_rows_inverse(const typename C2<T>::type* __restrict__ F, GridArgs g,
     for (int q = 0; q < npair; ++q) {
       int c0 = 2 * (pair0 + q), c1 = c0 + 1;
       for (int y = threadIdx.x; y < n; y += blockDim.x) {
-        V v = r[(size_t)q * L + y];
+        V v = r[(size_t)q * PL + pidx(y)];
         out[(size_t)c0 * G + (size_t)x * n + y] = v.x;
         if (c1 < ncol) out[(size_t)c1 * G + (size_t)x * n + y] = v.y;
       }
@@ -729,7 +817,7 @@ k_rows_inverse(const typename C2<T>::type* __restrict__ F, GridArgs g,
   }
 }
 
-// 1-D convolution: a single block holds the whole transform (L <= 5184 f32).
+// 1-D convolution: a single block holds the whole transform.
 template <typename T, int MODE>
 __global__ void __launch_bounds__(1024)
 k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g,
@@ -738,9 +826,10 @@ k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = g.L, n = g.n;
+  const int PL = plen(L);
   V* K = reinterpret_cast<V*>(smem_raw);
   V* a = K + L;
-  V* b = a + 2 * L;
+  V* b = a + 2 * (size_t)PL;
   // spectrum: circ[:n] = first, circ[L-n+1:] = mirror (nbody.py:264-271)
   for (int j = threadIdx.x; j < L; j += blockDim.x) {
     V z = {0, 0};
@@ -751,12 +840,12 @@ k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g
       z.x = (T)base;
       z.y = (T)(base * base);
     }
-    a[j] = z;
+    a[pidx(j)] = z;
   }
-  V* r = block_fft<V, T>(a, b, pl, 1, L, tw, false);
+  V* r = block_fft<V, T>(a, b, pl, 1, PL, tw, false);
   const T scale = (T)(1.0 / (double)L);
   for (int k = threadIdx.x; k < L; k += blockDim.x) {
-    V v = r[k];
+    V v = r[pidx(k)];
     V kk;
     kk.x = v.x * scale;
     kk.y = v.y * scale;
@@ -780,7 +869,7 @@ k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g
             if (c1 < ncol) v.y = coeffs[(size_t)c1 * n + y];
           }
         }
-        a[(size_t)s * L + y] = v;
+        a[(size_t)s * PL + pidx(y)] = v;
       }
     }
     if (MODE == MODE_TSNE) {
@@ -790,11 +879,12 @@ k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g
         rec[0] = 0; rec[1] = 0;
       }
     }
-    V* fr = block_fft<V, T>(a, b, pl, ns, L, tw, false);
+    V* fr = block_fft<V, T>(a, b, pl, ns, PL, tw, false);
     V* other = (fr == a) ? b : a;
     for (int t = threadIdx.x; t < ns * L; t += blockDim.x) {
       int s = t / L, k = t - s * L;
-      V v = fr[t];
+      V* p = fr + (size_t)s * PL + pidx(k);
+      V v = *p;
       V kk = K[k];
       V o;
       if (MODE == MODE_TSNE) {
@@ -813,17 +903,17 @@ k_conv1d(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, GridArgs g
         T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
         o.x = v.x * m; o.y = v.y * m;
       }
-      fr[t] = o;
+      *p = o;
     }
-    V* ir = block_fft<V, T>(fr, other, pl, ns, L, tw, true);
+    V* ir = block_fft<V, T>(fr, other, pl, ns, PL, tw, true);
     for (int y = threadIdx.x; y < n; y += blockDim.x) {
       if (MODE == MODE_TSNE) {
-        V A = ir[y], B = ir[L + y];
+        V A = ir[pidx(y)], B = ir[PL + pidx(y)];
         T* rec = pot + (size_t)y * kNodeSlots;
         rec[0] = B.x; rec[1] = A.x; rec[2] = 0; rec[3] = B.y;
       } else {
         for (int s = 0; s < ns; ++s) {
-          V v = ir[(size_t)s * L + y];
+          V v = ir[(size_t)s * PL + pidx(y)];
           int c0 = 2 * (q0 + s), c1 = c0 + 1;
           out[(size_t)c0 * n + y] = v.x;
           if (c1 < ncol) out[(size_t)c1 * n + y] = v.y;
@@ -870,7 +960,7 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
   double* scal = (double*)ctx->scal.ptr;
   T* pot = (T*)ctx->pot.ptr;
   if (gr.dims == 1) {
-    size_t smem = sizeof(V) * (size_t)L * 5;
+    size_t smem = sizeof(V) * ((size_t)L + 4 * (size_t)plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_conv1d<T, MODE>, smem));
     k_conv1d<T, MODE><<<1, 1024, smem, st>>>(accum, coeffs, ncol, g, tw, pl, kern, with_k1 ? 1 : 0,
                                              pot, out, scal, (double)n_total);
@@ -879,31 +969,35 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
   }
   const int maxpair = 2;
   FITSNE_TRY(ensure(ctx->fbuf, sizeof(V) * (size_t)maxpair * n * L));
-  FITSNE_TRY(ensure(ctx->sbuf, sizeof(V) * (size_t)n * H));
-  FITSNE_TRY(ensure(ctx->zpart, sizeof(double) * (size_t)H));
+  // spectrum rows (n x H) followed by the spectrum table Khat (H x L)
+  FITSNE_TRY(ensure(ctx->sbuf, sizeof(V) * ((size_t)n * H + (size_t)H * L)));
+  FITSNE_TRY(ensure(ctx->zpart, sizeof(double) * (size_t)L));
   V* F = (V*)ctx->fbuf.ptr;
   V* Sb = (V*)ctx->sbuf.ptr;
+  V* Kh = Sb + (size_t)n * H;
   double* zp = (double*)ctx->zpart.ptr;
   const int npair_total = (MODE == MODE_TSNE) ? 2 : (ncol + 1) / 2;
   for (int pair0 = 0; pair0 < npair_total; pair0 += maxpair) {
     const int npair = std::min(maxpair, npair_total - pair0);
     // the spectrum rows are recomputed per pair group (one group for t-SNE)
     const int nd = (MODE == MODE_TSNE) ? 2 : npair;
-    const int merged = sizeof(V) * (size_t)2 * (nd + 1) * L <= 113 * 1024 ? 1 : 0;
-    size_t smem_r = sizeof(V) * (size_t)2 * (merged ? nd + 1 : std::max(nd, 1)) * L;
+    const int merged = sizeof(V) * ((size_t)L + 2 * (size_t)(nd + 1) * plen(L)) <= 113 * 1024 ? 1 : 0;
+    size_t smem_r = sizeof(V) * ((size_t)L + 2 * (size_t)(merged ? nd + 1 : std::max(nd, 1)) * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
     k_rows_forward<T, MODE><<<merged ? n : 2 * n, 256, smem_r, st>>>(accum, coeffs, ncol, pair0,
                                                                      npair, F, Sb, g, tw, pl, merged);
     FITSNE_CHECK_LAUNCH();
-    // data signals per batched FFT: as many as fit two blocks per SM (<= 113 KB)
-    int batch = 4;
-    while (batch > 1 && sizeof(V) * (size_t)(3 + 2 * batch) * L > 113 * 1024) batch /= 2;
-    size_t smem_c = sizeof(V) * (size_t)(3 + 2 * batch) * L;
+    if (pair0 == 0) {
+      size_t smem_s = sizeof(V) * ((size_t)L + 2 * (size_t)kSpecCols * plen(L));
+      FITSNE_TRY(set_smem<T>((const void*)k_spec_cols<T>, smem_s));
+      k_spec_cols<T><<<(H + kSpecCols - 1) / kSpecCols, 256, smem_s, st>>>(Sb, g, tw, pl, Kh);
+      FITSNE_CHECK_LAUNCH();
+    }
+    size_t smem_c = sizeof(V) * ((size_t)L + 2 * (size_t)npair * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_cols<T, MODE>, smem_c));
-    k_cols<T, MODE><<<H, 256, smem_c, st>>>(F, Sb, g, tw, pl, npair, kern, with_k1 ? 1 : 0, batch,
-                                            zp);
+    k_cols<T, MODE><<<L, 256, smem_c, st>>>(F, Kh, g, tw, pl, npair, kern, with_k1 ? 1 : 0, zp);
     FITSNE_CHECK_LAUNCH();
-    size_t smem_i = sizeof(V) * (size_t)2 * npair * L;
+    size_t smem_i = sizeof(V) * ((size_t)L + 2 * (size_t)npair * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_rows_inverse<T, MODE>, smem_i));
     k_rows_inverse<T, MODE><<<n, 256, smem_i, st>>>(F, g, tw, pl, npair, ncol, pair0, pot, out, zp,
                                                     scal, (double)n_total);
