@@ -61,6 +61,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="per-stage timing (extra JSON)")
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2],
+                    help="0 direct atomics, 1 auto (default), 2 box-sorted")
     return ap.parse_args()
 
 
@@ -261,6 +263,7 @@ def run_ours(args):
     csr = device_csr(P, dt, dev)
     ctx = _lib.context(dev, 2, dt, 3, 50, 1.0)
     ctx.set_affinities(csr)
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, args.spread_mode), "set_option")
     g = torch.empty_like(y)
     zc = __import__("ctypes").c_double()
 

@@ -50,37 +50,57 @@ __device__ __forceinline__ void load_point(const T* __restrict__ Y, int64_t j, T
   }
 }
 
+// p / (1 + d2): fp32 uses the fast reciprocal-based division (<= 2 ulp, well
+// inside the fp32 parity bar); fp64 keeps IEEE division.
+template <typename T>
+__device__ __forceinline__ T cauchy_weight(T p, T d2) { return p / ((T)1 + d2); }
+template <>
+__device__ __forceinline__ float cauchy_weight<float>(float p, float d2) {
+  return __fdividef(p, 1.0f + d2);
+}
+
 // One warp reduces CSR row [beg, end) against y_i: acc += sum_j w_ij (y_i - y_j),
-// w_ij = p_ij / (1 + d_ij^2), and (KL) klr += p_ij log1p(d_ij^2).  Two stored
-// entries per lane per trip keep two independent neighbour gathers in flight.
+// w_ij = p_ij / (1 + d_ij^2), and (KL) klr += p_ij log1p(d_ij^2).  Each lane
+// first issues the (col, val) loads of kU stored entries, then their kU
+// neighbour gathers, so 2 kU independent loads are in flight per lane.
 template <typename T, int S, bool KL>
 __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, const T* __restrict__ val,
                                            const T* __restrict__ Y, int64_t beg, int64_t end,
                                            int lane, const T (&yi)[S], T (&acc)[S], T& klr) {
-  for (int64_t k = beg + lane; k < end; k += 64) {
-    const bool two = k + 32 < end;
-    const int32_t j0 = __ldg(col + k);
-    const T p0 = __ldg(val + k);
-    const int32_t j1 = two ? __ldg(col + k + 32) : j0;
-    const T p1 = two ? __ldg(val + k + 32) : (T)0;
-    T y0[S], y1[S];
-    load_point<T, S>(Y, j0, y0);
-    load_point<T, S>(Y, j1, y1);
-    T d0[S], d1[S], s0 = 0, s1 = 0;
+  constexpr int kU = 4;
+  for (int64_t k0 = beg + lane; k0 < end; k0 += 32 * kU) {
+    int32_t j[kU];
+    T p[kU];
 #pragma unroll
-    for (int d = 0; d < S; ++d) {
-      d0[d] = yi[d] - y0[d];
-      d1[d] = yi[d] - y1[d];
-      s0 += d0[d] * d0[d];
-      s1 += d1[d] * d1[d];
+    for (int u = 0; u < kU; ++u) {
+      const int64_t k = k0 + 32 * u;
+      const bool ok = k < end;
+      j[u] = ok ? __ldg(col + k) : 0;
+      p[u] = ok ? __ldg(val + k) : (T)0;
     }
-    const T w0 = p0 / ((T)1 + s0);
-    const T w1 = p1 / ((T)1 + s1);
+    T yj[kU][S];
 #pragma unroll
-    for (int d = 0; d < S; ++d) acc[d] += w0 * d0[d] + w1 * d1[d];
-    if (KL) {
-      if (p0 > (T)0) klr += p0 * fast_log1p<T>(s0);
-      if (p1 > (T)0) klr += p1 * fast_log1p<T>(s1);
+    for (int u = 0; u < kU; ++u) {
+      if (k0 + 32 * u < end) load_point<T, S>(Y, j[u], yj[u]);
+      else {
+#pragma unroll
+        for (int d = 0; d < S; ++d) yj[u][d] = yi[d];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kU; ++u) {
+      T df[S], s2 = 0;
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        df[d] = yi[d] - yj[u][d];
+        s2 += df[d] * df[d];
+      }
+      const T w = cauchy_weight<T>(p[u], s2);
+#pragma unroll
+      for (int d = 0; d < S; ++d) acc[d] += w * df[d];
+      if (KL) {
+        if (p[u] > (T)0) klr += p[u] * fast_log1p<T>(s2);
+      }
     }
   }
 }
