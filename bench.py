@@ -232,7 +232,8 @@ def run_ours(args):
         ev = parallel.ShardedGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
                                       points_per_interval=3)
         y_full = torch.from_numpy(Y).to(device=dev, dtype=dt)
-        step = lambda: ev.gradient(y_full, 1.0)  # noqa: E731
+        y_local = ev.local(y_full).contiguous()
+        step = lambda: ev.gradient(y_local, 1.0)  # noqa: E731  (all-gathers Y inside)
         for _ in range(args.warmup):
             step()
         dist.barrier()

@@ -1,0 +1,158 @@
+"""Sharded (multi-GPU) t-SNE gradient: one process per GPU, torch.distributed.
+
+Points and CSR rows are partitioned by contiguous index range (rank r owns
+[N r / R, N (r+1) / R)).  One evaluation of 4 (alpha F_attr - F_rep)
+(optimizer.py:248-262) for the local rows:
+
+  1. local bounding box                  fitsne_bbox
+  2. all-reduce MIN / MAX of the box     -> identical grid on every rank
+     (grid formulas nbody.py:131-143, fitsne_grid_from_bbox)
+  3. all-gather of Y                     (needed by the row-partitioned SpMV)
+  4. spread of the local points into a private accumulator   fitsne_spread_tsne
+  5. all-reduce SUM of the accumulator (4 slots x G nodes)
+  6. FFT stage + Parseval Z (replicated; the grid is small)  fitsne_fft_tsne
+  7. gather of F_rep at the local points                     fitsne_gather_tsne
+  8. SpMV over the local rows + combine                      fitsne_gradient_rows
+
+The stage arithmetic is pluggable (`stages`): `LibStages` runs the CUDA
+library; the multi-process CPU tests plug in an oracle-backed implementation
+to exercise the partitioning and the collectives with the gloo backend.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+from . import _lib
+from .affinities import device_csr, n_points
+
+__all__ = ["shard_range", "LibStages", "ShardedGradient"]
+
+
+def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
+    return n * rank // world, n * (rank + 1) // world
+
+
+class LibStages:
+    """Stage implementation on the CUDA library (one context per rank)."""
+
+    launches_per_step = 8  # bbox x2, spread, rows, spec cols, cols, rows inverse, gather + SpMV
+
+    def __init__(self, P, dims, dtype, device, min_intervals, points_per_interval,
+                 intervals_per_integer, row_begin, row_end):
+        self.dims = dims
+        self.dtype = dtype
+        self.device = device
+        self.n_total = n_points(P)
+        self.ctx = _lib.Context(device, dims, dtype, points_per_interval, min_intervals,
+                                intervals_per_integer)
+        self.csr = device_csr(P, dtype, device, row_begin, row_end)
+        self.ctx.set_affinities(self.csr)
+
+    # -- collectives run on device tensors (NCCL) --------------------------
+    def to_comm(self, x: np.ndarray) -> torch.Tensor:
+        return torch.as_tensor(x, dtype=torch.float64, device=self.device)
+
+    def bbox(self, y_local: torch.Tensor) -> np.ndarray:
+        out = (C.c_double * (2 * self.dims))()
+        _lib.check(self.ctx.lib.fitsne_bbox(self.ctx.h, _lib.ptr(y_local), y_local.shape[0], out,
+                                            self.ctx.stream), "fitsne_bbox")
+        return np.array(out[:], dtype=np.float64)
+
+    def set_grid(self, bbox: np.ndarray) -> None:
+        arr = (C.c_double * (2 * self.dims))(*bbox.tolist())
+        g = _lib.Grid()
+        _lib.check(self.ctx.lib.fitsne_grid_from_bbox(self.ctx.h, arr, C.byref(g)),
+                   "fitsne_grid_from_bbox")
+
+    def spread(self, y_local: torch.Tensor) -> torch.Tensor:
+        n_acc = int(self.ctx.lib.fitsne_grid_accum_len(self.ctx.h))
+        acc = torch.zeros(n_acc, dtype=self.dtype, device=self.device)
+        _lib.check(self.ctx.lib.fitsne_spread_tsne(self.ctx.h, _lib.ptr(y_local), y_local.shape[0],
+                                                   _lib.ptr(acc), self.ctx.stream),
+                   "fitsne_spread_tsne")
+        return acc
+
+    def fft(self, acc: torch.Tensor) -> float:
+        z = C.c_double()
+        _lib.check(self.ctx.lib.fitsne_fft_tsne(self.ctx.h, _lib.ptr(acc), self.n_total, 0,
+                                                C.byref(z), self.ctx.stream), "fitsne_fft_tsne")
+        return float(z.value)
+
+    def gather(self, y_local: torch.Tensor) -> torch.Tensor:
+        f = torch.empty_like(y_local)
+        _lib.check(self.ctx.lib.fitsne_gather_tsne(self.ctx.h, _lib.ptr(y_local), y_local.shape[0],
+                                                   _lib.ptr(f), None, None, self.ctx.stream),
+                   "fitsne_gather_tsne")
+        return f
+
+    def attract_rows(self, y_full: torch.Tensor, forces_local: torch.Tensor,
+                     alpha: float) -> torch.Tensor:
+        g = torch.empty_like(forces_local)
+        _lib.check(self.ctx.lib.fitsne_gradient_rows(self.ctx.h, _lib.ptr(y_full),
+                                                     _lib.ptr(forces_local), float(alpha),
+                                                     _lib.ptr(g), self.ctx.stream),
+                   "fitsne_gradient_rows")
+        return g
+
+
+class ShardedGradient:
+    """Row-partitioned gradient over a torch.distributed process group."""
+
+    def __init__(self, P, n_dims=2, dtype=torch.float32, device=None, min_intervals=20,
+                 points_per_interval=3, intervals_per_integer=1.0, group=None, stages=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.n = n_points(P)
+        self.dims = n_dims
+        self.row_begin, self.row_end = shard_range(self.n, self.rank, self.world)
+        self.counts = [shard_range(self.n, r, self.world)[1] - shard_range(self.n, r, self.world)[0]
+                       for r in range(self.world)]
+        if stages is None:
+            stages = LibStages(P, n_dims, dtype, device, min_intervals, points_per_interval,
+                               intervals_per_integer, self.row_begin, self.row_end)
+        self.stages = stages
+        self.launches_per_step = getattr(stages, "launches_per_step", 0)
+
+    def local(self, y_full):
+        return y_full[self.row_begin:self.row_end]
+
+    def _all_gather_rows(self, y_local):
+        m = max(self.counts)
+        pad = y_local.new_zeros((m, self.dims))
+        pad[: y_local.shape[0]] = y_local
+        bufs = [torch.empty_like(pad) for _ in range(self.world)]
+        dist.all_gather(bufs, pad, group=self.group)
+        return torch.cat([b[:c] for b, c in zip(bufs, self.counts)], 0).contiguous()
+
+    def gradient(self, y_local, alpha: float = 1.0, y_full=None):
+        """Gradient rows of this rank (n_local, s); y_local are its own points."""
+        if alpha < 1.0:
+            raise ValueError("exaggeration alpha must be >= 1")
+        st = self.stages
+        # 1-2: global bounding box -> identical grid everywhere
+        bb = st.bbox(y_local)
+        s = self.dims
+        lo = st.to_comm(bb[:s])
+        hi = st.to_comm(bb[s:])
+        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
+        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.group)
+        st.set_grid(np.concatenate([lo.cpu().numpy(), hi.cpu().numpy()]))
+        # 3: all-gather Y (skipped when the caller already holds it)
+        if y_full is None:
+            y_full = self._all_gather_rows(y_local)
+        # 4-5: private spread + grid all-reduce
+        acc = st.spread(y_local)
+        dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group)
+        # 6: replicated FFT stage
+        z = st.fft(acc)
+        if not z > 0:
+            raise ValueError("normalization Z must be positive")
+        # 7-8: gather local F_rep, SpMV over local rows
+        f_local = st.gather(y_local)
+        return st.attract_rows(y_full, f_local, alpha)

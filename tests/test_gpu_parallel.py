@@ -1,0 +1,47 @@
+"""Sharded-gradient stages on the CUDA library (LibStages) in a single-rank
+NCCL group: every collective runs, the math must equal the oracle gradient.
+(Multi-rank partitioning is covered with gloo on CPU in test_parallel_gloo.)"""
+
+from __future__ import annotations
+
+import os
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+
+from oracle import fitsne_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def nccl_group(cuda):
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    if not dist.is_initialized():
+        dist.init_process_group("nccl", rank=0, world_size=1)
+    yield
+    dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-9), (torch.float32, 1e-3)])
+def test_lib_stages_single_rank(nccl_group, dtype, tol):
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    from paper_1712_09005_b200.parallel import ShardedGradient
+    rng = np.random.default_rng(3)
+    n = 20000
+    c = rng.uniform(-30, 30, (10, 2))
+    y = c[rng.integers(0, 10, n)] + 2 * rng.standard_normal((n, 2))
+    r = np.repeat(np.arange(n), 10)
+    cc = rng.integers(0, n - 1, n * 10)
+    cc = cc + (cc >= r)
+    key = np.unique(np.minimum(r, cc) * n + np.maximum(r, cc))
+    P = SparseAffinities(n=n, rows=key // n, cols=key % n, values=np.full(key.size, 0.5 / key.size))
+    sg = ShardedGradient(P, n_dims=2, dtype=dtype, device=0, min_intervals=50)
+    yt = torch.from_numpy(y).to(device=0, dtype=dtype)
+    g = sg.gradient(yt, alpha=12.0).double().cpu().numpy()
+    ref = O.grad(P.rows, P.cols, P.values, y.astype(np.float32).astype(np.float64)
+                 if dtype == torch.float32 else y, 12.0, 50, 3, "fft")
+    assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= tol
