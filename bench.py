@@ -60,9 +60,15 @@ def parse():
     ap.add_argument("--dtype", default="float32", choices=["float32", "float64"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--breakdown", action="store_true", help="per-stage timing (extra JSON)")
+    ap.add_argument("--full-run", action="store_true",
+                    help="also time the complete 1000-iteration C3 t-SNE run (run_tsne, fused "
+                         "device iterations, late exaggeration 4 from 750) and report it")
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2],
                     help="0 direct atomics, 1 auto (default), 2 box-sorted")
+    ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2],
+                    help="0 serial, 1 (default) SpMV || repulsion, 2 + priority repulsion stream")
+    ap.add_argument("--spmv-blocks", type=int, default=0, help="persistent SpMV blocks per SM (0: one tile per warp)")
     return ap.parse_args()
 
 
@@ -265,6 +271,8 @@ def run_ours(args):
     ctx = _lib.context(dev, 2, dt, 3, 50, 1.0)
     ctx.set_affinities(csr)
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, args.spread_mode), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, args.overlap_mode), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 3, args.spmv_blocks), "set_option")
     g = torch.empty_like(y)
     zc = __import__("ctypes").c_double()
 
@@ -352,7 +360,33 @@ def run_ours(args):
     }
     if breakdown:
         line["breakdown_ms"] = breakdown
+    if args.full_run:
+        line["full_run"] = full_run(P, dt, dev)
+        line["full_run_no_reorder"] = full_run(P, dt, dev, reorder=False)
     print(json.dumps(line), flush=True)
+
+
+def full_run(P, dt, dev, n_iter=1000, reorder=True):
+    """Config 3 as described: a full t-SNE run (Y0 ~ N(0, 1e-4^2), early
+    exaggeration 12 for 250 iterations, late exaggeration 4 from 750)."""
+    import torch
+    from paper_1712_09005_b200 import optimizer
+    cfg = optimizer.TsneConfig(
+        dims=2, n_iter=n_iter, learning_rate=200.0, min_intervals=50, points_per_interval=3,
+        exaggeration=optimizer.ExaggerationSchedule(12.0, 250, 4.0, 750), seed=0, pca_dims=None,
+        repulsion_method="fft", dtype="float32" if dt == torch.float32 else "float64", device=dev,
+        reorder_iters=(100, 250, 500, 750) if reorder else None)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = optimizer.run_tsne(affinities=P, config=cfg)
+    torch.cuda.synchronize()
+    sec = time.perf_counter() - t0
+    span = np.ptp(res.embedding, axis=0)
+    return {"iterations": n_iter, "seconds": sec, "grad_evals_per_s": n_iter / sec,
+            "kl_first": float(res.kl_log[0]), "kl_final": float(res.kl_log[-1]),
+            "final_span": [float(s) for s in span],
+            "reorder": bool(reorder),
+            "note": "wall clock of run_tsne incl. one bbox readback per iteration"}
 
 
 def stage_breakdown(ctx, y, n, dt, steps, stream):

@@ -82,7 +82,16 @@ int fitsne_set_interp(fitsne_ctx* ctx, int points_per_interval, int min_interval
  *   FITSNE_OPT_SORTED_SPREAD: 0 = one atomic per point and node; 1 (default)
  *   = box-sorted segmented spread (p = 3) when the points crowd into few boxes
  *   (>= 128 points per occupied box); 2 = always box-sorted. */
-enum fitsne_option { FITSNE_OPT_SORTED_SPREAD = 1 };
+enum fitsne_option {
+  FITSNE_OPT_SORTED_SPREAD = 1,
+  FITSNE_OPT_OVERLAP = 2,
+  FITSNE_OPT_SPMV_BLOCKS_PER_SM = 3
+};
+/*   FITSNE_OPT_OVERLAP: 0 = serial; 1 (default) = persistent attractive SpMV on
+ *   the caller's stream overlapping spread/FFT on an internal stream; 2 = same
+ *   with the internal stream at high priority.
+ *   FITSNE_OPT_SPMV_BLOCKS_PER_SM: persistent SpMV grid size in the overlap
+ *   modes (default 5 blocks of 256 threads per SM). */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 
 /* --- a1: make_grid (nbody.py:118-150).  Device bbox reduction + fp64 grid

@@ -162,3 +162,29 @@ def ordered_total(P) -> float:
     if hasattr(P, "ordered_total"):
         return float(P.ordered_total)
     return float(P.sum())
+
+
+def permute_csr(csr: DeviceCSR, perm: torch.Tensor, inv: torch.Tensor) -> DeviceCSR:
+    """Symmetric relabelling P' = P[perm][:, perm] of a full (all-rows) CSR.
+
+    perm[new] = old, inv[old] = new.  Row segments move with their rows and
+    column indices are relabelled; entries inside a row keep their order (no
+    re-sort is needed for locality: a warp's gathers touch few cache lines as
+    long as the labels of a row's neighbours are close).
+    """
+    if csr.row_begin != 0 or csr.n_rows != csr.n_total:
+        raise ValueError("permute_csr needs the full matrix")
+    rowptr, col, val = csr.rowptr, csr.col, csr.val
+    n = csr.n_rows
+    deg = rowptr[1:] - rowptr[:-1]
+    new_deg = deg[perm]
+    new_rowptr = torch.zeros_like(rowptr)
+    torch.cumsum(new_deg, 0, out=new_rowptr[1:])
+    nnz = int(new_rowptr[-1].item())
+    row_of = torch.repeat_interleave(torch.arange(n, device=rowptr.device), new_deg,
+                                     output_size=nnz)
+    src = torch.arange(nnz, device=rowptr.device) - new_rowptr[row_of] + rowptr[perm][row_of]
+    del row_of
+    new_col = inv[col[src].long()].to(torch.int32)
+    new_val = val[src]
+    return DeviceCSR(new_rowptr, new_col.contiguous(), new_val.contiguous(), 0, n, csr.ordered_total)

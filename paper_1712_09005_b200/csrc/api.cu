@@ -121,6 +121,9 @@ int fitsne_destroy(fitsne_ctx* c) {
   DevBuf* bufs[] = {&c->accum, &c->fbuf, &c->sbuf, &c->pot, &c->tw, &c->zpart, &c->bbox_part,
                     &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf};
   for (DevBuf* b : bufs) release(*b);
+  if (c->ev_in) cudaEventDestroy(c->ev_in);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->side) cudaStreamDestroy(c->side);
   if (c->h_grid) cudaFreeHost(c->h_grid);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -143,6 +146,24 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
   if (option == FITSNE_OPT_SORTED_SPREAD) {
     if (value < 0 || value > 2) { set_error("sorted spread mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
     ctx->sorted_spread = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_OVERLAP) {
+    if (value < 0 || value > 2) { set_error("overlap mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    if (ctx->side && value != ctx->overlap) {  // priority is fixed at creation
+      cudaStreamSynchronize(ctx->side);
+      cudaStreamDestroy(ctx->side);
+      ctx->side = nullptr;
+      if (ctx->ev_in) cudaEventDestroy(ctx->ev_in);
+      if (ctx->ev_done) cudaEventDestroy(ctx->ev_done);
+      ctx->ev_in = ctx->ev_done = nullptr;
+    }
+    ctx->overlap = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_SPMV_BLOCKS_PER_SM) {
+    if (value < 0 || value > 32) { set_error("SpMV blocks per SM must be in [0, 32]"); return FITSNE_EINVAL; }
+    ctx->spmv_blocks_per_sm = value;
     return FITSNE_OK;
   }
   set_error("unknown option");
@@ -308,12 +329,9 @@ int fitsne_gradient(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, do
   if (!(alpha >= 1.0)) { set_error("exaggeration alpha must be >= 1"); return FITSNE_EINVAL; }
   const int64_t n = ctx->n_total;
   if (n < 2) { set_error("repulsion needs at least two points"); return FITSNE_EINVAL; }
-  FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)n * ctx->dims));
-  FITSNE_TRY(make_grid(ctx, Y, n, st));
-  FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
-  FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
-  // gather of F_rep fused into the SpMV warps (k_attract MODE 2)
-  FITSNE_TRY(attractive(ctx, Y, nullptr, alpha, grad, 2, false, st));
+  // attractive SpMV on a side stream overlapping grid + spread + FFT, then a
+  // thread-per-point gather-and-combine (attract.cu: gradient_overlapped)
+  FITSNE_TRY(gradient_overlapped(ctx, Y, alpha, grad, st));
   if (z_host) {
     FITSNE_TRY(read_scalars(ctx, 1, st));
     *z_host = ctx->h_scal[0];

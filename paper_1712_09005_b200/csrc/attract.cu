@@ -224,9 +224,17 @@ __global__ void k_fold(const double* __restrict__ part, int n, double* __restric
 }
 
 // one 32-row tile per warp (the hardware scheduler balances the tiles)
+// Overlap modes use a persistent grid (ctx->spmv_blocks_per_sm blocks per SM,
+// warps grid-stride over the 32-row tiles) so all SpMV blocks are resident
+// at once and the concurrently launched FFT blocks find free SM slots;
+// otherwise one tile per warp.
 static int attract_grid(fitsne_ctx* ctx) {
   int64_t tiles = (ctx->n_rows + 31) / 32;
   int64_t blocks = (tiles + kBlock / 32 - 1) / (kBlock / 32);
+  if (ctx->overlap != 0 && ctx->spmv_blocks_per_sm > 0) {
+    const int64_t cap = (int64_t)ctx->num_sms * ctx->spmv_blocks_per_sm;
+    if (blocks > cap) blocks = cap;
+  }
   if (blocks < 1) blocks = 1;
   if (blocks > (1LL << 30)) blocks = (1LL << 30);
   return (int)blocks;
@@ -498,32 +506,148 @@ __global__ void k_kl_final(const double* __restrict__ part, int n, const double*
   }
 }
 
+// ---------------------------------------------------------------------------
+// Overlapped schedule.  The attractive SpMV does not depend on the grid, so it
+// runs on a side stream concurrently with bbox -> spread -> FFT (the SpMV is
+// bound by L1/L2 gathers, the FFT stages by shared memory and issue, so they
+// share SMs well).  A thread-per-point combine kernel then gathers F_rep from
+// the potential grid and finishes the gradient (and, for run_tsne, the
+// momentum / gains update, optimizer.py:299-323).
+// ---------------------------------------------------------------------------
+template <typename T, int S, int P, bool STEP>
+__global__ void __launch_bounds__(kBlock)
+k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ pot,
+          const double* __restrict__ scal, const T* __restrict__ attr, T alpha,
+          T* __restrict__ grad, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel,
+          T* __restrict__ gains, int32_t* __restrict__ status) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  int bad = 0;
+  if (i < n) {
+    T yi[S], at[S];
+    load_point<T, S>(Y, i, yi);
+    load_point<T, S>(attr, i, at);
+    T phi[4];
+    point_gather<T, S, P>(yi, g, pot, phi);
+    const T Z = (T)scal[0];
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      const int64_t o = i * S + d;
+      const T gd = (T)4 * (alpha * at[d] - frep_from_phi<T, S>(yi, phi, Z, d));
+      if (!STEP) {
+        grad[o] = gd;
+      } else {
+        if (!isfinite(gd)) bad |= 1;
+        const T v = vel[o], gn = gains[o];
+        const bool agree = npsign(gd) == npsign(v);
+        const T vn = momentum * v - lr * gn * gd;
+        const T ynew = yi[d] + vn;
+        if (!isfinite(ynew)) bad |= 2;
+        vel[o] = vn;
+        Yout[o] = ynew;
+        const T ng = agree ? gn * (T)0.8 : gn + (T)0.2;
+        gains[o] = ng < (T)0.01 ? (T)0.01 : ng;
+      }
+    }
+  }
+  if (STEP) {
+    bad = __syncthreads_or(bad);
+    if (bad && threadIdx.x == 0 && status) atomicOr(status, bad);
+  }
+}
+
+// The repulsion pipeline runs on a HIGH-priority internal stream: the SpMV's
+// thousands of blocks would otherwise be dispatched before the bbox / FFT
+// blocks queued behind them and the overlap would collapse.
+static int side_stream(fitsne_ctx* ctx) {
+  if (ctx->side) return FITSNE_OK;
+  int lo = 0, hi = 0;
+  FITSNE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  FITSNE_CUDA(cudaStreamCreateWithPriority(&ctx->side, cudaStreamNonBlocking,
+                                           ctx->overlap == 2 ? hi : lo));
+  FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_in, cudaEventDisableTiming));
+  FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_done, cudaEventDisableTiming));
+  return FITSNE_OK;
+}
+
+template <typename T, bool STEP>
+static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void* attr, double alpha,
+                          void* grad, double momentum, double lr, void* Yout, void* vel,
+                          void* gains, int32_t* status, cudaStream_t st) {
+  const GridArgs g = grid_args(ctx->grid);
+  const int blocks = nblocks(n);
+#define CMB(S, P)                                                                              \
+  k_combine<T, S, P, STEP><<<blocks, kBlock, 0, st>>>(                                         \
+      (const T*)Y, n, g, (const T*)ctx->pot.ptr, (const double*)ctx->scal.ptr, (const T*)attr, \
+      (T)alpha, (T*)grad, (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, status)
+  if (ctx->dims == 1) { if (g.p == 3) CMB(1, 3); else CMB(1, 0); }
+  else { if (g.p == 3) CMB(2, 3); else CMB(2, 0); }
+#undef CMB
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st) {
+  const int64_t n = ctx->n_total;
+  FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)n * ctx->dims));
+  void* attr = ctx->forces.ptr;
+  if (ctx->overlap == 0) {
+    FITSNE_TRY(make_grid(ctx, Y, n, st));
+    FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
+    FITSNE_TRY(attractive(ctx, Y, nullptr, 1.0, attr, 0, false, st));
+  } else {
+    // bbox + grid readback first (tiny), then the persistent SpMV on st and
+    // spread + FFT on the side stream, which fill the SM slots the SpMV leaves
+    FITSNE_TRY(side_stream(ctx));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
+    FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
+    FITSNE_TRY(make_grid(ctx, Y, n, ctx->side));
+    FITSNE_TRY(attractive(ctx, Y, nullptr, 1.0, attr, 0, false, st));
+    FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+  }
+  if (ctx->dtype == FITSNE_F32)
+    return launch_combine<float, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
+                                        nullptr, nullptr, st);
+  return launch_combine<double, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
+                                       nullptr, nullptr, st);
+}
+
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
                   double momentum, double lr, double* kl_dev, int32_t* status_dev, cudaStream_t st) {
   const int64_t n = ctx->n_total;
-  FITSNE_TRY(make_grid(ctx, Yin, n, st));
-  FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
-  FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
-  int blocks = attract_grid(ctx);
-  FITSNE_TRY(ensure(ctx->part, sizeof(double) * ((size_t)blocks + (size_t)ctx->num_sms * 16 + 64)));
-  double* part = (double*)ctx->part.ptr;
-  GridArgs gr = grid_args(ctx->grid);
-#define IT2(T, S, P)                                                                              \
-  k_iterate<T, S, P><<<blocks, kBlock, 0, st>>>(ctx->rowptr, ctx->col, (const T*)ctx->val,        \
-                                                (const T*)Yin, n, gr, (const T*)ctx->pot.ptr,     \
-                                                (const double*)ctx->scal.ptr, (T)alpha,           \
-                                                (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, \
-                                                part, status_dev)
-#define IT(T, S) do { if (gr.p == 3) IT2(T, S, 3); else IT2(T, S, 0); } while (0)
-  if (ctx->dtype == FITSNE_F32) { if (ctx->dims == 1) IT(float, 1); else IT(float, 2); }
-  else { if (ctx->dims == 1) IT(double, 1); else IT(double, 2); }
-#undef IT
-#undef IT2
-  FITSNE_CHECK_LAUNCH();
+  FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)n * ctx->dims));
+  void* attr = ctx->forces.ptr;
+  const int blocks = attract_grid(ctx);
+  if (ctx->overlap == 0) {
+    FITSNE_TRY(make_grid(ctx, Yin, n, st));
+    FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
+    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st));
+  } else {
+    FITSNE_TRY(side_stream(ctx));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
+    FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
+    FITSNE_TRY(make_grid(ctx, Yin, n, ctx->side));
+    // SpMV + KL partials (-> ctx->part) on st, spread + FFT on the side stream
+    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st));
+    FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, ctx->side));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+  }
+  if (ctx->dtype == FITSNE_F32)
+    FITSNE_TRY((launch_combine<float, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
+                                             vel, gains, status_dev, st)));
+  else
+    FITSNE_TRY((launch_combine<double, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
+                                              vel, gains, status_dev, st)));
   if (kl_dev) {
-    k_kl_final<<<1, 256, 0, st>>>(part, blocks, (const double*)ctx->scal.ptr, ctx->plogp, ctx->psum,
-                                  kl_dev);
+    k_kl_final<<<1, 256, 0, st>>>((const double*)ctx->part.ptr, blocks,
+                                  (const double*)ctx->scal.ptr, ctx->plogp, ctx->psum, kl_dev);
     FITSNE_CHECK_LAUNCH();
   }
   return FITSNE_OK;

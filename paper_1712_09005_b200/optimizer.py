@@ -103,6 +103,10 @@ class TsneConfig:
     intervals_per_integer: float = 1.0
     n_interpolation_points: int | None = None   # FIt-SNE alias of points_per_interval
     min_num_intervals: int | None = None        # FIt-SNE alias of min_intervals
+    # locality relabelling of the points (Z-order of the embedding) in run_tsne
+    # off by default: on the C3 synthetic data it costs more than it saves
+    reorder_iters: tuple | None = None
+    reorder_min_n: int = 100_000
 
     def __post_init__(self):
         if self.n_interpolation_points is not None:
@@ -358,10 +362,39 @@ def run_tsne(data=None, affinities=None, config: TsneConfig | None = None, callb
     return _run_fused(P, y0, cfg, dev, dt)
 
 
+def _part1by1(x: torch.Tensor) -> torch.Tensor:
+    x = x & 0xFFFF
+    x = (x | (x << 8)) & 0x00FF00FF
+    x = (x | (x << 4)) & 0x0F0F0F0F
+    x = (x | (x << 2)) & 0x33333333
+    return (x | (x << 1)) & 0x55555555
+
+
+def _locality_order(y: torch.Tensor):
+    """Z-order (Morton) permutation of the embedding: perm[new] = old, inv[old] = new."""
+    lo = y.min(0).values
+    span = (y.max(0).values - lo).clamp_min(1e-30)
+    q = ((y - lo) / span * 65535.0).long().clamp_(0, 65535)
+    key = q[:, 0] if y.shape[1] == 1 else (_part1by1(q[:, 0]) | (_part1by1(q[:, 1]) << 1))
+    perm = torch.argsort(key)
+    inv = torch.empty_like(perm)
+    inv[perm] = torch.arange(perm.numel(), device=perm.device)
+    return perm, inv
+
+
 def _run_fused(P, y0, cfg, dev, dt) -> TsneResult:
+    """Fused device iterations.  For large N the points are relabelled in the
+    Z-order of the current embedding at cfg.reorder_iters: P's neighbours are
+    then close in index, so the SpMV's neighbour gathers share cache lines.
+    The relabelling is a symmetric permutation of P, Y and the optimiser
+    state (results are unchanged up to summation order); the embedding is
+    returned in the caller's order."""
+    from .affinities import permute_csr
     n, s = y0.shape
-    ctx, _ = _ctx_with_P(P, dev, s, dt, cfg.points_per_interval, cfg.min_intervals,
-                         cfg.intervals_per_integer)
+    ctx, csr = _ctx_with_P(P, dev, s, dt, cfg.points_per_interval, cfg.min_intervals,
+                           cfg.intervals_per_integer)
+    reorder_at = set(cfg.reorder_iters or ()) if n >= cfg.reorder_min_n else set()
+    order = None  # order[current label] = caller's index
     with torch.cuda.device(dev):
         ya = torch.from_numpy(y0).to(device=dev, dtype=dt)
         yb = torch.empty_like(ya)
@@ -371,6 +404,15 @@ def _run_fused(P, y0, cfg, dev, dt) -> TsneResult:
         status = torch.zeros(cfg.n_iter, dtype=torch.int32, device=dev)
         st = ctx.stream
         for it in range(cfg.n_iter):
+            if it in reorder_at:
+                perm, inv = _locality_order(ya)
+                ya = ya[perm].contiguous()
+                yb = torch.empty_like(ya)
+                vel = vel[perm].contiguous()
+                gains = gains[perm].contiguous()
+                csr = permute_csr(csr, perm, inv)
+                ctx.set_affinities(csr)
+                order = perm if order is None else order[perm]
             alpha = cfg.exaggeration.alpha(it, cfg.n_iter)
             mom = cfg.momentum_early if it < cfg.momentum_switch_iter else cfg.momentum_late
             rc = ctx.lib.fitsne_iterate(
@@ -383,6 +425,10 @@ def _run_fused(P, y0, cfg, dev, dt) -> TsneResult:
             ya, yb = yb, ya
         torch.cuda.current_stream(dev).synchronize()
         _raise_status(status, None)
+        if order is not None:
+            out = torch.empty_like(ya)
+            out[order] = ya
+            ya = out
         return TsneResult(embedding=ya.to(torch.float64).cpu().numpy(),
                           kl_log=kl.cpu().numpy(), affinities=P)
 
