@@ -332,6 +332,243 @@ k_spread_sorted(const T* __restrict__ Y, const uint32_t* __restrict__ keys,
   }
 }
 
+// =============================================================================
+// v2 (grids with <= kSmemBoxes boxes): counting sort by box with a full
+// per-block shared-memory histogram, then one warp per (box, part).
+//   k_box_count   : keys + block histogram -> global counts (<= 1 atomic per
+//                   (block, box): contention bounded by the block count)
+//   k_box_scan    : exclusive scan of the counts (box offsets) and of the
+//                   per-box part counts ceil(cnt / kPart) (work items)
+//   k_box_scatter : block histogram again, one global reservation per
+//                   (block, box), then shared-memory slots; writes the
+//                   points' coordinates in box order
+//   k_box_reduce  : warp per (box, part): coalesced reads of the sorted
+//                   coordinates, register accumulation of the 9 x 3 node
+//                   values, one warp reduction, plain stores when the box has
+//                   one part (no atomics, no contention), atomics otherwise
+// =============================================================================
+static constexpr int kSmemBoxes = 48 * 1024;   // 192 KB of int counters
+static constexpr int kCountBlock = 1024;
+static constexpr int kPart = 512;              // points per reduce work item
+static constexpr int kGroup = 8;               // lanes per reduce work item
+
+template <typename T, int S>
+__global__ void __launch_bounds__(kCountBlock)
+k_box_count(const T* __restrict__ Y, int64_t n, GridArgs g, int nbox, int64_t chunk,
+            uint32_t* __restrict__ keys, uint32_t* __restrict__ counts) {
+  extern __shared__ uint32_t s_cnt[];
+  for (int b = threadIdx.x; b < nbox; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  const int64_t beg = blockIdx.x * chunk;
+  const int64_t end = (beg + chunk < n) ? beg + chunk : n;
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const uint32_t key = point_box<T, S>(Y, i, g);
+    keys[i] = key;
+    atomicAdd(&s_cnt[key], 1u);
+  }
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbox; b += blockDim.x) {
+    const uint32_t c = s_cnt[b];
+    if (c) atomicAdd(&counts[b], c);
+  }
+}
+
+// one block: offsets = exclusive scan of counts; items = exclusive scan of
+// ceil(count / kPart); cursor = offsets (for the scatter's reservations)
+__global__ void __launch_bounds__(1024)
+k_box_scan(const uint32_t* __restrict__ counts, int nbox, uint32_t* __restrict__ offsets,
+           uint32_t* __restrict__ cursor, uint32_t* __restrict__ items,
+           uint32_t* __restrict__ item_box) {
+  __shared__ uint32_t s_w[2][32];
+  __shared__ uint32_t s_carry[2];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  if (threadIdx.x == 0) { s_carry[0] = 0; s_carry[1] = 0; }
+  __syncthreads();
+  for (int c0 = 0; c0 <= nbox; c0 += blockDim.x) {
+    const int b = c0 + threadIdx.x;
+    const uint32_t x = (b < nbox) ? counts[b] : 0u;
+    const uint32_t y = (b < nbox) ? (x + kPart - 1) / kPart : 0u;
+    uint32_t ix = x, iy = y;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t ux = __shfl_up_sync(0xffffffffu, ix, o);
+      const uint32_t uy = __shfl_up_sync(0xffffffffu, iy, o);
+      if (lane >= o) { ix += ux; iy += uy; }
+    }
+    if (lane == 31) { s_w[0][wid] = ix; s_w[1][wid] = iy; }
+    __syncthreads();
+    uint32_t px = 0, py = 0, tx = 0, ty = 0;
+    for (int w = 0; w < nw; ++w) {
+      if (w < wid) { px += s_w[0][w]; py += s_w[1][w]; }
+      tx += s_w[0][w];
+      ty += s_w[1][w];
+    }
+    const uint32_t cx = s_carry[0], cy = s_carry[1];
+    if (b <= nbox) {
+      const uint32_t ox = cx + px + ix - x, oy = cy + py + iy - y;
+      offsets[b] = ox;
+      items[b] = oy;
+      if (b < nbox) {
+        cursor[b] = ox;
+        for (uint32_t k = 0; k < y; ++k) item_box[oy + k] = (uint32_t)b;
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) { s_carry[0] = cx + tx; s_carry[1] = cy + ty; }
+    __syncthreads();
+  }
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(kCountBlock)
+k_box_scatter(const T* __restrict__ Y, int64_t n, int nbox, int64_t chunk,
+              const uint32_t* __restrict__ keys, uint32_t* __restrict__ cursor,
+              T* __restrict__ ysorted) {
+  extern __shared__ uint32_t s_cnt[];
+  for (int b = threadIdx.x; b < nbox; b += blockDim.x) s_cnt[b] = 0;
+  __syncthreads();
+  const int64_t beg = blockIdx.x * chunk;
+  const int64_t end = (beg + chunk < n) ? beg + chunk : n;
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) atomicAdd(&s_cnt[__ldg(keys + i)], 1u);
+  __syncthreads();
+  for (int b = threadIdx.x; b < nbox; b += blockDim.x) {
+    const uint32_t c = s_cnt[b];
+    s_cnt[b] = c ? atomicAdd(&cursor[b], c) : 0u;   // this block's base in box b
+  }
+  __syncthreads();
+  for (int64_t i = beg + threadIdx.x; i < end; i += blockDim.x) {
+    const uint32_t slot = atomicAdd(&s_cnt[__ldg(keys + i)], 1u);
+#pragma unroll
+    for (int d = 0; d < S; ++d) ysorted[(size_t)slot * S + d] = Y[i * S + d];
+  }
+}
+
+template <typename T, int S>
+__global__ void __launch_bounds__(256)
+k_box_reduce(const T* __restrict__ ysorted, const uint32_t* __restrict__ offsets,
+             const uint32_t* __restrict__ items, const uint32_t* __restrict__ item_box, int nbox,
+             GridArgs g, T* __restrict__ acc) {
+  // one group of kGroup lanes per work item (box, part); kGroup-lane shuffles
+  constexpr int NN = (S == 2) ? 9 : 3;
+  constexpr int NC = S + 1;
+  const int gl = threadIdx.x & (kGroup - 1);
+  const int64_t item = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) / kGroup;
+  const uint32_t total = __ldg(items + nbox);
+  const bool live = item < (int64_t)total;
+  int box = 0;
+  uint32_t p0 = 0, p1 = 0;
+  bool whole = true;
+  if (live) {
+    box = (int)__ldg(item_box + item);
+    const uint32_t part = (uint32_t)item - __ldg(items + box);
+    const uint32_t b0 = __ldg(offsets + box), b1 = __ldg(offsets + box + 1);
+    p0 = b0 + part * kPart;
+    p1 = (p0 + kPart < b1) ? p0 + kPart : b1;
+    whole = (b1 - b0) <= (uint32_t)kPart;
+  }
+  using W = typename std::conditional<sizeof(T) == 4, float, double>::type;
+  W v[NN][NC];
+#pragma unroll
+  for (int m = 0; m < NN; ++m)
+#pragma unroll
+    for (int c = 0; c < NC; ++c) v[m][c] = 0;
+  for (uint32_t k = p0 + gl; k < p1; k += kGroup) {
+    T y[S];
+#pragma unroll
+    for (int d = 0; d < S; ++d) y[d] = ysorted[(size_t)k * S + d];
+    W wx[3], wy[3] = {1, 0, 0};
+    if constexpr (sizeof(T) == 4) {
+      box_weights3_f32((float)y[0], g.lo[0], g.h[0], g.lo_f[0], g.invh_f[0], g.guard[0], g.n_int, wx);
+      if (S == 2)
+        box_weights3_f32((float)y[S - 1], g.lo[S - 1], g.h[S - 1], g.lo_f[S - 1], g.invh_f[S - 1],
+                         g.guard[S - 1], g.n_int, wy);
+    } else {
+      box_weights((double)y[0], g.lo[0], g.h[0], g.n_int, 3, wx);
+      if (S == 2) box_weights((double)y[S - 1], g.lo[S - 1], g.h[S - 1], g.n_int, 3, wy);
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int bb = 0; bb < ((S == 2) ? 3 : 1); ++bb) {
+        const int m = (S == 2) ? a * 3 + bb : a;
+        const W w = wx[a] * wy[bb];
+        v[m][0] += w;
+        v[m][1] += w * (W)y[0];
+        if (S == 2) v[m][2] += w * (W)y[S - 1];
+      }
+  }
+#pragma unroll
+  for (int m = 0; m < NN; ++m)
+#pragma unroll
+    for (int c = 0; c < NC; ++c)
+#pragma unroll
+      for (int o = kGroup / 2; o > 0; o >>= 1) v[m][c] += __shfl_xor_sync(0xffffffffu, v[m][c], o, kGroup);
+  if (!live) return;
+  const uint32_t cx = (S == 2) ? (uint32_t)box / (uint32_t)g.n_int : (uint32_t)box;
+  const uint32_t cy = (S == 2) ? (uint32_t)box - cx * (uint32_t)g.n_int : 0u;
+#pragma unroll
+  for (int m = 0; m < NN; ++m) {
+    if ((m % kGroup) != gl) continue;   // group lane gl writes nodes gl, gl + kGroup
+    const int a = (S == 2) ? m / 3 : m, bb = (S == 2) ? m % 3 : 0;
+    const int64_t node = (S == 2) ? (((int64_t)cx * 3 + a) * g.n + (int64_t)cy * 3 + bb)
+                                  : ((int64_t)cx * 3 + a);
+    T* dst = acc + node * kNodeSlots;
+    if (whole) {
+      dst[0] = (T)v[m][0];
+      dst[1] = (T)v[m][1];
+      if (S == 2) dst[2] = (T)v[m][2];
+    } else {
+      flush_node<T>(acc, node, (T)v[m][0], (T)v[m][1], (S == 2) ? (T)v[m][2] : (T)0);
+    }
+  }
+}
+
+static int spread_counting(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, int nbox,
+                           cudaStream_t st) {
+  const GridArgs g = grid_args(ctx->grid);
+  const int S = ctx->dims;
+  const size_t es = dsize(ctx->dtype);
+  // blocks: ~2 per SM, contiguous chunks
+  int nblk = 2 * ctx->num_sms;
+  int64_t chunk = (n + nblk - 1) / nblk;
+  if (chunk < 4096) { chunk = 4096; nblk = (int)((n + chunk - 1) / chunk); }
+  const int64_t max_items = (int64_t)nbox + (n + kPart - 1) / kPart;
+  const size_t ints = 4 * (size_t)nbox + (size_t)max_items + 16;
+  const size_t bytes = sizeof(uint32_t) * ((size_t)n + ints) + es * S * (size_t)n + 256;
+  FITSNE_TRY(ensure(ctx->sortbuf, bytes));
+  uint32_t* keys = (uint32_t*)ctx->sortbuf.ptr;
+  uint32_t* counts = keys + n;
+  uint32_t* offsets = counts + nbox + 1;
+  uint32_t* cursor = offsets + nbox + 1;
+  uint32_t* items = cursor + nbox + 1;
+  uint32_t* item_box = items + nbox + 2;
+  void* ysorted = (void*)(((uintptr_t)(item_box + max_items + 2) + 15) & ~(uintptr_t)15);
+  FITSNE_CUDA(cudaMemsetAsync(counts, 0, sizeof(uint32_t) * nbox, st));
+  const size_t smem = sizeof(uint32_t) * (size_t)nbox;
+#define LAUNCH2(T, SS)                                                                          \
+  do {                                                                                         \
+    FITSNE_CUDA(cudaFuncSetAttribute((const void*)k_box_count<T, SS>,                          \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    FITSNE_CUDA(cudaFuncSetAttribute((const void*)k_box_scatter<T, SS>,                        \
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));  \
+    k_box_count<T, SS><<<nblk, kCountBlock, smem, st>>>((const T*)Y, n, g, nbox, chunk, keys,  \
+                                                        counts);                               \
+    FITSNE_CHECK_LAUNCH();                                                                     \
+    k_box_scan<<<1, 1024, 0, st>>>(counts, nbox, offsets, cursor, items, item_box);            \
+    FITSNE_CHECK_LAUNCH();                                                                     \
+    k_box_scatter<T, SS><<<nblk, kCountBlock, smem, st>>>((const T*)Y, n, nbox, chunk, keys,   \
+                                                          cursor, (T*)ysorted);                \
+    FITSNE_CHECK_LAUNCH();                                                                     \
+    k_box_reduce<T, SS><<<(int)((max_items * kGroup + 255) / 256), 256, 0, st>>>(              \
+        (const T*)ysorted, offsets, items, item_box, nbox, g, (T*)accum);                      \
+    FITSNE_CHECK_LAUNCH();                                                                     \
+  } while (0)
+  if (ctx->dtype == FITSNE_F32) { if (S == 1) LAUNCH2(float, 1); else LAUNCH2(float, 2); }
+  else { if (S == 1) LAUNCH2(double, 1); else LAUNCH2(double, 2); }
+#undef LAUNCH2
+  return FITSNE_OK;
+}
+
 // Sorted spread entry: returns FITSNE_EINVAL when this path does not apply
 // (p != 3), in which case the caller uses the direct scatter.
 int spread_sorted(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
@@ -339,6 +576,7 @@ int spread_sorted(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaSt
   if (g.p != 3 || n <= 0 || n > 0x7fffffffLL) return FITSNE_EINVAL;
   const int S = ctx->dims;
   const uint64_t nbox = (S == 2) ? (uint64_t)g.n_int * g.n_int : (uint64_t)g.n_int;
+  if (nbox <= (uint64_t)kSmemBoxes) return spread_counting(ctx, Y, n, accum, (int)nbox, st);
   int bits = 1;
   while (bits < 32 && ((uint64_t)1 << bits) < nbox) ++bits;
   const int passes = (bits + 7) / 8;

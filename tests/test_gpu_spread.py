@@ -62,3 +62,18 @@ def test_sorted_spread_matches_bincount(cuda, case, dims, dtype):
     for c in range(dims + 1):
         assert rel_inf(a[:, c], ref[:, c]) <= tol, c
         assert rel_inf(b[:, c], ref[:, c]) <= tol, c
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+def test_sorted_spread_large_grid_radix_path(cuda, dtype):
+    """> 48k boxes: the LSD-radix variant of the sorted spread."""
+    rng = np.random.default_rng(9)
+    y = rng.uniform(-200, 200, (60_000, 2))
+    if dtype == "float32":
+        y = y.astype(np.float32).astype(np.float64)
+    a, g = _spread(y, dtype, True, 2)
+    assert g.n_intervals ** 2 > 48 * 1024
+    ref = _oracle(y, g, 2)
+    tol = 1e-12 if dtype == "float64" else 5e-4
+    for c in range(3):
+        assert rel_inf(a[:, c], ref[:, c]) <= tol, c

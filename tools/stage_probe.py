@@ -12,7 +12,13 @@ ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--case", default="blobs")
 a = ap.parse_args()
 rng = np.random.default_rng(0)
-if a.case == "blobs":
+if a.case == "c3like":
+    # 40 power-law-sized anisotropic blobs, span ~200 (n_int ~ 200 < 219: counting-sort path)
+    w = np.arange(1, 41, dtype=float) ** -1.5; w /= w.sum()
+    lab = rng.choice(40, a.n, p=w)
+    c = rng.uniform(-70, 70, (40, 2)); s = rng.uniform(3, 15, (40, 2))
+    y = c[lab] + s[lab] * rng.standard_normal((a.n, 2))
+elif a.case == "blobs":
     c = rng.uniform(-80, 80, (40, 2)); s = rng.uniform(2, 12, 40)
     lab = rng.integers(0, 40, a.n)
     y = c[lab] + s[lab, None] * rng.standard_normal((a.n, 2))
