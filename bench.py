@@ -69,6 +69,7 @@ def parse():
     ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2],
                     help="0 serial, 1 (default) SpMV || repulsion, 2 + priority repulsion stream")
     ap.add_argument("--spmv-blocks", type=int, default=0, help="persistent SpMV blocks per SM (0: one tile per warp)")
+    ap.add_argument("--spread-replicas", type=int, default=4, help="spread accumulator replicas")
     return ap.parse_args()
 
 
@@ -273,6 +274,7 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, args.spread_mode), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, args.overlap_mode), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 3, args.spmv_blocks), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, args.spread_replicas), "set_option")
     g = torch.empty_like(y)
     zc = __import__("ctypes").c_double()
 

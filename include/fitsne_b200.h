@@ -85,8 +85,12 @@ int fitsne_set_interp(fitsne_ctx* ctx, int points_per_interval, int min_interval
 enum fitsne_option {
   FITSNE_OPT_SORTED_SPREAD = 1,
   FITSNE_OPT_OVERLAP = 2,
-  FITSNE_OPT_SPMV_BLOCKS_PER_SM = 3
+  FITSNE_OPT_SPMV_BLOCKS_PER_SM = 3,
+  FITSNE_OPT_SPREAD_REPLICAS = 4
 };
+/*   FITSNE_OPT_SPREAD_REPLICAS: power of two (default 4): warps of the direct
+ *   spread add into one of this many accumulator copies (summed by the FFT row
+ *   stage), dividing same-address atomic contention in crowded boxes. */
 /*   FITSNE_OPT_OVERLAP: 0 = serial; 1 (default) = persistent attractive SpMV on
  *   the caller's stream overlapping spread/FFT on an internal stream; 2 = same
  *   with the internal stream at high priority.

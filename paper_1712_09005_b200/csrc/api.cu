@@ -161,6 +161,17 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     ctx->overlap = value;
     return FITSNE_OK;
   }
+  if (option == FITSNE_OPT_SPREAD_REPLICAS) {
+    if (value < 1 || value > 16 || (value & (value - 1))) {
+      set_error("spread replicas must be a power of two in [1, 16]");
+      return FITSNE_EINVAL;
+    }
+    if (value != ctx->spread_replicas) {
+      ctx->spread_replicas = value;
+      ctx->accum_clean = false;   // re-zero the (possibly larger) accumulator
+    }
+    return FITSNE_OK;
+  }
   if (option == FITSNE_OPT_SPMV_BLOCKS_PER_SM) {
     if (value < 0 || value > 32) { set_error("SpMV blocks per SM must be in [0, 32]"); return FITSNE_EINVAL; }
     ctx->spmv_blocks_per_sm = value;

@@ -130,6 +130,7 @@ struct fitsne_ctx {
   fitsne::DevBuf gen;       // generic scratch
   fitsne::DevBuf sortbuf;   // box sort keys / values / histograms
   int sorted_spread = 1;      // box-sorted spread (p = 3): 0 never, 1 when crowded, 2 always
+  int spread_replicas = 4;    // replicas of the internal spread accumulator (power of two)
   int overlap = 1;                 // 0 serial, 1 SpMV || repulsion, 2 same + priority repulsion
   int spmv_blocks_per_sm = 0;      // >0: persistent SpMV grid in the overlap modes
   cudaStream_t side = nullptr;     // repulsion stream (overlaps the attractive SpMV)

@@ -258,10 +258,16 @@ int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
 // a2/a3: box assignment + Lagrange weights, spreading
 // =============================================================================
 // t-SNE charges (1, y_0[, y_1]) of each point into 4-slot node records.
+// nrep > 1: warps add into one of nrep replicas of the accumulator (replica =
+// warp index mod nrep, stride rstride elements) so the points of a crowded
+// box do not all serialise on the same L2 addresses; the row-FFT stage sums
+// the replicas when it reads the grid.
 template <typename T, int S, int P>
-__global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T* __restrict__ acc) {
+__global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T* __restrict__ acc,
+                              int nrep, int64_t rstride) {
   int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (i >= n) return;
+  acc += (int64_t)((threadIdx.x >> 5) & (nrep - 1)) * rstride;
   if constexpr (sizeof(T) == 4 && P == 3 && S == 2) {
     // fp32 mode, p = 3: guarded fp32 box estimate (exact indices), fp32 weights
     const float2 yy = __ldg(reinterpret_cast<const float2*>(Y) + i);
@@ -320,9 +326,10 @@ __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T*
 }
 
 template <typename T, int S>
-static void launch_spread_tsne(const T* Y, int64_t n, const GridArgs& g, T* acc, cudaStream_t st) {
-  if (g.p == 3) k_spread_tsne<T, S, 3><<<grid_for(n), kBlock, 0, st>>>(Y, n, g, acc);
-  else k_spread_tsne<T, S, 0><<<grid_for(n), kBlock, 0, st>>>(Y, n, g, acc);
+static void launch_spread_tsne(const T* Y, int64_t n, const GridArgs& g, T* acc, int nrep,
+                               int64_t rstride, cudaStream_t st) {
+  if (g.p == 3) k_spread_tsne<T, S, 3><<<grid_for(n), kBlock, 0, st>>>(Y, n, g, acc, nrep, rstride);
+  else k_spread_tsne<T, S, 0><<<grid_for(n), kBlock, 0, st>>>(Y, n, g, acc, nrep, rstride);
 }
 
 static size_t accum_elems(const fitsne_grid& g) {
@@ -331,8 +338,14 @@ static size_t accum_elems(const fitsne_grid& g) {
   return G * kNodeSlots;
 }
 
+// replicas of the internal accumulator (power of two; 1 for caller buffers)
+static int accum_reps(fitsne_ctx* ctx, const void* accum) {
+  if (ctx->dims == 1) return 1;
+  return (accum == nullptr || accum == ctx->accum.ptr) ? ctx->spread_replicas : 1;
+}
+
 static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
-  size_t bytes = accum_elems(ctx->grid) * dsize(ctx->dtype);
+  size_t bytes = accum_elems(ctx->grid) * dsize(ctx->dtype) * (size_t)ctx->spread_replicas;
   if (ctx->accum.cap < bytes) {
     FITSNE_TRY(ensure(ctx->accum, bytes));
     ctx->accum_clean = false;
@@ -347,6 +360,8 @@ static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
 int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
   if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
   GridArgs g = grid_args(ctx->grid);
+  const int nrep = accum_reps(ctx, accum);
+  const int64_t rstride = (int64_t)accum_elems(ctx->grid);
   if (accum == nullptr) {
     FITSNE_TRY(ensure_accum(ctx, st));
     accum = ctx->accum.ptr;
@@ -369,11 +384,11 @@ int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
   }
   if (n > 0) {
     if (ctx->dtype == FITSNE_F32) {
-      if (ctx->dims == 1) launch_spread_tsne<float, 1>((const float*)Y, n, g, (float*)accum, st);
-      else launch_spread_tsne<float, 2>((const float*)Y, n, g, (float*)accum, st);
+      if (ctx->dims == 1) launch_spread_tsne<float, 1>((const float*)Y, n, g, (float*)accum, nrep, rstride, st);
+      else launch_spread_tsne<float, 2>((const float*)Y, n, g, (float*)accum, nrep, rstride, st);
     } else {
-      if (ctx->dims == 1) launch_spread_tsne<double, 1>((const double*)Y, n, g, (double*)accum, st);
-      else launch_spread_tsne<double, 2>((const double*)Y, n, g, (double*)accum, st);
+      if (ctx->dims == 1) launch_spread_tsne<double, 1>((const double*)Y, n, g, (double*)accum, nrep, rstride, st);
+      else launch_spread_tsne<double, 2>((const double*)Y, n, g, (double*)accum, nrep, rstride, st);
     }
     FITSNE_CHECK_LAUNCH();
   }
@@ -517,7 +532,8 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int pair0, int npair,
                typename C2<T>::type* __restrict__ F, typename C2<T>::type* __restrict__ Sbuf,
-               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int merged) {
+               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int merged,
+               int nrep, int64_t rstride) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = g.L, n = g.n;
@@ -541,13 +557,15 @@ k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int 
           const int y = y0 + u * blockDim.x;
           rv[u][0] = rv[u][1] = rv[u][2] = 0;
           if (y < n) {
-            T* rec = acc + ((size_t)x * n + y) * kNodeSlots;
-            if constexpr (sizeof(T) == 4) {
-              const float4 f = *reinterpret_cast<const float4*>(rec);
-              rv[u][0] = f.x; rv[u][1] = f.y; rv[u][2] = f.z;
-            } else {
-              const double2 f0 = *reinterpret_cast<const double2*>(rec);
-              rv[u][0] = f0.x; rv[u][1] = f0.y; rv[u][2] = rec[2];
+            for (int rp = 0; rp < nrep; ++rp) {  // sum the spread replicas
+              T* rec = acc + (size_t)rp * rstride + ((size_t)x * n + y) * kNodeSlots;
+              if constexpr (sizeof(T) == 4) {
+                const float4 f = *reinterpret_cast<const float4*>(rec);
+                rv[u][0] += f.x; rv[u][1] += f.y; rv[u][2] += f.z;
+              } else {
+                const double2 f0 = *reinterpret_cast<const double2*>(rec);
+                rv[u][0] += f0.x; rv[u][1] += f0.y; rv[u][2] += rec[2];
+              }
             }
           }
         }
@@ -562,9 +580,11 @@ k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int 
           a[PL + pidx(y)] = B;
           if (y < n) {
             // consume-and-clear: leaves the accumulator zeroed for the next spread
-            T* rec = acc + ((size_t)x * n + y) * kNodeSlots;
-            if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(rec) = make_float4(0.f, 0.f, 0.f, 0.f);
-            else { rec[0] = 0; rec[1] = 0; rec[2] = 0; }
+            for (int rp = 0; rp < nrep; ++rp) {
+              T* rec = acc + (size_t)rp * rstride + ((size_t)x * n + y) * kNodeSlots;
+              if constexpr (sizeof(T) == 4) *reinterpret_cast<float4*>(rec) = make_float4(0.f, 0.f, 0.f, 0.f);
+              else { rec[0] = 0; rec[1] = 0; rec[2] = 0; }
+            }
           }
         }
       } else {
@@ -984,8 +1004,9 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
     const int merged = sizeof(V) * ((size_t)L + 2 * (size_t)(nd + 1) * plen(L)) <= 113 * 1024 ? 1 : 0;
     size_t smem_r = sizeof(V) * ((size_t)L + 2 * (size_t)(merged ? nd + 1 : std::max(nd, 1)) * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
-    k_rows_forward<T, MODE><<<merged ? n : 2 * n, 256, smem_r, st>>>(accum, coeffs, ncol, pair0,
-                                                                     npair, F, Sb, g, tw, pl, merged);
+    k_rows_forward<T, MODE><<<merged ? n : 2 * n, 256, smem_r, st>>>(
+        accum, coeffs, ncol, pair0, npair, F, Sb, g, tw, pl, merged, accum_reps(ctx, accum),
+        (int64_t)accum_elems(gr));
     FITSNE_CHECK_LAUNCH();
     if (pair0 == 0) {
       size_t smem_s = sizeof(V) * ((size_t)L + 2 * (size_t)kSpecCols * plen(L));
