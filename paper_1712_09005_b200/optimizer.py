@@ -344,13 +344,22 @@ def run_tsne(data=None, affinities=None, config: TsneConfig | None = None, callb
         raise ValueError("provide exactly one of data or affinities")
     seeds = np.random.SeedSequence(cfg.seed).spawn(3)
     if data is not None:
-        raise NotImplementedError(
-            "run_tsne(data=...) needs the affinity pipeline (kNN + perplexity + symmetrize), "
-            "which is outside this package's hot path; compute P with "
-            "fftsne.affinities.affinities_from_data and pass affinities=P"
-        )
-    P = affinities
-    _validate_affinities(P)
+        # (PCA ->) affinities on the device (optimizer.py:351-372; affinity_build.py)
+        from .affinity_build import AffinityConfig, affinities_from_data, pca_reduce
+        x = np.asarray(data, dtype=float)
+        if x.ndim != 2:
+            raise ValueError("data must be (N, d)")
+        dev0 = cfg.device if cfg.device is not None else A.device_of()
+        if cfg.pca_dims is not None and x.shape[1] > cfg.pca_dims:
+            x = pca_reduce(x, cfg.pca_dims, seed=int(seeds[2].generate_state(1)[0]), device=dev0)
+        aff_cfg = AffinityConfig(perplexity=cfg.perplexity, n_neighbors=cfg.n_neighbors,
+                                 method=cfg.knn_method, n_trees=cfg.n_trees,
+                                 subsample=cfg.subsample,
+                                 seed=int(seeds[0].generate_state(1)[0]))
+        P, _ = affinities_from_data(x, aff_cfg, device=dev0)
+    else:
+        P = affinities
+        _validate_affinities(P)
     n = n_points(P)
     rng = np.random.default_rng(seeds[1])
     y0 = rng.normal(0.0, 1e-4, size=(n, cfg.dims))          # optimizer.py:378-379
