@@ -31,8 +31,11 @@ static inline int nblocks(int64_t n, int block = kBlock) {
 
 template <typename T>
 __device__ __forceinline__ T fast_log1p(T x);
+// fp32: SFU log of (1 + x) (2 ulp-level error for 1+x in normal range; for
+// x below 2^-24 it returns 0 where log1p returns ~x, a p*x term that is far
+// below the KL's fp32 resolution)
 template <>
-__device__ __forceinline__ float fast_log1p<float>(float x) { return log1pf(x); }
+__device__ __forceinline__ float fast_log1p<float>(float x) { return __logf(1.0f + x); }
 template <>
 __device__ __forceinline__ double fast_log1p<double>(double x) { return log1p(x); }
 
@@ -268,7 +271,7 @@ static int launch_attract(fitsne_ctx* ctx, const T* Y, const T* frep, T alpha, T
 }
 
 int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double alpha, void* out,
-               int mode, bool kl, cudaStream_t st) {
+               int mode, bool kl, cudaStream_t st, bool fold) {
   if (!ctx->rowptr) { set_error("no affinities registered"); return FITSNE_EINVAL; }
   if (mode == 2 && !ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
   const int blocks = attract_grid(ctx);
@@ -281,8 +284,8 @@ int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double al
   else
     FITSNE_TRY(launch_attract<double>(ctx, (const double*)Yfull, (const double*)forces, alpha,
                                       (double*)out, mode, kl, part, blocks, st));
-  if (kl) {
-    k_fold<<<1, 256, 0, st>>>(part, blocks, (double*)ctx->scal.ptr + 1);
+  if (kl && fold) {
+    k_fold<<<1, 1024, 0, st>>>(part, blocks, (double*)ctx->scal.ptr + 1);
     FITSNE_CHECK_LAUNCH();
   }
   return FITSNE_OK;
@@ -626,14 +629,14 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
     FITSNE_TRY(make_grid(ctx, Yin, n, st));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
-    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st));
+    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st, false));
   } else {
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
     FITSNE_TRY(make_grid(ctx, Yin, n, ctx->side));
     // SpMV + KL partials (-> ctx->part) on st, spread + FFT on the side stream
-    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st));
+    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st, false));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
@@ -646,7 +649,7 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
     FITSNE_TRY((launch_combine<double, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
                                               vel, gains, status_dev, st)));
   if (kl_dev) {
-    k_kl_final<<<1, 256, 0, st>>>((const double*)ctx->part.ptr, blocks,
+    k_kl_final<<<1, 1024, 0, st>>>((const double*)ctx->part.ptr, blocks,
                                   (const double*)ctx->scal.ptr, ctx->plogp, ctx->psum, kl_dev);
     FITSNE_CHECK_LAUNCH();
   }

@@ -41,8 +41,10 @@ int exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* q, int nq
                 int include_self, void* out, cudaStream_t st);
 
 // attractive / KL / step ------------------------------------------------------------
+// fold=false leaves the KL partials in ctx->part (the caller folds them)
 int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double alpha,
-               void* out, int mode, bool kl, cudaStream_t st);  // mode 0 F_attr, 1 grad(forces), 2 grad(fused gather)
+               void* out, int mode, bool kl, cudaStream_t st,
+               bool fold = true);  // mode 0 F_attr, 1 grad(forces), 2 grad(fused gather)
 int kl_sum(fitsne_ctx* ctx, const void* Yfull, cudaStream_t st);  // -> scal[1] = sum p log1p(d2)
 int compute_plogp(fitsne_ctx* ctx, cudaStream_t st);
 int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gains, int64_t n,

@@ -349,8 +349,8 @@ k_spread_sorted(const T* __restrict__ Y, const uint32_t* __restrict__ keys,
 // =============================================================================
 static constexpr int kSmemBoxes = 48 * 1024;   // 192 KB of int counters
 static constexpr int kCountBlock = 1024;
-static constexpr int kPart = 512;              // points per reduce work item
-static constexpr int kGroup = 8;               // lanes per reduce work item
+static constexpr int kPart = 256;              // points per reduce work item
+static constexpr int kGroup = 32;              // lanes per reduce work item (a warp)
 
 template <typename T, int S>
 __global__ void __launch_bounds__(kCountBlock)
