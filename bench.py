@@ -84,8 +84,41 @@ class ClockSampler:
         self.samples = []
         self._stop = threading.Event()
         self._t = None
+        self._nvml = None
+        self.error = None
+
+    def _nvml_open(self):
+        import pynvml as N
+        N.nvmlInit()
+        h = N.nvmlDeviceGetHandleByIndex(self.index)
+        self._nvml = (N, h, N.nvmlDeviceGetMaxClockInfo(h, N.NVML_CLOCK_SM))
+
+    def _nvml_sample(self):
+        N, h, mx = self._nvml
+        sm = N.nvmlDeviceGetClockInfo(h, N.NVML_CLOCK_SM)
+        try:
+            r = N.nvmlDeviceGetCurrentClocksEventReasons(h)
+        except Exception:
+            r = N.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+        row = [str(sm), str(mx), "", "", "", "", ""]
+        for b, pos in ((N.nvmlClocksThrottleReasonHwSlowdown, 3),
+                       (N.nvmlClocksThrottleReasonHwThermalSlowdown, 4),
+                       (N.nvmlClocksThrottleReasonSwThermalSlowdown, 5),
+                       (N.nvmlClocksThrottleReasonSwPowerCap, 6)):
+            row[pos] = "Active" if (r & b) else "Not Active"
+        self.samples.append(row)
 
     def _run(self):
+        if self._nvml is not None:
+            # NVML every ~2 ms: the timed region is only tens of milliseconds
+            while not self._stop.is_set():
+                try:
+                    self._nvml_sample()
+                except Exception as e:  # noqa: BLE001
+                    self.error = repr(e)
+                    return
+                self._stop.wait(0.002)
+            return
         while not self._stop.is_set():
             try:
                 out = subprocess.run(
@@ -94,22 +127,36 @@ class ClockSampler:
                 parts = [p.strip() for p in out.stdout.strip().split(",")]
                 if len(parts) >= 7:
                     self.samples.append(parts)
-            except Exception:
-                pass
+            except Exception as e:  # noqa: BLE001
+                self.error = repr(e)
             self._stop.wait(0.1)
 
     def __enter__(self):
+        # open NVML before the timed region starts; the first sample is taken
+        # synchronously so even a very short region is covered
+        try:
+            self._nvml_open()
+            self._nvml_sample()
+        except Exception as e:  # noqa: BLE001
+            self._nvml = None
+            self.error = repr(e)
         self._t = threading.Thread(target=self._run, daemon=True)
         self._t.start()
         return self
 
     def __exit__(self, *a):
+        if self._nvml is not None:
+            try:
+                self._nvml_sample()
+            except Exception:  # noqa: BLE001
+                pass
         self._stop.set()
         self._t.join(timeout=10)
 
     def summary(self):
         if not self.samples:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"],
+                    "error": self.error}
         sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
         mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
@@ -117,7 +164,8 @@ class ClockSampler:
                           if s[3 + k].lower() == "active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.samples)}
+                "samples": len(self.samples),
+                "source": "nvml" if self._nvml is not None else "nvidia-smi"}
 
 
 # ----------------------------------------------------------------------------- data
