@@ -86,16 +86,22 @@ enum fitsne_option {
   FITSNE_OPT_SORTED_SPREAD = 1,
   FITSNE_OPT_OVERLAP = 2,
   FITSNE_OPT_SPMV_BLOCKS_PER_SM = 3,
-  FITSNE_OPT_SPREAD_REPLICAS = 4
+  FITSNE_OPT_SPREAD_REPLICAS = 4,
+  FITSNE_OPT_TILED_SPMV = 5,
+  FITSNE_OPT_TILE_ROWS = 6,
+  FITSNE_OPT_TILE_COLS = 7,
+  FITSNE_OPT_TILED_CTAS = 8
 };
-/*   FITSNE_OPT_SPREAD_REPLICAS: power of two (default 4): warps of the direct
- *   spread add into one of this many accumulator copies (summed by the FFT row
- *   stage), dividing same-address atomic contention in crowded boxes. */
-/*   FITSNE_OPT_OVERLAP: 0 = serial; 1 (default) = persistent attractive SpMV on
- *   the caller's stream overlapping spread/FFT on an internal stream; 2 = same
- *   with the internal stream at high priority.
- *   FITSNE_OPT_SPMV_BLOCKS_PER_SM: persistent SpMV grid size in the overlap
- *   modes (default 5 blocks of 256 threads per SM). */
+/*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
+ *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
+ *   column-chunk tiles (sliced-ELL inside each tile) whose column chunk of Y
+ *   is staged in shared memory by bulk copies; 2 = tiled whenever applicable.
+ *   The tiled copy is built on first use after fitsne_set_affinities.
+ *   FITSNE_OPT_TILE_ROWS / FITSNE_OPT_TILE_COLS: tile shape (rows per row
+ *   block, default 4096; points per column chunk, default 6144); both even and
+ *   <= 16384.  Shapes whose shared-memory footprint (24 rows + 16 cols + 4.3
+ *   rows bytes) exceeds 226 KiB use the CSR kernel.  FITSNE_OPT_TILED_CTAS:
+ *   persistent grid of the tiled kernel (default 0 = one CTA per SM). */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 
 /* --- a1: make_grid (nbody.py:118-150).  Device bbox reduction + fp64 grid

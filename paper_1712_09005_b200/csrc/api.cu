@@ -121,6 +121,7 @@ int fitsne_destroy(fitsne_ctx* c) {
   DevBuf* bufs[] = {&c->accum, &c->fbuf, &c->sbuf, &c->pot, &c->tw, &c->zpart, &c->bbox_part,
                     &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf};
   for (DevBuf* b : bufs) release(*b);
+  free_tiled(c);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->side) cudaStreamDestroy(c->side);
@@ -175,6 +176,27 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
   if (option == FITSNE_OPT_SPMV_BLOCKS_PER_SM) {
     if (value < 0 || value > 32) { set_error("SpMV blocks per SM must be in [0, 32]"); return FITSNE_EINVAL; }
     ctx->spmv_blocks_per_sm = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_TILED_SPMV) {
+    if (value < 0 || value > 2) { set_error("tiled SpMV mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    ctx->tiled_spmv = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_TILE_ROWS || option == FITSNE_OPT_TILE_COLS) {
+    if (value < 2 || value > 16384 || (value & 1)) {
+      set_error("tile rows / cols must be even and in [2, 16384]");
+      return FITSNE_EINVAL;
+    }
+    const int R = option == FITSNE_OPT_TILE_ROWS ? value : ctx->tile_rows;
+    const int C = option == FITSNE_OPT_TILE_COLS ? value : ctx->tile_cols;
+    ctx->tile_rows = R;
+    ctx->tile_cols = C;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_TILED_CTAS) {
+    if (value < 0 || value > 65536) { set_error("tiled CTAs must be in [0, 65536]"); return FITSNE_EINVAL; }
+    ctx->tiled_ctas = value;
     return FITSNE_OK;
   }
   set_error("unknown option");
@@ -320,6 +342,7 @@ int fitsne_set_affinities(fitsne_ctx* ctx, const int64_t* rowptr, const int32_t*
   ctx->n_total = n_total;
   ctx->nnz = nnz;
   ctx->plogp_valid = false;
+  free_tiled(ctx);  // contents may have changed: re-tile on next use
   return FITSNE_OK;
 }
 

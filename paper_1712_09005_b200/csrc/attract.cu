@@ -274,6 +274,21 @@ int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double al
                int mode, bool kl, cudaStream_t st, bool fold) {
   if (!ctx->rowptr) { set_error("no affinities registered"); return FITSNE_EINVAL; }
   if (mode == 2 && !ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  if (mode != 2 && tiled_usable(ctx, Yfull, st)) {
+    void* fattr = nullptr;
+    double* part = nullptr;
+    int np = 0;
+    FITSNE_TRY(attract_tiled(ctx, Yfull, kl, st, &fattr, &part, &np));
+    FITSNE_TRY(tiled_finish(ctx, forces, alpha, mode, out, st));
+    ctx->kl_part = part;
+    ctx->kl_nparts = np;
+    if (kl && fold) {
+      k_fold<<<1, 1024, 0, st>>>(part, np, (double*)ctx->scal.ptr + 1);
+      FITSNE_CHECK_LAUNCH();
+    }
+    return FITSNE_OK;
+  }
   const int blocks = attract_grid(ctx);
   FITSNE_TRY(ensure(ctx->part, sizeof(double) * ((size_t)blocks + (size_t)ctx->num_sms * 16 + 64)));
   FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
@@ -284,6 +299,8 @@ int attractive(fitsne_ctx* ctx, const void* Yfull, const void* forces, double al
   else
     FITSNE_TRY(launch_attract<double>(ctx, (const double*)Yfull, (const double*)forces, alpha,
                                       (double*)out, mode, kl, part, blocks, st));
+  ctx->kl_part = part;
+  ctx->kl_nparts = blocks;
   if (kl && fold) {
     k_fold<<<1, 1024, 0, st>>>(part, blocks, (double*)ctx->scal.ptr + 1);
     FITSNE_CHECK_LAUNCH();
@@ -522,13 +539,17 @@ __global__ void __launch_bounds__(kBlock)
 k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ pot,
           const double* __restrict__ scal, const T* __restrict__ attr, T alpha,
           T* __restrict__ grad, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel,
-          T* __restrict__ gains, int32_t* __restrict__ status) {
+          T* __restrict__ gains, int32_t* __restrict__ status, T* __restrict__ attr_clear) {
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int bad = 0;
   if (i < n) {
     T yi[S], at[S];
     load_point<T, S>(Y, i, yi);
     load_point<T, S>(attr, i, at);
+    if (attr_clear) {  // consume-and-clear the tiled SpMV's accumulator
+#pragma unroll
+      for (int d = 0; d < S; ++d) attr_clear[i * S + d] = (T)0;
+    }
     T phi[4];
     point_gather<T, S, P>(yi, g, pot, phi);
     const T Z = (T)scal[0];
@@ -575,13 +596,14 @@ static int side_stream(fitsne_ctx* ctx) {
 template <typename T, bool STEP>
 static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void* attr, double alpha,
                           void* grad, double momentum, double lr, void* Yout, void* vel,
-                          void* gains, int32_t* status, cudaStream_t st) {
+                          void* gains, int32_t* status, bool clear, cudaStream_t st) {
   const GridArgs g = grid_args(ctx->grid);
   const int blocks = nblocks(n);
 #define CMB(S, P)                                                                              \
   k_combine<T, S, P, STEP><<<blocks, kBlock, 0, st>>>(                                         \
       (const T*)Y, n, g, (const T*)ctx->pot.ptr, (const double*)ctx->scal.ptr, (const T*)attr, \
-      (T)alpha, (T*)grad, (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, status)
+      (T)alpha, (T*)grad, (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, status,            \
+      clear ? (T*)attr : (T*)nullptr)
   if (ctx->dims == 1) { if (g.p == 3) CMB(1, 3); else CMB(1, 0); }
   else { if (g.p == 3) CMB(2, 3); else CMB(2, 0); }
 #undef CMB
@@ -589,23 +611,43 @@ static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void*
   return FITSNE_OK;
 }
 
+// Attractive SpMV feeding the combine kernel: the tiled kernel when it applies
+// (its accumulator is cleared by the combine), else the CSR kernel into
+// ctx->forces.  KL partials are left in ctx->kl_part / kl_nparts.
+static int spmv_for_combine(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** attr,
+                            bool* clear) {
+  if (tiled_usable(ctx, Y, st)) {
+    double* part = nullptr;
+    int np = 0;
+    FITSNE_TRY(attract_tiled(ctx, Y, kl, st, attr, &part, &np));
+    ctx->kl_part = part;
+    ctx->kl_nparts = np;
+    *clear = true;
+    return FITSNE_OK;
+  }
+  FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)ctx->n_total * ctx->dims));
+  *attr = ctx->forces.ptr;
+  *clear = false;
+  return attractive(ctx, Y, nullptr, 1.0, *attr, 0, kl, st, false);
+}
+
 int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st) {
   const int64_t n = ctx->n_total;
-  FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)n * ctx->dims));
-  void* attr = ctx->forces.ptr;
+  void* attr = nullptr;
+  bool clear = false;
   if (ctx->overlap == 0) {
     FITSNE_TRY(make_grid(ctx, Y, n, st));
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
-    FITSNE_TRY(attractive(ctx, Y, nullptr, 1.0, attr, 0, false, st));
+    FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
   } else {
-    // bbox + grid readback first (tiny), then the persistent SpMV on st and
-    // spread + FFT on the side stream, which fill the SM slots the SpMV leaves
+    // bbox + grid readback first (tiny), then the SpMV on st and spread + FFT
+    // on the side stream, which fill the SM slots the SpMV leaves
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
     FITSNE_TRY(make_grid(ctx, Y, n, ctx->side));
-    FITSNE_TRY(attractive(ctx, Y, nullptr, 1.0, attr, 0, false, st));
+    FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
@@ -613,30 +655,29 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
   }
   if (ctx->dtype == FITSNE_F32)
     return launch_combine<float, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
-                                        nullptr, nullptr, st);
+                                        nullptr, nullptr, clear, st);
   return launch_combine<double, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
-                                       nullptr, nullptr, st);
+                                       nullptr, nullptr, clear, st);
 }
 
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
                   double momentum, double lr, double* kl_dev, int32_t* status_dev, cudaStream_t st) {
   const int64_t n = ctx->n_total;
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
-  FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)n * ctx->dims));
-  void* attr = ctx->forces.ptr;
-  const int blocks = attract_grid(ctx);
+  void* attr = nullptr;
+  bool clear = false;
   if (ctx->overlap == 0) {
     FITSNE_TRY(make_grid(ctx, Yin, n, st));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
-    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st, false));
+    FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
   } else {
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
     FITSNE_TRY(make_grid(ctx, Yin, n, ctx->side));
-    // SpMV + KL partials (-> ctx->part) on st, spread + FFT on the side stream
-    FITSNE_TRY(attractive(ctx, Yin, nullptr, 1.0, attr, 0, kl_dev != nullptr, st, false));
+    // SpMV + KL partials on st, spread + FFT on the side stream
+    FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
@@ -644,13 +685,13 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
   }
   if (ctx->dtype == FITSNE_F32)
     FITSNE_TRY((launch_combine<float, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
-                                             vel, gains, status_dev, st)));
+                                             vel, gains, status_dev, clear, st)));
   else
     FITSNE_TRY((launch_combine<double, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
-                                              vel, gains, status_dev, st)));
+                                              vel, gains, status_dev, clear, st)));
   if (kl_dev) {
-    k_kl_final<<<1, 1024, 0, st>>>((const double*)ctx->part.ptr, blocks,
-                                  (const double*)ctx->scal.ptr, ctx->plogp, ctx->psum, kl_dev);
+    k_kl_final<<<1, 1024, 0, st>>>(ctx->kl_part, ctx->kl_nparts, (const double*)ctx->scal.ptr,
+                                  ctx->plogp, ctx->psum, kl_dev);
     FITSNE_CHECK_LAUNCH();
   }
   return FITSNE_OK;

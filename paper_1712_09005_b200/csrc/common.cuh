@@ -99,6 +99,8 @@ struct DevBuf {
   size_t cap = 0;
 };
 
+struct TiledP;  // tiled copy of P (tiled.cu)
+
 }  // namespace fitsne
 
 struct fitsne_ctx {
@@ -133,6 +135,11 @@ struct fitsne_ctx {
   int spread_replicas = 4;    // replicas of the internal spread accumulator (power of two)
   int overlap = 1;                 // 0 serial, 1 SpMV || repulsion, 2 same + priority repulsion
   int spmv_blocks_per_sm = 0;      // >0: persistent SpMV grid in the overlap modes
+  int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable
+  int tile_rows = 4096, tile_cols = 6144, tiled_ctas = 0;
+  fitsne::TiledP* tiled = nullptr; // built lazily from the registered CSR
+  double* kl_part = nullptr;       // where the last SpMV left its KL partials
+  int kl_nparts = 0;
   cudaStream_t side = nullptr;     // repulsion stream (overlaps the attractive SpMV)
   cudaEvent_t ev_in = nullptr, ev_done = nullptr;
   double raw_bbox[4] = {0, 0, 0, 0};  // unpadded min/max of the last grid's points

@@ -56,6 +56,18 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
                   double alpha, double momentum, double lr, double* kl_dev, int32_t* status_dev,
                   cudaStream_t st);
 
+// tiled attractive SpMV (tiled.cu) -------------------------------------------------
+// true when the tiled kernel applies to this call (builds the tiled copy of P
+// on first use)
+bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st);
+// F_attr -> *fattr (zeroed buffer owned by the tiled copy; the consumer clears
+// it), KL partials -> (*part)[0, *nparts)
+int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** fattr,
+                  double** part, int* nparts);
+// out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
+int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st);
+void free_tiled(fitsne_ctx* ctx);
+
 int read_scalars(fitsne_ctx* ctx, int count, cudaStream_t st);  // scal[0..count) -> h_scal
 int sub_inplace(fitsne_ctx* ctx, void* out, const void* q, int64_t count, cudaStream_t st);
 

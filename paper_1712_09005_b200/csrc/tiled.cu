@@ -1,0 +1,825 @@
+// Tiled attractive SpMV (compute_attractive, optimizer.py:150-166) for fp32
+// 2-D embeddings.
+//
+// The row-per-warp CSR kernel (attract.cu) is bound by its neighbour gathers:
+// every stored entry reads y_j from a different 32-byte L2 sector (a kNN
+// graph has no index locality to exploit), so it moves ~4x more bytes through
+// L2->L1 than the CSR stream itself.  Here P is re-laid out once, on first
+// use, as tiles of (row block of R rows) x (column chunk of C points):
+//
+//   * a persistent CTA walks its share of the tiles in row-block-major order;
+//     the Y rows of the current block and their force accumulators live in
+//     shared memory, and the tile's column chunk of Y (C points, 64 KB) is
+//     bulk-copied into shared memory (cp.async.bulk + mbarrier, double
+//     buffered: the next tile's chunk lands while this one is processed);
+//   * inside a tile the rows present are sorted by their entry count and
+//     packed 32 per slab (sliced ELL): lane l of a warp owns row rows[l] of
+//     the slab and walks its entries at slots (off + k) * 32 + l, so the
+//     16-bit chunk-local column and the fp32 value streams are read fully
+//     coalesced (6 bytes per slot instead of the CSR's 8), y_j comes from
+//     shared memory, and each row is flushed once per tile with no atomics;
+//   * row-block partial forces are added to the output with vector
+//     reductions (a row block may be split between two CTAs).
+//
+// Only the summation order differs from the CSR kernel.
+#include <cub/cub.cuh>
+
+#include <algorithm>
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace fitsne {
+
+// What the producer warp needs per tile: which Y chunk to stage and where the
+// tile's header blob is.  The blob (16-byte aligned, copied into shared memory
+// with the chunk) holds
+//   int32 meta[4] = {row block, slab count, first group, group count}
+//   uint32 goff[nslab + 1]   group offsets of the slabs (padded to 4 entries)
+//   uint16 rows[nslab][32]   tile-local row of each lane (0xFFFF: empty lane)
+// where a "group" is 32 consecutive slots, one per lane.
+struct TileLoad {
+  int32_t chunk;
+  int32_t hdr_bytes;
+  int64_t hdr_off;
+};
+
+__host__ __device__ inline int hdr_goff_words(int nslab) { return (nslab + 1 + 3) & ~3; }
+__host__ __device__ inline int hdr_bytes_for(int nslab) {
+  return 16 + 4 * hdr_goff_words(nslab) + 64 * nslab;
+}
+
+static constexpr int kTiledThreads = 1024;        // 31 consumer warps + 1 producer warp
+static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
+static constexpr int kTiledU = 4;                 // groups per lane per pipeline step
+static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
+static constexpr int kTiledStages = 2;            // chunk + header ring depth
+
+struct TiledP {
+  DevBuf tiles, sched, slab_off, rows, hdr, cols, vals, fattr, part;
+  int64_t ntiles = 0, nslabs = 0, nslots = 0;
+  int hdr_max = 0;  // largest header blob (bytes)
+  int R = 0, C = 0, grid = 0;
+  // the CSR this copy was built from
+  const int64_t* rowptr = nullptr;
+  const int32_t* col = nullptr;
+  const void* val = nullptr;
+  int64_t n_rows = 0, row_begin = 0, n_total = 0, nnz = 0;
+  bool failed = false;  // build impossible for this CSR (size limits / memory)
+};
+
+static void release_buf(DevBuf& b) {
+  if (b.ptr) cudaFree(b.ptr);
+  b.ptr = nullptr;
+  b.cap = 0;
+}
+
+// exact-size allocation (the tiled arrays are large; no growth headroom)
+static int alloc_exact(DevBuf& b, size_t bytes) {
+  release_buf(b);
+  if (bytes == 0) bytes = 16;
+  if (cudaMalloc(&b.ptr, bytes) != cudaSuccess) {
+    cudaGetLastError();
+    b.ptr = nullptr;
+    set_error("device allocation failed while tiling P");
+    return FITSNE_ENOMEM;
+  }
+  b.cap = bytes;
+  return FITSNE_OK;
+}
+
+void free_tiled(fitsne_ctx* ctx) {
+  if (!ctx->tiled) return;
+  TiledP* t = ctx->tiled;
+  DevBuf* bufs[] = {&t->tiles, &t->sched, &t->slab_off, &t->rows, &t->hdr, &t->cols, &t->vals,
+                    &t->fattr, &t->part};
+  for (DevBuf* b : bufs) release_buf(*b);
+  delete t;
+  ctx->tiled = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// build: CSR -> segments (row, chunk) -> sort by (tile, count desc) -> slabs
+// ---------------------------------------------------------------------------
+// segments of one row = maximal runs of entries in the same column chunk
+// (columns are sorted inside a row, so a chunk's entries are contiguous)
+__global__ void k_seg_count(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                            int64_t n_rows, int C, int32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_rows) return;
+  const int64_t b = rowptr[r], e = rowptr[r + 1];
+  int total = 0;
+  for (int64_t k0 = b; k0 < e; k0 += 32) {
+    const int64_t k = k0 + lane;
+    bool f = false;
+    if (k < e) f = (k == b) || (col[k] / C != col[k - 1] / C);
+    total += __popc(__ballot_sync(0xffffffffu, f));
+  }
+  if (lane == 0) cnt[r] = total;
+}
+
+__global__ void k_seg_emit(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                           int64_t n_rows, int C, int nch, int R, const int64_t* __restrict__ segstart,
+                           int64_t* __restrict__ seg_begin, int32_t* __restrict__ seg_row,
+                           uint64_t* __restrict__ key) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_rows) return;
+  const int64_t b = rowptr[r], e = rowptr[r + 1];
+  int64_t base = segstart[r];
+  const int64_t tile_row = (r / R) * (int64_t)nch;
+  for (int64_t k0 = b; k0 < e; k0 += 32) {
+    const int64_t k = k0 + lane;
+    bool f = false;
+    int ch = 0;
+    if (k < e) {
+      ch = col[k] / C;
+      f = (k == b) || (ch != col[k - 1] / C);
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, f);
+    if (f) {
+      const int64_t s = base + __popc(m & ((1u << lane) - 1u));
+      seg_begin[s] = k;
+      seg_row[s] = (int32_t)r;
+      key[s] = (uint64_t)(tile_row + ch) << 16;  // count filled in by k_seg_finish
+    }
+    base += __popc(m);
+  }
+}
+
+__global__ void k_seg_finish(const int64_t* __restrict__ rowptr, const int64_t* __restrict__ segstart,
+                             const int64_t* __restrict__ seg_begin, const int32_t* __restrict__ seg_row,
+                             int64_t nseg, uint64_t* __restrict__ key, uint32_t* __restrict__ idx,
+                             int32_t* __restrict__ seg_cnt) {
+  const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (s >= nseg) return;
+  const int32_t r = seg_row[s];
+  const int64_t end = (s + 1 < segstart[r + 1]) ? seg_begin[s + 1] : rowptr[r + 1];
+  const int32_t c = (int32_t)(end - seg_begin[s]);
+  seg_cnt[s] = c;
+  // larger counts first inside a tile (sliced-ELL sorting window = the tile)
+  key[s] |= (uint64_t)(0xFFFF - c);
+  idx[s] = (uint32_t)s;
+}
+
+__global__ void k_tile_bounds(const uint64_t* __restrict__ key, int64_t nseg,
+                              int32_t* __restrict__ tfirst, int32_t* __restrict__ tcount) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const uint64_t t = key[q] >> 16;
+  if (q == 0 || (key[q - 1] >> 16) != t) {
+    int64_t e = q + 1;
+    // count: find the end of this tile's run (runs are short relative to nseg;
+    // binary search over the sorted keys)
+    int64_t lo = q, hi = nseg;  // first index with tile > t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if ((key[mid] >> 16) > t) hi = mid; else lo = mid + 1;
+    }
+    e = lo;
+    tfirst[t] = (int32_t)q;
+    tcount[t] = (int32_t)(e - q);
+  }
+}
+
+__global__ void k_tile_nslab(const int32_t* __restrict__ tcount, int64_t nt, int32_t* __restrict__ nslab) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t < nt) nslab[t] = (tcount[t] + 31) / 32;
+}
+
+__global__ void k_slab_kmax(const int32_t* __restrict__ tfirst, const int32_t* __restrict__ nslab,
+                            const int32_t* __restrict__ slab_begin, const uint32_t* __restrict__ sidx,
+                            const int32_t* __restrict__ seg_cnt, int64_t nt, uint32_t* __restrict__ kmax) {
+  const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (t >= nt) return;
+  const int ns = nslab[t];
+  for (int j = 0; j < ns; ++j) kmax[slab_begin[t] + j] = (uint32_t)seg_cnt[sidx[tfirst[t] + 32 * j]];
+}
+
+__global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __restrict__ sidx,
+                            int64_t nseg, const int32_t* __restrict__ tfirst,
+                            const int32_t* __restrict__ slab_begin, const uint32_t* __restrict__ slab_off,
+                            const int64_t* __restrict__ seg_begin, const int32_t* __restrict__ seg_row,
+                            const int32_t* __restrict__ seg_cnt, const int32_t* __restrict__ col,
+                            const float* __restrict__ val, int nch, int R, int C,
+                            uint16_t* __restrict__ rows, uint16_t* __restrict__ cols,
+                            float* __restrict__ vals) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const int64_t t = (int64_t)(key[q] >> 16);
+  const int64_t rel = q - tfirst[t];
+  const int64_t slab = slab_begin[t] + rel / 32;
+  const int lane = (int)(rel & 31);
+  const uint32_t s = sidx[q];
+  const int32_t r = seg_row[s];
+  const int rb = (int)(t / nch), ch = (int)(t % nch);
+  rows[slab * 32 + lane] = (uint16_t)(r - (int64_t)rb * R);
+  const int64_t b = seg_begin[s];
+  const int c = seg_cnt[s];
+  const int64_t o = (int64_t)slab_off[slab];
+  for (int k = 0; k < c; ++k) {
+    const int64_t slot = (o + k) * 32 + lane;
+    cols[slot] = (uint16_t)(col[b + k] - ch * C);
+    vals[slot] = val[b + k];
+  }
+}
+
+// one warp per tile: assemble its header blob
+__global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_t* __restrict__ t_sb,
+                               const int32_t* __restrict__ t_ns, const int64_t* __restrict__ t_hoff,
+                               int64_t ntiles, int nch, const uint32_t* __restrict__ slab_off,
+                               const uint16_t* __restrict__ rows, unsigned char* __restrict__ hdr) {
+  const int lane = threadIdx.x & 31;
+  const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (t >= ntiles) return;
+  const int sb = t_sb[t], ns = t_ns[t];
+  unsigned char* h = hdr + t_hoff[t];
+  int32_t* meta = reinterpret_cast<int32_t*>(h);
+  uint32_t* goff = reinterpret_cast<uint32_t*>(h + 16);
+  uint16_t* hr = reinterpret_cast<uint16_t*>(h + 16 + 4 * hdr_goff_words(ns));
+  const uint32_t g0 = slab_off[sb];
+  if (lane == 0) {
+    meta[0] = t_dense[t] / nch;
+    meta[1] = ns;
+    meta[2] = (int32_t)g0;
+    meta[3] = (int32_t)(slab_off[sb + ns] - g0);
+  }
+  for (int j = lane; j < hdr_goff_words(ns); j += 32) goff[j] = j <= ns ? slab_off[sb + j] - g0 : 0u;
+  for (int64_t k = lane; k < (int64_t)ns * 32; k += 32) hr[k] = rows[(int64_t)sb * 32 + k];
+}
+
+struct TmpBufs {
+  std::vector<void*> ptrs;
+  ~TmpBufs() { for (void* p : ptrs) cudaFree(p); }
+  template <typename T>
+  int alloc(T** out, size_t count) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) {
+      cudaGetLastError();
+      set_error("device allocation failed while tiling P");
+      return FITSNE_ENOMEM;
+    }
+    ptrs.push_back(p);
+    *out = (T*)p;
+    return FITSNE_OK;
+  }
+};
+
+static inline int nb(int64_t n, int block) { return (int)std::max<int64_t>(1, (n + block - 1) / block); }
+
+// Exclusive scan of n items in -> out (CUB), temp storage from `tmp`.
+template <typename In, typename Out>
+static int excl_scan(TmpBufs& tmp, In* in, Out* out, int64_t n, cudaStream_t st) {
+  size_t bytes = 0;
+  FITSNE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, bytes, in, out, n, st));
+  void* t = nullptr;
+  unsigned char* tb = nullptr;
+  FITSNE_TRY(tmp.alloc(&tb, bytes));
+  t = tb;
+  FITSNE_CUDA(cub::DeviceScan::ExclusiveSum(t, bytes, in, out, n, st));
+  return FITSNE_OK;
+}
+
+static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
+  const int64_t n_rows = ctx->n_rows, n_total = ctx->n_total, nnz = ctx->nnz;
+  const int R = ctx->tile_rows, C = ctx->tile_cols;
+  const int64_t nrb = (n_rows + R - 1) / R, nch = (n_total + C - 1) / C;
+  const int64_t ntd = nrb * nch;  // dense tile count
+  if (ntd >= (1LL << 31) || nnz >= (1LL << 31) || nrb >= (1LL << 31)) {
+    set_error("P too large for the tiled layout");
+    return FITSNE_ETOOBIG;
+  }
+  TmpBufs tmp;
+  int32_t* segcnt;
+  int64_t* segstart;
+  FITSNE_TRY(tmp.alloc(&segcnt, n_rows + 1));
+  FITSNE_TRY(tmp.alloc(&segstart, n_rows + 1));
+  FITSNE_CUDA(cudaMemsetAsync(segcnt, 0, sizeof(int32_t) * (n_rows + 1), st));
+  k_seg_count<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, ctx->col, n_rows, C, segcnt);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_TRY(excl_scan(tmp, segcnt, segstart, n_rows + 1, st));
+  int64_t nseg = 0;
+  FITSNE_CUDA(cudaMemcpyAsync(&nseg, segstart + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  if (nseg <= 0) { set_error("empty P"); return FITSNE_EINVAL; }
+
+  int64_t* seg_begin;
+  int32_t *seg_row, *seg_cnt;
+  uint64_t *key, *key2;
+  uint32_t *idx, *idx2;
+  FITSNE_TRY(tmp.alloc(&seg_begin, nseg));
+  FITSNE_TRY(tmp.alloc(&seg_row, nseg));
+  FITSNE_TRY(tmp.alloc(&seg_cnt, nseg));
+  FITSNE_TRY(tmp.alloc(&key, nseg));
+  FITSNE_TRY(tmp.alloc(&key2, nseg));
+  FITSNE_TRY(tmp.alloc(&idx, nseg));
+  FITSNE_TRY(tmp.alloc(&idx2, nseg));
+  k_seg_emit<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, ctx->col, n_rows, C, (int)nch, R,
+                                                   segstart, seg_begin, seg_row, key);
+  FITSNE_CHECK_LAUNCH();
+  k_seg_finish<<<nb(nseg, 256), 256, 0, st>>>(ctx->rowptr, segstart, seg_begin, seg_row, nseg, key,
+                                              idx, seg_cnt);
+  FITSNE_CHECK_LAUNCH();
+  int end_bit = 16;
+  while ((1LL << (end_bit - 16)) < ntd) ++end_bit;
+  {
+    size_t bytes = 0;
+    FITSNE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key2, idx, idx2, nseg, 0, end_bit, st));
+    unsigned char* tb;
+    FITSNE_TRY(tmp.alloc(&tb, bytes));
+    FITSNE_CUDA(cub::DeviceRadixSort::SortPairs(tb, bytes, key, key2, idx, idx2, nseg, 0, end_bit, st));
+  }
+  int32_t *tfirst, *tcount, *nslab, *slab_begin;
+  FITSNE_TRY(tmp.alloc(&tfirst, ntd));
+  FITSNE_TRY(tmp.alloc(&tcount, ntd));
+  FITSNE_TRY(tmp.alloc(&nslab, ntd + 1));
+  FITSNE_TRY(tmp.alloc(&slab_begin, ntd + 1));
+  FITSNE_CUDA(cudaMemsetAsync(tfirst, 0, sizeof(int32_t) * ntd, st));
+  FITSNE_CUDA(cudaMemsetAsync(tcount, 0, sizeof(int32_t) * ntd, st));
+  FITSNE_CUDA(cudaMemsetAsync(nslab, 0, sizeof(int32_t) * (ntd + 1), st));
+  k_tile_bounds<<<nb(nseg, 256), 256, 0, st>>>(key2, nseg, tfirst, tcount);
+  FITSNE_CHECK_LAUNCH();
+  k_tile_nslab<<<nb(ntd, 256), 256, 0, st>>>(tcount, ntd, nslab);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_TRY(excl_scan(tmp, nslab, slab_begin, ntd + 1, st));
+  int32_t nslabs = 0;
+  FITSNE_CUDA(cudaMemcpyAsync(&nslabs, slab_begin + ntd, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+
+  uint32_t* kmax;
+  FITSNE_TRY(tmp.alloc(&kmax, (size_t)nslabs + 1));
+  FITSNE_CUDA(cudaMemsetAsync(kmax, 0, sizeof(uint32_t) * ((size_t)nslabs + 1), st));
+  k_slab_kmax<<<nb(ntd, 256), 256, 0, st>>>(tfirst, nslab, slab_begin, idx2, seg_cnt, ntd, kmax);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_TRY(alloc_exact(T->slab_off, sizeof(uint32_t) * ((size_t)nslabs + 1)));
+  uint32_t* slab_off = (uint32_t*)T->slab_off.ptr;
+  FITSNE_TRY(excl_scan(tmp, kmax, slab_off, (int64_t)nslabs + 1, st));
+  uint32_t total_k = 0;
+  FITSNE_CUDA(cudaMemcpyAsync(&total_k, slab_off + nslabs, sizeof(uint32_t), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  const int64_t nslots = (int64_t)total_k * 32;
+
+  FITSNE_TRY(alloc_exact(T->rows, sizeof(uint16_t) * (size_t)nslabs * 32));
+  // kTiledPad extra slots: the kernel reads whole groups of slots past a
+  // slab's end (values masked), so the last slab must not run off the array
+  FITSNE_TRY(alloc_exact(T->cols, sizeof(uint16_t) * (size_t)(nslots + kTiledPad)));
+  FITSNE_TRY(alloc_exact(T->vals, sizeof(float) * (size_t)(nslots + kTiledPad)));
+  FITSNE_CUDA(cudaMemsetAsync(T->rows.ptr, 0xFF, sizeof(uint16_t) * (size_t)nslabs * 32, st));
+  FITSNE_CUDA(cudaMemsetAsync(T->cols.ptr, 0, sizeof(uint16_t) * (size_t)(nslots + kTiledPad), st));
+  FITSNE_CUDA(cudaMemsetAsync(T->vals.ptr, 0, sizeof(float) * (size_t)(nslots + kTiledPad), st));
+  k_tile_fill<<<nb(nseg, 256), 256, 0, st>>>(key2, idx2, nseg, tfirst, slab_begin, slab_off, seg_begin,
+                                             seg_row, seg_cnt, ctx->col, (const float*)ctx->val,
+                                             (int)nch, R, C, (uint16_t*)T->rows.ptr,
+                                             (uint16_t*)T->cols.ptr, (float*)T->vals.ptr);
+  FITSNE_CHECK_LAUNCH();
+
+  // host: compact tile list, header blobs, static schedule balanced on cost
+  std::vector<int32_t> h_nslab(ntd), h_sb(ntd);
+  std::vector<uint32_t> h_off((size_t)nslabs + 1);
+  FITSNE_CUDA(cudaMemcpyAsync(h_nslab.data(), nslab, sizeof(int32_t) * ntd, cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaMemcpyAsync(h_sb.data(), slab_begin, sizeof(int32_t) * ntd, cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaMemcpyAsync(h_off.data(), slab_off, sizeof(uint32_t) * ((size_t)nslabs + 1),
+                              cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  if ((uint64_t)h_off[nslabs] + 2 * kTiledU >= (1ULL << 31)) {
+    set_error("P too large for the tiled layout");
+    return FITSNE_ETOOBIG;
+  }
+  std::vector<TileLoad> tiles;
+  std::vector<int32_t> t_dense, t_sb, t_ns;
+  std::vector<int64_t> t_hoff;
+  std::vector<double> cost;
+  int64_t hoff = 0;
+  int hmax = 16;
+  for (int64_t t = 0; t < ntd; ++t) {
+    if (h_nslab[t] == 0) continue;
+    const int ns = h_nslab[t];
+    TileLoad d;
+    d.chunk = (int32_t)(t % nch);
+    d.hdr_bytes = hdr_bytes_for(ns);
+    d.hdr_off = hoff;
+    hoff += d.hdr_bytes;
+    hmax = std::max(hmax, d.hdr_bytes);
+    const double groups = (double)(h_off[h_sb[t] + ns] - h_off[h_sb[t]]);
+    // streamed groups + per-slab flush + chunk / header staging
+    cost.push_back(32.0 * groups + 48.0 * ns + 0.5 * C);
+    tiles.push_back(d);
+    t_dense.push_back((int32_t)t);
+    t_sb.push_back(h_sb[t]);
+    t_ns.push_back(ns);
+    t_hoff.push_back(d.hdr_off);
+  }
+  const int64_t nt = (int64_t)tiles.size();
+  FITSNE_TRY(alloc_exact(T->hdr, (size_t)std::max<int64_t>(hoff, 16)));
+  {
+    int32_t *d_dense, *d_sb, *d_ns;
+    int64_t* d_hoff;
+    FITSNE_TRY(tmp.alloc(&d_dense, nt));
+    FITSNE_TRY(tmp.alloc(&d_sb, nt));
+    FITSNE_TRY(tmp.alloc(&d_ns, nt));
+    FITSNE_TRY(tmp.alloc(&d_hoff, nt));
+    FITSNE_CUDA(cudaMemcpyAsync(d_dense, t_dense.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, st));
+    FITSNE_CUDA(cudaMemcpyAsync(d_sb, t_sb.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, st));
+    FITSNE_CUDA(cudaMemcpyAsync(d_ns, t_ns.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, st));
+    FITSNE_CUDA(cudaMemcpyAsync(d_hoff, t_hoff.data(), sizeof(int64_t) * nt, cudaMemcpyHostToDevice, st));
+    k_tile_headers<<<nb(nt * 32, 256), 256, 0, st>>>(d_dense, d_sb, d_ns, d_hoff, nt, (int)nch, slab_off,
+                                                    (const uint16_t*)T->rows.ptr,
+                                                    (unsigned char*)T->hdr.ptr);
+    FITSNE_CHECK_LAUNCH();
+    FITSNE_CUDA(cudaStreamSynchronize(st));
+  }
+  const int grid = ctx->tiled_ctas > 0 ? ctx->tiled_ctas : ctx->num_sms;
+  std::vector<int32_t> sched(grid + 1, (int32_t)nt);
+  double total = 0;
+  for (double c : cost) total += c;
+  {
+    double acc = 0;
+    int k = 1;
+    sched[0] = 0;
+    for (int64_t t = 0; t < nt && k < grid; ++t) {
+      acc += cost[t];
+      while (k < grid && acc >= total * k / grid) sched[k++] = (int32_t)(t + 1);
+    }
+    for (; k < grid; ++k) sched[k] = (int32_t)nt;
+    sched[grid] = (int32_t)nt;
+  }
+  FITSNE_TRY(alloc_exact(T->tiles, sizeof(TileLoad) * (size_t)std::max<int64_t>(nt, 1)));
+  FITSNE_TRY(alloc_exact(T->sched, sizeof(int32_t) * (grid + 1)));
+  FITSNE_CUDA(cudaMemcpyAsync(T->tiles.ptr, tiles.data(), sizeof(TileLoad) * nt, cudaMemcpyHostToDevice, st));
+  FITSNE_CUDA(cudaMemcpyAsync(T->sched.ptr, sched.data(), sizeof(int32_t) * (grid + 1),
+                              cudaMemcpyHostToDevice, st));
+  FITSNE_TRY(alloc_exact(T->fattr, sizeof(float) * 2 * (size_t)std::max<int64_t>(n_rows, 1)));
+  FITSNE_CUDA(cudaMemsetAsync(T->fattr.ptr, 0, sizeof(float) * 2 * (size_t)n_rows, st));
+  FITSNE_TRY(alloc_exact(T->part, sizeof(double) * (grid + 1)));
+  FITSNE_CUDA(cudaStreamSynchronize(st));  // host vectors and temporaries go out of scope
+  release_buf(T->rows);      // folded into the header blobs
+  release_buf(T->slab_off);
+  T->ntiles = nt;
+  T->nslabs = nslabs;
+  T->nslots = nslots;
+  T->hdr_max = hmax;
+  T->R = R;
+  T->C = C;
+  T->grid = grid;
+  return FITSNE_OK;
+}
+
+static size_t stage_bytes(int C, int hdr_max) { return (size_t)C * 8 + (size_t)((hdr_max + 15) & ~15); }
+static size_t tiled_smem(int R, int C, int hdr_max) {
+  return sizeof(float2) * 3 * (size_t)R + kTiledStages * stage_bytes(C, hdr_max);
+}
+
+// Use the tiled kernel for this call?  Builds the tiled copy on first use.
+bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
+  if (ctx->tiled_spmv == 0 || ctx->dtype != FITSNE_F32 || ctx->dims != 2 || !ctx->rowptr) return false;
+  if (((uintptr_t)Y & 15) != 0) return false;
+  if (ctx->tiled_spmv == 1 && ctx->nnz < (1LL << 22)) return false;
+  if (tiled_smem(ctx->tile_rows, ctx->tile_cols, hdr_bytes_for((ctx->tile_rows + 31) / 32)) >
+      227 * 1024 - 1024)
+    return false;  // tile shape does not fit in shared memory
+  TiledP* T = ctx->tiled;
+  const bool same = T && T->rowptr == ctx->rowptr && T->col == ctx->col && T->val == ctx->val &&
+                    T->n_rows == ctx->n_rows && T->row_begin == ctx->row_begin &&
+                    T->n_total == ctx->n_total && T->nnz == ctx->nnz && T->R == ctx->tile_rows &&
+                    T->C == ctx->tile_cols &&
+                    T->grid == (ctx->tiled_ctas > 0 ? ctx->tiled_ctas : ctx->num_sms);
+  if (same) return !T->failed;
+  if (T && T->failed && T->rowptr == ctx->rowptr && T->col == ctx->col && T->val == ctx->val &&
+      T->nnz == ctx->nnz)
+    return false;
+  free_tiled(ctx);
+  T = new TiledP();
+  ctx->tiled = T;
+  T->rowptr = ctx->rowptr;
+  T->col = ctx->col;
+  T->val = ctx->val;
+  T->n_rows = ctx->n_rows;
+  T->row_begin = ctx->row_begin;
+  T->n_total = ctx->n_total;
+  T->nnz = ctx->nnz;
+  T->R = ctx->tile_rows;
+  T->C = ctx->tile_cols;
+  T->grid = ctx->tiled_ctas > 0 ? ctx->tiled_ctas : ctx->num_sms;
+  if (ctx->n_rows < 1 || ctx->nnz < 1 || build_tiled(ctx, T, st) != FITSNE_OK) {
+    // keep the CSR kernel for this P; release what the attempt allocated
+    cudaStreamSynchronize(st);
+    cudaGetLastError();
+    DevBuf* bufs[] = {&T->tiles, &T->sched, &T->slab_off, &T->rows, &T->hdr, &T->cols, &T->vals,
+                      &T->fattr, &T->part};
+    for (DevBuf* b : bufs) release_buf(*b);
+    T->failed = true;
+    return false;
+  }
+  return true;
+}
+
+// ---------------------------------------------------------------------------
+// kernel
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t smem_addr(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(b)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_addr(b)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_addr(b)) : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra LAB_WAIT;\n"
+      "}\n" ::"r"(smem_addr(b)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* b) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b))
+      : "memory");
+}
+
+// consumer-only barrier (the producer warp never joins it)
+__device__ __forceinline__ void consumer_sync() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kTiledConsumers * 32) : "memory");
+}
+
+// 1 / x for x >= 1 (no denormal handling needed): one MUFU.RCP
+__device__ __forceinline__ float rcp_approx(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+
+// Warp-specialised persistent kernel.  Warp 31 (one lane) streams, per tile,
+// the Y column chunk and the tile's header blob into a 2-stage shared-memory
+// ring with bulk copies (full barriers: transaction bytes; empty barriers: one
+// arrival per consumer warp).  Consumer warps 0..30 split each tile's slot
+// groups evenly, walk them with a 2-deep register pipeline of (column, value)
+// loads, gather y_j from the staged chunk and flush a row's partial force into
+// the row block's shared accumulator at every slab boundary.  Row-block
+// changes (rare: a CTA's tiles are a contiguous run of the row-block-major
+// order) flush the accumulator to global memory with vector reductions.
+template <bool KL>
+__global__ void __launch_bounds__(kTiledThreads, 1)
+k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ sched,
+                const unsigned char* __restrict__ hdr, const uint16_t* __restrict__ cols,
+                const float* __restrict__ vals, const float2* __restrict__ Y, int64_t row_begin,
+                int64_t n_rows, int64_t n_total, int R, int C, int stage_sz,
+                float2* __restrict__ fattr, double* __restrict__ klpart) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  float2* ys = reinterpret_cast<float2*>(smem_raw);
+  float2* acc = ys + R;  // two accumulators: [0, R) even tiles, [R, 2R) odd tiles
+  unsigned char* ring = reinterpret_cast<unsigned char*>(acc + 2 * R);
+  __shared__ __align__(8) uint64_t full[kTiledStages], empty[kTiledStages];
+  __shared__ double red[kTiledConsumers];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int t0 = sched[blockIdx.x], t1 = sched[blockIdx.x + 1];
+  if (tid == 0) {
+    for (int b = 0; b < kTiledStages; ++b) {
+      mbar_init(&full[b], 1);
+      mbar_init(&empty[b], kTiledConsumers);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == kTiledConsumers) {
+    // ---------------- producer ----------------
+    if (lane == 0) {
+      for (int t = t0; t < t1; ++t) {
+        const int it = t - t0, b = it % kTiledStages;
+        if (it >= kTiledStages) mbar_wait(&empty[b], (uint32_t)(((it / kTiledStages) - 1) & 1));
+        const TileLoad d = tiles[t];
+        unsigned char* st = ring + (size_t)b * stage_sz;
+        float2* cdst = reinterpret_cast<float2*>(st);
+        unsigned char* hdst = st + (size_t)C * 8;
+        const int64_t c0 = (int64_t)d.chunk * C;
+        const int64_t cnt = (n_total - c0 < C) ? (n_total - c0) : C;
+        const uint32_t cbytes = (uint32_t)(cnt & ~1LL) * 8u;
+        // odd tail point (bulk copies move multiples of 16 bytes): a plain
+        // store, published to the consumers by the release of the arrive below
+        if (cnt & 1) cdst[cnt - 1] = Y[c0 + cnt - 1];
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive_tx(&full[b], cbytes + (uint32_t)d.hdr_bytes);
+        if (cbytes) bulk_g2s(cdst, Y + c0, cbytes, &full[b]);
+        bulk_g2s(hdst, hdr + d.hdr_off, (uint32_t)d.hdr_bytes, &full[b]);
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumers ----------------
+  // Work split: consumer warps take equal runs of the tile's slot groups; a
+  // slab cut by a run boundary is shared by two warps and flushed atomically,
+  // every other slab belongs to one warp.  Across tiles, consumers are at most
+  // one tile apart (the producer refills a stage only after every consumer
+  // released it), so even and odd tiles accumulate into separate arrays and
+  // those flushes are plain shared-memory read-modify-writes.
+  float kl = 0.f;
+  double kld = 0.0;
+  int cur_rb = -1;
+  int64_t r0 = 0;
+  int nr = 0;
+  auto flush_block = [&]() {
+    for (int i = tid; i < nr; i += kTiledConsumers * 32) {
+      const float2 a = acc[i], c = acc[R + i];
+      const float2 v = make_float2(a.x + c.x, a.y + c.y);
+      if (v.x != 0.f || v.y != 0.f) atomicAdd(fattr + r0 + i, v);
+    }
+  };
+  for (int t = t0; t < t1; ++t) {
+    const int it = t - t0, b = it % kTiledStages;
+    const unsigned char* st = ring + (size_t)b * stage_sz;
+    const float2* cb = reinterpret_cast<const float2*>(st);
+    const unsigned char* h = st + (size_t)C * 8;
+    mbar_wait(&full[b], (uint32_t)((it / kTiledStages) & 1));
+    const int32_t* meta = reinterpret_cast<const int32_t*>(h);
+    const int rb = meta[0], ns = meta[1];
+    const int64_t g0 = (uint32_t)meta[2];
+    const int ng = meta[3];
+    const uint32_t* goff = reinterpret_cast<const uint32_t*>(h + 16);
+    const uint16_t* hrows = reinterpret_cast<const uint16_t*>(h + 16 + 4 * hdr_goff_words(ns));
+    if (rb != cur_rb) {
+      consumer_sync();  // every consumer is done with the previous row block
+      if (cur_rb >= 0) flush_block();
+      cur_rb = rb;
+      r0 = (int64_t)rb * R;
+      nr = (n_rows - r0 < R) ? (int)(n_rows - r0) : R;
+      for (int i = tid; i < R; i += kTiledConsumers * 32) {
+        ys[i] = i < nr ? Y[row_begin + r0 + i] : make_float2(0.f, 0.f);
+        acc[i] = make_float2(0.f, 0.f);
+        acc[R + i] = make_float2(0.f, 0.f);
+      }
+      consumer_sync();
+    }
+    float2* accp = acc + (size_t)(it & 1) * R;
+    const int lo = (int)(((int64_t)ng * warp) / kTiledConsumers);
+    const int hi = (int)(((int64_t)ng * (warp + 1)) / kTiledConsumers);
+    if (lo < hi) {
+      // slab containing group lo: last s with goff[s] <= lo
+      int a = 0, z = ns;
+      while (z - a > 1) {
+        const int m = (a + z) >> 1;
+        if ((int)goff[m] <= lo) a = m; else z = m;
+      }
+      int s = a;
+      int s_end = (int)goff[s + 1];
+      bool shared_slab = (int)goff[s] < lo || s_end > hi;
+      int row = hrows[s * 32 + lane];
+      float2 yi = row != 0xFFFF ? ys[row] : make_float2(0.f, 0.f);
+      float ax = 0.f, ay = 0.f;
+      auto flush_row = [&]() {
+        if (row == 0xFFFF) return;
+        if (shared_slab) {
+          atomicAdd(&accp[row].x, ax);
+          atomicAdd(&accp[row].y, ay);
+        } else {
+          float2 v = accp[row];
+          v.x += ax;
+          v.y += ay;
+          accp[row] = v;
+        }
+      };
+      const uint16_t* cp = cols + (size_t)(g0 + lo) * 32 + lane;
+      const float* vp = vals + (size_t)(g0 + lo) * 32 + lane;
+      unsigned short cA[kTiledU], cB[kTiledU];
+      float pA[kTiledU], pB[kTiledU];
+#pragma unroll
+      for (int u = 0; u < kTiledU; ++u) {
+        cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
+        pA[u] = __ldcs(vp + u * 32);
+      }
+      for (int g = lo; g < hi; g += kTiledU) {
+        // prefetch the next step (reads past hi stay inside the padded arrays)
+#pragma unroll
+        for (int u = 0; u < kTiledU; ++u) {
+          cB[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + (kTiledU + u) * 32);
+          pB[u] = __ldcs(vp + (kTiledU + u) * 32);
+        }
+        float2 yj[kTiledU];
+#pragma unroll
+        for (int u = 0; u < kTiledU; ++u) yj[u] = cb[cA[u]];
+#pragma unroll
+        for (int u = 0; u < kTiledU; ++u) {
+          const int gg = g + u;
+          if (gg < hi) {
+            if (gg == s_end) {  // warp-uniform slab boundary
+              flush_row();
+              ax = ay = 0.f;
+              ++s;
+              s_end = (int)goff[s + 1];
+              shared_slab = s_end > hi;
+              row = hrows[s * 32 + lane];
+              yi = row != 0xFFFF ? ys[row] : make_float2(0.f, 0.f);
+            }
+            const float dx = yi.x - yj[u].x, dy = yi.y - yj[u].y;
+            const float q = 1.0f + (dx * dx + dy * dy);
+            const float w = pA[u] * rcp_approx(q);
+            ax += w * dx;
+            ay += w * dy;
+            if (KL) kl += pA[u] * __logf(q);
+          }
+        }
+#pragma unroll
+        for (int u = 0; u < kTiledU; ++u) { cA[u] = cB[u]; pA[u] = pB[u]; }
+        cp += kTiledU * 32;
+        vp += kTiledU * 32;
+      }
+      flush_row();
+      if (KL) { kld += (double)kl; kl = 0.f; }
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&empty[b]);
+  }
+  consumer_sync();
+  if (cur_rb >= 0) flush_block();
+  if (KL) {
+    kld = warp_sum(kld);
+    if (lane == 0) red[warp] = kld;
+    consumer_sync();
+    if (tid == 0) {
+      double sum = 0;
+      for (int w = 0; w < kTiledConsumers; ++w) sum += red[w];
+      klpart[blockIdx.x] = sum;
+    }
+  }
+}
+
+// out = F_attr (mode 0) or 4 (alpha F_attr - F_rep) (mode 1); clears F_attr
+__global__ void k_tiled_finish(float2* __restrict__ fattr, int64_t n, const float2* __restrict__ frep,
+                               float alpha, int mode, float2* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float2 a = fattr[i];
+  float2 r = a;
+  if (mode == 1) {
+    const float2 f = frep[i];
+    r.x = 4.f * (alpha * a.x - f.x);
+    r.y = 4.f * (alpha * a.y - f.y);
+  }
+  fattr[i] = make_float2(0.f, 0.f);
+  out[i] = r;
+}
+
+// Runs the tiled SpMV: F_attr accumulates into the tiled copy's zeroed buffer
+// (*fattr_out; the consumer must clear it), KL partials -> T->part[0, grid).
+int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** fattr_out,
+                  double** part_out, int* nparts) {
+  TiledP* T = ctx->tiled;
+  const size_t smem = tiled_smem(T->R, T->C, T->hdr_max);
+  const int stage_sz = (int)stage_bytes(T->C, T->hdr_max);
+  static thread_local int configured_dev = -1;
+  static thread_local size_t configured_smem = 0;
+  if (configured_dev != ctx->device || configured_smem < smem) {
+    FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)smem));
+    configured_dev = ctx->device;
+    configured_smem = smem;
+  }
+  double* part = (double*)T->part.ptr;
+#define TILED_ARGS                                                                                  \
+  (const TileLoad*)T->tiles.ptr, (const int32_t*)T->sched.ptr, (const unsigned char*)T->hdr.ptr,    \
+      (const uint16_t*)T->cols.ptr, (const float*)T->vals.ptr, (const float2*)Y, ctx->row_begin,    \
+      ctx->n_rows, ctx->n_total, T->R, T->C, stage_sz, (float2*)T->fattr.ptr, part
+  if (kl)
+    k_attract_tiled<true><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
+  else
+    k_attract_tiled<false><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
+#undef TILED_ARGS
+  FITSNE_CHECK_LAUNCH();
+  *fattr_out = T->fattr.ptr;
+  if (part_out) *part_out = part;
+  if (nparts) *nparts = T->grid;
+  return FITSNE_OK;
+}
+
+int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st) {
+  TiledP* T = ctx->tiled;
+  const int64_t n = ctx->n_rows;
+  k_tiled_finish<<<nb(n, 256), 256, 0, st>>>((float2*)T->fattr.ptr, n, (const float2*)frep, (float)alpha,
+                                             mode, (float2*)out);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+}  // namespace fitsne

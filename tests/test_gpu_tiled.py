@@ -1,0 +1,179 @@
+"""Tiled attractive SpMV (csrc/tiled.cu) against the oracle and the CSR kernel.
+
+The tiled layout is forced (FITSNE_OPT_TILED_SPMV = 2) with small tile
+shapes so that the small inputs here span many row blocks, column chunks and
+CTAs (row blocks split between CTAs, CTAs with no tiles, odd point counts,
+partial chunks).  fp32 tolerance: rel-L2 <= 1e-5 on F_attr (the bar for the
+gradient is 1e-3); the KL sum to 1e-6.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import rel_l2
+from oracle import fitsne_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+OPT_TILED, OPT_ROWS, OPT_COLS, OPT_CTAS = 5, 6, 7, 8
+
+
+def _graph(n, k, seed, clustered=True):
+    """Symmetric kNN-like P (upper COO) with cluster structure, plus Y."""
+    rng = np.random.default_rng(seed)
+    if clustered:
+        lab = np.sort(rng.integers(0, 7, n))
+        rows, cols = [], []
+        for i in range(n):
+            same = np.flatnonzero(lab == lab[i])
+            j = rng.choice(same, size=min(k, same.size), replace=False)
+            rows.append(np.full(j.size, i))
+            cols.append(j)
+        r, c = np.concatenate(rows), np.concatenate(cols)
+    else:
+        r = np.repeat(np.arange(n), k)
+        c = rng.integers(0, n, n * k)
+    keep = r != c
+    lo, hi = np.minimum(r[keep], c[keep]), np.maximum(r[keep], c[keep])
+    key = np.unique(lo.astype(np.int64) * n + hi)
+    rr, cc = key // n, key % n
+    v = rng.random(rr.size) + 0.05
+    v /= 2 * v.sum()
+    Y = rng.standard_normal((n, 2)) * 10
+    return rr, cc, v, Y
+
+
+def _csr(n, rr, cc, v, row_begin=0, row_end=None):
+    from paper_1712_09005_b200.affinities import csr_from_full
+    dev = torch.device("cuda", 0)
+    r = torch.from_numpy(np.concatenate([rr, cc])).to(dev)
+    c = torch.from_numpy(np.concatenate([cc, rr])).to(dev)
+    w = torch.from_numpy(np.concatenate([v, v])).to(dev)
+    return csr_from_full(n, r, c, w, torch.float32, row_begin, n if row_end is None else row_end)
+
+
+def _ctx(tiled, rows=64, cols=128, ctas=0):
+    from paper_1712_09005_b200 import _lib
+    ctx = _lib.Context(0, 2, torch.float32, 3, 20, 1.0)
+    for opt, val in ((OPT_TILED, tiled), (OPT_ROWS, rows), (OPT_COLS, cols), (OPT_CTAS, ctas)):
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, opt, val), "set_option")
+    return ctx
+
+
+def _attr(ctx, csr, y):
+    from paper_1712_09005_b200 import _lib
+    ctx.set_affinities(csr)
+    out = torch.empty((csr.n_rows, 2), dtype=torch.float32, device=y.device)
+    _lib.check(ctx.lib.fitsne_attractive(ctx.h, _lib.ptr(y), _lib.ptr(out), ctx.stream), "attractive")
+    torch.cuda.synchronize()
+    return out.cpu().numpy().astype(np.float64)
+
+
+SHAPES = [(64, 128, 0), (64, 128, 3), (2, 2, 0), (256, 1024, 7), (4096, 6144, 0), (128, 64, 5000)]
+
+
+@pytest.mark.parametrize("shape", SHAPES)
+@pytest.mark.parametrize("n,k,clustered", [(3001, 25, True), (1500, 40, False)])
+def test_tiled_attractive_vs_oracle(cuda, shape, n, k, clustered):
+    rr, cc, v, Y = _graph(n, k, seed=n + k, clustered=clustered)
+    csr = _csr(n, rr, cc, v)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    want = O.attraction(rr, cc, v, Y.astype(np.float32).astype(np.float64))
+    got = _attr(_ctx(2, *shape), csr, y)
+    assert rel_l2(got, want) <= 1e-5
+    base = _attr(_ctx(0), csr, y)
+    assert rel_l2(got, base) <= 1e-5
+
+
+def test_tiled_repeat_calls_clear_accumulator(cuda):
+    rr, cc, v, Y = _graph(2001, 20, seed=5)
+    csr = _csr(2001, rr, cc, v)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    ctx = _ctx(2, 64, 256, 4)
+    a = _attr(ctx, csr, y)
+    b = _attr(ctx, csr, y)
+    assert rel_l2(a, b) <= 1e-6  # consume-and-clear: no accumulation across calls
+
+
+def test_tiled_row_range(cuda):
+    """Rows [a, b) of P against the full Y (the sharded multi-GPU layout)."""
+    n = 2500
+    rr, cc, v, Y = _graph(n, 30, seed=11)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    full = O.attraction(rr, cc, v, Y.astype(np.float32).astype(np.float64))
+    for a, b in ((0, 700), (700, 1901), (1901, n)):
+        csr = _csr(n, rr, cc, v, a, b)
+        got = _attr(_ctx(2, 128, 256, 6), csr, y)
+        assert rel_l2(got, full[a:b]) <= 1e-5
+
+
+def test_tiled_kl_and_gradient(cuda):
+    from paper_1712_09005_b200 import _lib
+    n = 3001
+    rr, cc, v, Y = _graph(n, 25, seed=3)
+    csr = _csr(n, rr, cc, v)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    res = {}
+    for mode in (0, 2):
+        ctx = _ctx(mode, 128, 512, 5)
+        ctx.set_affinities(csr)
+        kl = C.c_double()
+        _lib.check(ctx.lib.fitsne_kl(ctx.h, _lib.ptr(y), 1.0, C.byref(kl), ctx.stream), "kl")
+        g = torch.empty_like(y)
+        _lib.check(ctx.lib.fitsne_gradient(ctx.h, _lib.ptr(y), 12.0, _lib.ptr(g), None, ctx.stream),
+                   "gradient")
+        torch.cuda.synchronize()
+        res[mode] = (kl.value, g.cpu().numpy().astype(np.float64))
+    assert abs(res[2][0] - res[0][0]) <= 1e-6 * abs(res[0][0])
+    assert rel_l2(res[2][1], res[0][1]) <= 1e-5
+    Yd = Y.astype(np.float32).astype(np.float64)
+    want = O.grad(rr, cc, v, Yd, 12.0, min_intervals=20, p=3)
+    assert rel_l2(res[2][1], want) <= 1e-3
+
+
+def test_tiled_run_tsne_matches_csr(cuda):
+    """The fused iteration (SpMV + KL + update) with the tiled kernel tracks
+    the CSR kernel's trajectory over the first iterations."""
+    from paper_1712_09005_b200 import _lib, optimizer
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    n = 2000
+    rr, cc, v, _ = _graph(n, 20, seed=21)
+    P = SparseAffinities(n=n, rows=rr, cols=cc, values=v)
+    logs = {}
+    for mode in (0, 2):
+        ctx = _lib.context(0, 2, torch.float32, 3, 50, 1.0)
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, OPT_TILED, mode), "set_option")
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, OPT_ROWS, 256), "set_option")
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, OPT_COLS, 512), "set_option")
+        cfg = optimizer.TsneConfig(dims=2, n_iter=30, seed=1, dtype="float32", min_intervals=50,
+                                   exaggeration=optimizer.ExaggerationSchedule(12.0, 10))
+        logs[mode] = np.asarray(optimizer.run_tsne(affinities=P, config=cfg).kl_log, dtype=float)
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, OPT_TILED, 1), "set_option")
+    assert np.max(np.abs(logs[2] - logs[0]) / np.abs(logs[0])) <= 1e-4
+
+
+def test_misaligned_y_uses_csr_kernel(cuda):
+    rr, cc, v, Y = _graph(1001, 15, seed=8)
+    csr = _csr(1001, rr, cc, v)
+    buf = torch.zeros(2 * 1001 + 4, dtype=torch.float32, device="cuda")
+    y_al = buf[4:].view(1001, 2)   # 16-byte aligned: tiled kernel
+    y_al.copy_(torch.from_numpy(Y.astype(np.float32)))
+    buf2 = torch.zeros(2 * 1001 + 2, dtype=torch.float32, device="cuda")
+    y_mis = buf2[2:].view(1001, 2)  # 8-byte aligned only: bulk copies need 16, CSR kernel
+    y_mis.copy_(torch.from_numpy(Y.astype(np.float32)))
+    ctx = _ctx(2, 64, 128, 0)
+    a = _attr(ctx, csr, y_al)
+    b = _attr(ctx, csr, y_mis)
+    assert rel_l2(a, b) <= 1e-5
+
+
+def test_option_validation(cuda):
+    from paper_1712_09005_b200 import _lib
+    ctx = _lib.Context(0, 2, torch.float32, 3, 20, 1.0)
+    for opt, val in ((OPT_TILED, 3), (OPT_ROWS, 3), (OPT_COLS, 0), (OPT_COLS, 32768), (OPT_CTAS, -1)):
+        assert ctx.lib.fitsne_set_option(ctx.h, opt, val) != 0

@@ -23,7 +23,9 @@ def launches(path):
         name = d["Kernel Name"].split("(")[0]
         unit = d["Metric Unit"]
         v = float(d["Metric Value"].replace(",", ""))
-        v = v / 1e3 if unit == "nsecond" else (v if unit == "usecond" else v * 1e3)
+        scale = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0,
+                 "msecond": 1e3, "ms": 1e3}
+        v = v * scale[unit]
         agg[name].append(v)
     tot = sum(sum(v) for v in agg.values())
     out = []
@@ -59,7 +61,26 @@ def full(rep):
     return out
 
 
+def stalls(rep):
+    """Per kernel: warp stall reasons (cycles per issued instruction) and the
+    headline throughputs, largest first."""
+    raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr = rows[0]
+    pre, suf = "smsp__average_warps_issue_stalled_", "_per_issue_active.ratio"
+    out = []
+    for r in rows[2:]:
+        d = dict(zip(hdr, r))
+        st = {k[len(pre):-len(suf)]: float(v) for k, v in d.items()
+              if k.startswith(pre) and k.endswith(suf) and v not in ("", "n/a")}
+        st = dict(sorted(st.items(), key=lambda x: -x[1])[:8])
+        keep = {m: d.get(m) for m in METRICS if m in d}
+        out.append({"kernel": d["Kernel Name"].split("(")[0], "stalls": st, **keep})
+    return out
+
+
 if __name__ == "__main__":
     kind, path = sys.argv[1], sys.argv[2]
-    res = launches(path) if kind == "launches" else full(path)
+    res = {"launches": launches, "full": full, "stalls": stalls}[kind](path)
     print(json.dumps(res, indent=1))
