@@ -98,11 +98,16 @@ enum fitsne_option {
  *   is staged in shared memory by bulk copies; 2 = tiled whenever applicable.
  *   The tiled copy is built on first use after fitsne_set_affinities.
  *   FITSNE_OPT_TILE_ROWS / FITSNE_OPT_TILE_COLS: tile shape (rows per row
- *   block, default 4096; points per column chunk, default 6144); both even and
+ *   block, default 2048; points per column chunk, default 10240); both even and
  *   <= 16384.  Shapes whose shared-memory footprint (24 rows + 16 cols + 4.3
  *   rows bytes) exceeds 226 KiB use the CSR kernel.  FITSNE_OPT_TILED_CTAS:
- *   persistent grid of the tiled kernel (default 0 = one CTA per SM). */
+ *   persistent grid of the tiled kernel (default 0 = 13/16 of the SMs when the
+ *   repulsion runs concurrently on the side stream, else one CTA per SM). */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
+/* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
+ * only for its alignment): out[0..5] = {in use (0/1), tiles, slabs, slot
+ * groups, (row, chunk) segments, stored entries}. */
+int fitsne_tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, void* stream);
 
 /* --- a1: make_grid (nbody.py:118-150).  Device bbox reduction + fp64 grid
  * formulas; the grid is copied to *grid_host (one host sync) and kept as the

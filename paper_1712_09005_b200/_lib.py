@@ -52,6 +52,7 @@ _SIGS = {
     "fitsne_destroy": (_int, [_vp]),
     "fitsne_set_interp": (_int, [_vp, _int, _int, _dbl]),
     "fitsne_set_option": (_int, [_vp, _int, _int]),
+    "fitsne_tiled_stats": (_int, [_vp, _vp, _vp, _vp]),
     "fitsne_make_grid": (_int, [_vp, _vp, _i64, C.POINTER(Grid), _vp]),
     "fitsne_bbox": (_int, [_vp, _vp, _i64, C.POINTER(_dbl), _vp]),
     "fitsne_grid_from_bbox": (_int, [_vp, C.POINTER(_dbl), C.POINTER(Grid)]),

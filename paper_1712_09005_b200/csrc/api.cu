@@ -203,6 +203,12 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
   return FITSNE_EINVAL;
 }
 
+int fitsne_tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, void* stream) {
+  CTX_CHECK(ctx);
+  if (!out) { set_error("null output"); return FITSNE_EINVAL; }
+  return tiled_stats(ctx, Y, out, S_(stream));
+}
+
 int fitsne_make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, fitsne_grid* grid_host, void* stream) {
   CTX_CHECK(ctx);
   if (n < 1) { set_error("points must be a non-empty (N,) or (N, dims) array"); return FITSNE_EINVAL; }

@@ -136,7 +136,7 @@ struct fitsne_ctx {
   int overlap = 1;                 // 0 serial, 1 SpMV || repulsion, 2 same + priority repulsion
   int spmv_blocks_per_sm = 0;      // >0: persistent SpMV grid in the overlap modes
   int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable
-  int tile_rows = 4096, tile_cols = 6144, tiled_ctas = 0;
+  int tile_rows = 2048, tile_cols = 10240, tiled_ctas = 0;
   fitsne::TiledP* tiled = nullptr; // built lazily from the registered CSR
   double* kl_part = nullptr;       // where the last SpMV left its KL partials
   int kl_nparts = 0;

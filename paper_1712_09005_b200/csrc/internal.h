@@ -67,6 +67,7 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 // out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
 int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st);
 void free_tiled(fitsne_ctx* ctx);
+int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st);
 
 int read_scalars(fitsne_ctx* ctx, int count, cudaStream_t st);  // scal[0..count) -> h_scal
 int sub_inplace(fitsne_ctx* ctx, void* out, const void* q, int64_t count, cudaStream_t st);

@@ -37,6 +37,7 @@ namespace fitsne {
 // tile's header blob is.  The blob (16-byte aligned, copied into shared memory
 // with the chunk) holds
 //   int32 meta[4] = {row block, slab count, first group, group count}
+//   int32 wstart[32]         slab holding the first group of consumer warp w
 //   uint32 goff[nslab + 1]   group offsets of the slabs (padded to 4 entries)
 //   uint16 rows[nslab][32]   tile-local row of each lane (0xFFFF: empty lane)
 // where a "group" is 32 consecutive slots, one per lane.
@@ -44,11 +45,15 @@ struct TileLoad {
   int32_t chunk;
   int32_t hdr_bytes;
   int64_t hdr_off;
+  int32_t g0, ng;  // the tile's slot groups (for the L2 prefetch of its stream)
+  int32_t pad[2];
 };
 
 __host__ __device__ inline int hdr_goff_words(int nslab) { return (nslab + 1 + 3) & ~3; }
+constexpr int kHdrWstart = 16;                 // int32 wstart[32] after meta
+constexpr int kHdrGoff = kHdrWstart + 128;     // uint32 goff[] after wstart
 __host__ __device__ inline int hdr_bytes_for(int nslab) {
-  return 16 + 4 * hdr_goff_words(nslab) + 64 * nslab;
+  return kHdrGoff + 4 * hdr_goff_words(nslab) + 64 * nslab;
 }
 
 static constexpr int kTiledThreads = 1024;        // 31 consumer warps + 1 producer warp
@@ -56,10 +61,11 @@ static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
 static constexpr int kTiledU = 4;                 // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
 static constexpr int kTiledStages = 2;            // chunk + header ring depth
+static constexpr int kTiledPrefetch = 3;          // tiles of slot stream prefetched into L2
 
 struct TiledP {
   DevBuf tiles, sched, slab_off, rows, hdr, cols, vals, fattr, part;
-  int64_t ntiles = 0, nslabs = 0, nslots = 0;
+  int64_t ntiles = 0, nslabs = 0, nslots = 0, nseg = 0;
   int hdr_max = 0;  // largest header blob (bytes)
   int R = 0, C = 0, grid = 0;
   // the CSR this copy was built from
@@ -103,6 +109,17 @@ void free_tiled(fitsne_ctx* ctx) {
 // ---------------------------------------------------------------------------
 // build: CSR -> segments (row, chunk) -> sort by (tile, count desc) -> slabs
 // ---------------------------------------------------------------------------
+__global__ void k_rows_unsorted(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
+                                int64_t n_rows, int32_t* __restrict__ flag) {
+  const int lane = threadIdx.x & 31;
+  const int64_t r = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  if (r >= n_rows) return;
+  const int64_t b = rowptr[r], e = rowptr[r + 1];
+  bool bad = false;
+  for (int64_t k = b + 1 + lane; k < e; k += 32) bad |= col[k] < col[k - 1];
+  if (__any_sync(0xffffffffu, bad) && lane == 0) *flag = 1;
+}
+
 // segments of one row = maximal runs of entries in the same column chunk
 // (columns are sorted inside a row, so a chunk's entries are contiguous)
 __global__ void k_seg_count(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
@@ -238,17 +255,40 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
   const int sb = t_sb[t], ns = t_ns[t];
   unsigned char* h = hdr + t_hoff[t];
   int32_t* meta = reinterpret_cast<int32_t*>(h);
-  uint32_t* goff = reinterpret_cast<uint32_t*>(h + 16);
-  uint16_t* hr = reinterpret_cast<uint16_t*>(h + 16 + 4 * hdr_goff_words(ns));
+  int32_t* wstart = reinterpret_cast<int32_t*>(h + kHdrWstart);
+  uint32_t* goff = reinterpret_cast<uint32_t*>(h + kHdrGoff);
+  uint16_t* hr = reinterpret_cast<uint16_t*>(h + kHdrGoff + 4 * hdr_goff_words(ns));
   const uint32_t g0 = slab_off[sb];
+  const uint32_t ng = slab_off[sb + ns] - g0;
   if (lane == 0) {
     meta[0] = t_dense[t] / nch;
     meta[1] = ns;
     meta[2] = (int32_t)g0;
-    meta[3] = (int32_t)(slab_off[sb + ns] - g0);
+    meta[3] = (int32_t)ng;
+  }
+  {
+    // consumer warp `lane` starts at group ng * lane / kTiledConsumers: the
+    // last slab whose offset is <= that group
+    const uint32_t lo = (uint32_t)(((uint64_t)ng * (uint32_t)lane) / kTiledConsumers);
+    int a = 0, z = ns;
+    while (z - a > 1) {
+      const int m = (a + z) >> 1;
+      if (slab_off[sb + m] - g0 <= lo) a = m; else z = m;
+    }
+    wstart[lane] = a;
   }
   for (int j = lane; j < hdr_goff_words(ns); j += 32) goff[j] = j <= ns ? slab_off[sb + j] - g0 : 0u;
   for (int64_t k = lane; k < (int64_t)ns * 32; k += 32) hr[k] = rows[(int64_t)sb * 32 + k];
+}
+
+// Persistent grid: with the overlapped schedule about 1/5 of the SMs stay free
+// for the spread / FFT stages running concurrently on the side stream (the
+// tiled kernel fills an SM: 1024 threads x 64 registers, ~210 KB of shared
+// memory); serial schedules use every SM.
+static int tiled_grid(const fitsne_ctx* ctx) {
+  if (ctx->tiled_ctas > 0) return ctx->tiled_ctas;
+  if (ctx->overlap != 0) return std::max(1, (ctx->num_sms * 13) / 16);
+  return ctx->num_sms;
 }
 
 struct TmpBufs {
@@ -293,12 +333,41 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     return FITSNE_ETOOBIG;
   }
   TmpBufs tmp;
+  // rows must list their columns in ascending order (one segment per row and
+  // chunk); sort a copy if the registered CSR does not
+  const int32_t* col = ctx->col;
+  const float* val = (const float*)ctx->val;
+  {
+    int32_t* flag;
+    FITSNE_TRY(tmp.alloc(&flag, 1));
+    FITSNE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
+    k_rows_unsorted<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, col, n_rows, flag);
+    FITSNE_CHECK_LAUNCH();
+    int32_t h_flag = 0;
+    FITSNE_CUDA(cudaMemcpyAsync(&h_flag, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    FITSNE_CUDA(cudaStreamSynchronize(st));
+    if (h_flag) {
+      int32_t* scol;
+      float* sval;
+      FITSNE_TRY(tmp.alloc(&scol, nnz));
+      FITSNE_TRY(tmp.alloc(&sval, nnz));
+      size_t bytes = 0;
+      FITSNE_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, col, scol, val, sval, nnz, n_rows,
+                                                      ctx->rowptr, ctx->rowptr + 1, st));
+      unsigned char* tb;
+      FITSNE_TRY(tmp.alloc(&tb, bytes));
+      FITSNE_CUDA(cub::DeviceSegmentedSort::SortPairs(tb, bytes, col, scol, val, sval, nnz, n_rows,
+                                                      ctx->rowptr, ctx->rowptr + 1, st));
+      col = scol;
+      val = sval;
+    }
+  }
   int32_t* segcnt;
   int64_t* segstart;
   FITSNE_TRY(tmp.alloc(&segcnt, n_rows + 1));
   FITSNE_TRY(tmp.alloc(&segstart, n_rows + 1));
   FITSNE_CUDA(cudaMemsetAsync(segcnt, 0, sizeof(int32_t) * (n_rows + 1), st));
-  k_seg_count<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, ctx->col, n_rows, C, segcnt);
+  k_seg_count<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, col, n_rows, C, segcnt);
   FITSNE_CHECK_LAUNCH();
   FITSNE_TRY(excl_scan(tmp, segcnt, segstart, n_rows + 1, st));
   int64_t nseg = 0;
@@ -317,7 +386,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
   FITSNE_TRY(tmp.alloc(&key2, nseg));
   FITSNE_TRY(tmp.alloc(&idx, nseg));
   FITSNE_TRY(tmp.alloc(&idx2, nseg));
-  k_seg_emit<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, ctx->col, n_rows, C, (int)nch, R,
+  k_seg_emit<<<nb(n_rows * 32, 256), 256, 0, st>>>(ctx->rowptr, col, n_rows, C, (int)nch, R,
                                                    segstart, seg_begin, seg_row, key);
   FITSNE_CHECK_LAUNCH();
   k_seg_finish<<<nb(nseg, 256), 256, 0, st>>>(ctx->rowptr, segstart, seg_begin, seg_row, nseg, key,
@@ -371,7 +440,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
   FITSNE_CUDA(cudaMemsetAsync(T->cols.ptr, 0, sizeof(uint16_t) * (size_t)(nslots + kTiledPad), st));
   FITSNE_CUDA(cudaMemsetAsync(T->vals.ptr, 0, sizeof(float) * (size_t)(nslots + kTiledPad), st));
   k_tile_fill<<<nb(nseg, 256), 256, 0, st>>>(key2, idx2, nseg, tfirst, slab_begin, slab_off, seg_begin,
-                                             seg_row, seg_cnt, ctx->col, (const float*)ctx->val,
+                                             seg_row, seg_cnt, col, val,
                                              (int)nch, R, C, (uint16_t*)T->rows.ptr,
                                              (uint16_t*)T->cols.ptr, (float*)T->vals.ptr);
   FITSNE_CHECK_LAUNCH();
@@ -401,6 +470,9 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     d.chunk = (int32_t)(t % nch);
     d.hdr_bytes = hdr_bytes_for(ns);
     d.hdr_off = hoff;
+    d.g0 = (int32_t)h_off[h_sb[t]];
+    d.ng = (int32_t)(h_off[h_sb[t] + ns] - h_off[h_sb[t]]);
+    d.pad[0] = d.pad[1] = 0;
     hoff += d.hdr_bytes;
     hmax = std::max(hmax, d.hdr_bytes);
     const double groups = (double)(h_off[h_sb[t] + ns] - h_off[h_sb[t]]);
@@ -431,7 +503,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     FITSNE_CHECK_LAUNCH();
     FITSNE_CUDA(cudaStreamSynchronize(st));
   }
-  const int grid = ctx->tiled_ctas > 0 ? ctx->tiled_ctas : ctx->num_sms;
+  const int grid = tiled_grid(ctx);
   std::vector<int32_t> sched(grid + 1, (int32_t)nt);
   double total = 0;
   for (double c : cost) total += c;
@@ -458,6 +530,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
   release_buf(T->rows);      // folded into the header blobs
   release_buf(T->slab_off);
   T->ntiles = nt;
+  T->nseg = nseg;
   T->nslabs = nslabs;
   T->nslots = nslots;
   T->hdr_max = hmax;
@@ -485,7 +558,7 @@ bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
                     T->n_rows == ctx->n_rows && T->row_begin == ctx->row_begin &&
                     T->n_total == ctx->n_total && T->nnz == ctx->nnz && T->R == ctx->tile_rows &&
                     T->C == ctx->tile_cols &&
-                    T->grid == (ctx->tiled_ctas > 0 ? ctx->tiled_ctas : ctx->num_sms);
+                    T->grid == (tiled_grid(ctx));
   if (same) return !T->failed;
   if (T && T->failed && T->rowptr == ctx->rowptr && T->col == ctx->col && T->val == ctx->val &&
       T->nnz == ctx->nnz)
@@ -502,7 +575,7 @@ bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
   T->nnz = ctx->nnz;
   T->R = ctx->tile_rows;
   T->C = ctx->tile_cols;
-  T->grid = ctx->tiled_ctas > 0 ? ctx->tiled_ctas : ctx->num_sms;
+  T->grid = tiled_grid(ctx);
   if (ctx->n_rows < 1 || ctx->nnz < 1 || build_tiled(ctx, T, st) != FITSNE_OK) {
     // keep the CSR kernel for this P; release what the attempt allocated
     cudaStreamSynchronize(st);
@@ -556,6 +629,20 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
+// bulk prefetch of [p, p + bytes) into L2 (16-byte granularity)
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+__device__ __forceinline__ void prefetch_tile(const TileLoad& d, const uint16_t* cols, const float* vals) {
+  const char* c = reinterpret_cast<const char*>(cols + (size_t)d.g0 * 32);
+  const char* v = reinterpret_cast<const char*>(vals + (size_t)d.g0 * 32);
+  const size_t cb = (size_t)d.ng * 64, vb = (size_t)d.ng * 128;
+  constexpr size_t kPiece = 1 << 16;
+  for (size_t o = 0; o < cb; o += kPiece) prefetch_l2(c + o, (uint32_t)(cb - o < kPiece ? cb - o : kPiece));
+  for (size_t o = 0; o < vb; o += kPiece) prefetch_l2(v + o, (uint32_t)(vb - o < kPiece ? vb - o : kPiece));
+}
+
 // consumer-only barrier (the producer warp never joins it)
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kTiledConsumers * 32) : "memory");
@@ -604,8 +691,11 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   if (warp == kTiledConsumers) {
     // ---------------- producer ----------------
     if (lane == 0) {
+      // the slot streams of the first tiles go to L2 ahead of the consumers
+      for (int t = t0; t < t1 && t < t0 + kTiledPrefetch; ++t) prefetch_tile(tiles[t], cols, vals);
       for (int t = t0; t < t1; ++t) {
         const int it = t - t0, b = it % kTiledStages;
+        if (t + kTiledPrefetch < t1) prefetch_tile(tiles[t + kTiledPrefetch], cols, vals);
         if (it >= kTiledStages) mbar_wait(&empty[b], (uint32_t)(((it / kTiledStages) - 1) & 1));
         const TileLoad d = tiles[t];
         unsigned char* st = ring + (size_t)b * stage_sz;
@@ -655,8 +745,8 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
     const int rb = meta[0], ns = meta[1];
     const int64_t g0 = (uint32_t)meta[2];
     const int ng = meta[3];
-    const uint32_t* goff = reinterpret_cast<const uint32_t*>(h + 16);
-    const uint16_t* hrows = reinterpret_cast<const uint16_t*>(h + 16 + 4 * hdr_goff_words(ns));
+    const uint32_t* goff = reinterpret_cast<const uint32_t*>(h + kHdrGoff);
+    const uint16_t* hrows = reinterpret_cast<const uint16_t*>(h + kHdrGoff + 4 * hdr_goff_words(ns));
     if (rb != cur_rb) {
       consumer_sync();  // every consumer is done with the previous row block
       if (cur_rb >= 0) flush_block();
@@ -674,13 +764,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
     const int lo = (int)(((int64_t)ng * warp) / kTiledConsumers);
     const int hi = (int)(((int64_t)ng * (warp + 1)) / kTiledConsumers);
     if (lo < hi) {
-      // slab containing group lo: last s with goff[s] <= lo
-      int a = 0, z = ns;
-      while (z - a > 1) {
-        const int m = (a + z) >> 1;
-        if ((int)goff[m] <= lo) a = m; else z = m;
-      }
-      int s = a;
+      int s = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
       int s_end = (int)goff[s + 1];
       bool shared_slab = (int)goff[s] < lo || s_end > hi;
       int row = hrows[s * 32 + lane];
@@ -707,42 +791,43 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
         pA[u] = __ldcs(vp + u * 32);
       }
-      for (int g = lo; g < hi; g += kTiledU) {
+      // one group: slab boundary check (warp-uniform), gather, accumulate
+      auto step = [&](int gg, unsigned short c, float p) {
+        if (gg == s_end) {
+          flush_row();
+          ax = ay = 0.f;
+          ++s;
+          s_end = (int)goff[s + 1];
+          shared_slab = s_end > hi;
+          row = hrows[s * 32 + lane];
+          yi = row != 0xFFFF ? ys[row] : make_float2(0.f, 0.f);
+        }
+        const float2 yj = cb[c];
+        const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+        const float q = 1.0f + (dx * dx + dy * dy);
+        const float w = p * rcp_approx(q);
+        ax += w * dx;
+        ay += w * dy;
+        if (KL) kl += p * __logf(q);
+      };
+      int g = lo;
+      for (; g + kTiledU <= hi; g += kTiledU) {
         // prefetch the next step (reads past hi stay inside the padded arrays)
 #pragma unroll
         for (int u = 0; u < kTiledU; ++u) {
           cB[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + (kTiledU + u) * 32);
           pB[u] = __ldcs(vp + (kTiledU + u) * 32);
         }
-        float2 yj[kTiledU];
 #pragma unroll
-        for (int u = 0; u < kTiledU; ++u) yj[u] = cb[cA[u]];
-#pragma unroll
-        for (int u = 0; u < kTiledU; ++u) {
-          const int gg = g + u;
-          if (gg < hi) {
-            if (gg == s_end) {  // warp-uniform slab boundary
-              flush_row();
-              ax = ay = 0.f;
-              ++s;
-              s_end = (int)goff[s + 1];
-              shared_slab = s_end > hi;
-              row = hrows[s * 32 + lane];
-              yi = row != 0xFFFF ? ys[row] : make_float2(0.f, 0.f);
-            }
-            const float dx = yi.x - yj[u].x, dy = yi.y - yj[u].y;
-            const float q = 1.0f + (dx * dx + dy * dy);
-            const float w = pA[u] * rcp_approx(q);
-            ax += w * dx;
-            ay += w * dy;
-            if (KL) kl += pA[u] * __logf(q);
-          }
-        }
+        for (int u = 0; u < kTiledU; ++u) step(g + u, cA[u], pA[u]);
 #pragma unroll
         for (int u = 0; u < kTiledU; ++u) { cA[u] = cB[u]; pA[u] = pB[u]; }
         cp += kTiledU * 32;
         vp += kTiledU * 32;
       }
+#pragma unroll
+      for (int u = 0; u < kTiledU - 1; ++u)
+        if (g + u < hi) step(g + u, cA[u], pA[u]);
       flush_row();
       if (KL) { kld += (double)kl; kl = 0.f; }
     }
@@ -810,6 +895,18 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
   *fattr_out = T->fattr.ptr;
   if (part_out) *part_out = part;
   if (nparts) *nparts = T->grid;
+  return FITSNE_OK;
+}
+
+int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st) {
+  const bool use = tiled_usable(ctx, Y, st);
+  TiledP* T = ctx->tiled;
+  out[0] = use ? 1 : 0;
+  out[1] = use ? T->ntiles : 0;
+  out[2] = use ? T->nslabs : 0;
+  out[3] = use ? T->nslots / 32 : 0;
+  out[4] = use ? T->nseg : 0;
+  out[5] = ctx->nnz;
   return FITSNE_OK;
 }
 

@@ -177,3 +177,21 @@ def test_option_validation(cuda):
     ctx = _lib.Context(0, 2, torch.float32, 3, 20, 1.0)
     for opt, val in ((OPT_TILED, 3), (OPT_ROWS, 3), (OPT_COLS, 0), (OPT_COLS, 32768), (OPT_CTAS, -1)):
         assert ctx.lib.fitsne_set_option(ctx.h, opt, val) != 0
+
+
+def test_tiled_unsorted_rows(cuda):
+    """A CSR whose rows are not column-sorted (a relabelled P) is re-sorted
+    by the tiled build: every (row, chunk) is still one segment."""
+    from paper_1712_09005_b200.affinities import permute_csr
+    n = 3001
+    rr, cc, v, Y = _graph(n, 25, seed=17)
+    csr = _csr(n, rr, cc, v)
+    perm = torch.from_numpy(np.random.default_rng(0).permutation(n)).cuda()
+    inv = torch.empty_like(perm)
+    inv[perm] = torch.arange(n, device="cuda")
+    pcsr = permute_csr(csr, perm, inv)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()[perm].contiguous()
+    want = O.attraction(rr, cc, v, Y.astype(np.float32).astype(np.float64))[perm.cpu().numpy()]
+    for shape in ((64, 128, 0), (512, 1024, 9)):
+        got = _attr(_ctx(2, *shape), pcsr, y)
+        assert rel_l2(got, want) <= 1e-5

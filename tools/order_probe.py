@@ -79,22 +79,27 @@ def main():
         key[m] = (cl << 40) | morton(lp, 13)
     orders["cluster_localpc3"] = torch.argsort(key)
 
-    ctx = _lib.context(0, 2, torch.float32, 3, 50, 1.0)
+    ctxs = {}
+    for mode in (0, 2):
+        c = _lib.Context(0, 2, torch.float32, 3, 50, 1.0)
+        _lib.check(c.lib.fitsne_set_option(c.h, 5, mode), "opt")
+        ctxs[mode] = c
     for name, perm in orders.items():
         inv = torch.empty_like(perm)
         inv[perm] = torch.arange(n, device="cuda")
         csr = permute_csr(base, perm, inv)
         y = Y[perm].contiguous()
-        ctx.set_affinities(csr)
         g = torch.empty_like(y)
         f = torch.zeros_like(y)
-        t_spmv = timed(lambda: _lib.check(ctx.lib.fitsne_gradient_rows(
-            ctx.h, _lib.ptr(y), _lib.ptr(f), 1.0, _lib.ptr(g), ctx.stream), "rows"))
-        t_grad = timed(lambda: _lib.check(ctx.lib.fitsne_gradient(
-            ctx.h, _lib.ptr(y), 1.0, _lib.ptr(g), None, ctx.stream), "grad"))
-        # neighbour-label spread: mean |i - j| over stored entries (sampled rows)
-        rp = csr.rowptr
-        print(f"{name:18s} spmv {t_spmv * 1e3:7.1f} us  gradient {t_grad * 1e3:7.1f} us", flush=True)
+        line = f"{name:18s}"
+        for mode, ctx in ctxs.items():
+            ctx.set_affinities(csr)
+            t_spmv = timed(lambda: _lib.check(ctx.lib.fitsne_gradient_rows(
+                ctx.h, _lib.ptr(y), _lib.ptr(f), 1.0, _lib.ptr(g), ctx.stream), "rows"))
+            t_grad = timed(lambda: _lib.check(ctx.lib.fitsne_gradient(
+                ctx.h, _lib.ptr(y), 1.0, _lib.ptr(g), None, ctx.stream), "grad"))
+            line += f" | {'tiled' if mode else 'csr'} spmv {t_spmv * 1e3:6.1f} us grad {t_grad * 1e3:6.1f} us"
+        print(line, flush=True)
         del csr
 
 
