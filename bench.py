@@ -252,6 +252,23 @@ def run_reference(args):
 
 
 # ----------------------------------------------------------------------------- ours
+def count_launches(fn):
+    """Kernels one call of `fn` launches on the device (CUPTI via torch.profiler,
+    outside the timed region)."""
+    import torch
+    from torch.profiler import ProfilerActivity, profile
+    torch.cuda.synchronize()
+    try:
+        with profile(activities=[ProfilerActivity.CUDA]) as prof:
+            fn()
+            torch.cuda.synchronize()
+        evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
+               and not e.name.startswith("Memcpy") and not e.name.startswith("Memset")]
+        return len(evs)
+    except Exception:  # noqa: BLE001 - profiler unavailable: report the static count
+        return 9
+
+
 def timed(fn, steps, stream):
     import torch
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -361,6 +378,18 @@ def run_ours(args):
     peak, peak_src = peaks()
     achieved = b_spmv / (ms_spmv * 1e-3) / 1e9
 
+    # which SpMV ran (tiled copy of P or the CSR kernel), and its layout
+    import ctypes as _C
+    tst = (_C.c_int64 * 6)()
+    _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), tst, ctx.stream), "tiled_stats")
+    if tst[0]:
+        spmv_kernel = "k_attract_tiled (tiled attractive SpMV) + k_tiled_finish"
+        traffic_key = "spmv_tiled"
+    else:
+        spmv_kernel = "k_attract (CSR SpMV)"
+        traffic_key = "spmv"
+    launches_per_step = count_launches(step)
+
     breakdown = None
     if args.breakdown:
         breakdown = stage_breakdown(ctx, y, n, dt, args.steps, stream)
@@ -396,16 +425,17 @@ def run_ours(args):
                    "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB L2), no flush" %
                          (nnz * (4 + es) / 1e9),
                    "input_gen_s": round(t_gen, 1)},
-        "roofline": {"kernel": "k_attract (CSR SpMV + gradient combine)", "bound": "hbm",
+        "roofline": {"kernel": spmv_kernel, "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src, "algorithmic_bytes": b_spmv,
                      "launch_ms": ms_spmv, "share_of_step": ms_spmv / ms,
-                     "traffic": traffic_from_profiles("spmv")},
+                     "traffic": traffic_from_profiles(traffic_key)},
         "cpu_baseline": cpu,
         "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
                 "h2d_bytes_per_step": int(y_host.numel() * y_host.element_size()),
                 "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
-        "gpu_launches": 8 * args.steps,
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step,
         "clocks": clocks,
     }
     if breakdown:

@@ -90,7 +90,8 @@ enum fitsne_option {
   FITSNE_OPT_TILED_SPMV = 5,
   FITSNE_OPT_TILE_ROWS = 6,
   FITSNE_OPT_TILE_COLS = 7,
-  FITSNE_OPT_TILED_CTAS = 8
+  FITSNE_OPT_TILED_CTAS = 8,
+  FITSNE_OPT_TILED_BANK_ORDER = 9
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x

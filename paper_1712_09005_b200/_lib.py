@@ -9,13 +9,15 @@ library's own sm_100a code.
 from __future__ import annotations
 
 import ctypes as C
+import os
 import threading
 from pathlib import Path
 
 import torch
 
 _PKG = Path(__file__).resolve().parent
-LIB_PATH = _PKG / "libfitsne_b200.so"
+# FITSNE_LIB selects another in-tree build of the library (A/B experiments)
+LIB_PATH = _PKG / os.environ.get("FITSNE_LIB", "libfitsne_b200.so")
 
 OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG = range(8)
 F32, F64 = 0, 1

@@ -194,6 +194,11 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     ctx->tile_cols = C;
     return FITSNE_OK;
   }
+  if (option == FITSNE_OPT_TILED_BANK_ORDER) {
+    if (value < 0 || value > 1) { set_error("bank order must be 0 or 1"); return FITSNE_EINVAL; }
+    ctx->tiled_bank_order = value;
+    return FITSNE_OK;
+  }
   if (option == FITSNE_OPT_TILED_CTAS) {
     if (value < 0 || value > 65536) { set_error("tiled CTAs must be in [0, 65536]"); return FITSNE_EINVAL; }
     ctx->tiled_ctas = value;

@@ -137,6 +137,7 @@ struct fitsne_ctx {
   int spmv_blocks_per_sm = 0;      // >0: persistent SpMV grid in the overlap modes
   int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable
   int tile_rows = 2048, tile_cols = 10240, tiled_ctas = 0;
+  int tiled_bank_order = 1;        // bank-aware slot order inside slabs (tiled build)
   fitsne::TiledP* tiled = nullptr; // built lazily from the registered CSR
   double* kl_part = nullptr;       // where the last SpMV left its KL partials
   int kl_nparts = 0;

@@ -45,7 +45,7 @@ struct TileLoad {
   int32_t chunk;
   int32_t hdr_bytes;
   int64_t hdr_off;
-  int32_t g0, ng;  // the tile's slot groups (for the L2 prefetch of its stream)
+  int32_t g0, ng;  // the tile's slot groups
   int32_t pad[2];
 };
 
@@ -56,12 +56,15 @@ __host__ __device__ inline int hdr_bytes_for(int nslab) {
   return kHdrGoff + 4 * hdr_goff_words(nslab) + 64 * nslab;
 }
 
-static constexpr int kTiledThreads = 1024;        // 31 consumer warps + 1 producer warp
+static constexpr int kTiledThreads = 1024;  // 31 consumer warps + 1 producer warp
 static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
 static constexpr int kTiledU = 4;                 // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
+
+// Slot layout: group-major, lane-minor (a warp reads one group's columns and
+// values with one coalesced 64-byte and one 128-byte load).
+__host__ __device__ inline int64_t slot_index(int64_t g, int lane) { return g * 32 + lane; }
 static constexpr int kTiledStages = 2;            // chunk + header ring depth
-static constexpr int kTiledPrefetch = 3;          // tiles of slot stream prefetched into L2
 
 struct TiledP {
   DevBuf tiles, sched, slab_off, rows, hdr, cols, vals, fattr, part;
@@ -238,9 +241,79 @@ __global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __
   const int c = seg_cnt[s];
   const int64_t o = (int64_t)slab_off[slab];
   for (int k = 0; k < c; ++k) {
-    const int64_t slot = (o + k) * 32 + lane;
+    const int64_t slot = slot_index(o + k, lane);
     cols[slot] = (uint16_t)(col[b + k] - ch * C);
     vals[slot] = val[b + k];
+  }
+}
+
+// Bank-aware slot order.  Inside a slab, lane l may visit its row's entries in
+// any order; the y_j gather of step k is a 64-bit shared-memory load whose
+// half-warps conflict when two lanes hit the same bank pair (column mod 16).
+// Greedily pick, step by step and lane by lane, the remaining entry whose bank
+// pair is least used in the lane's half-warp.  Slabs longer than kBankCap keep
+// their order.  One warp per slab.
+static constexpr int kBankCap = 32;
+static constexpr int kBankWarps = 4;
+__global__ void __launch_bounds__(kBankWarps * 32)
+k_slab_bankorder(const uint32_t* __restrict__ slab_off, int64_t nslabs, uint16_t* __restrict__ cols,
+                 float* __restrict__ vals) {
+  __shared__ uint16_t lc[kBankWarps][32][kBankCap];
+  __shared__ float lv[kBankWarps][32][kBankCap];
+  __shared__ int cnt[kBankWarps][2][16];
+  const int lane = threadIdx.x & 31, wl = threadIdx.x >> 5;
+  const int64_t sl = blockIdx.x * (int64_t)kBankWarps + wl;
+  if (sl >= nslabs) return;
+  const int64_t o = slab_off[sl];
+  const int kmax = (int)(slab_off[sl + 1] - o);
+  if (kmax > kBankCap || kmax < 2) return;
+  // this lane's non-zero entries
+  int n = 0;
+  for (int k = 0; k < kmax; ++k) {
+    const size_t slot = (size_t)slot_index(o + k, lane);
+    const float v = vals[slot];
+    if (v != 0.f) {
+      lc[wl][lane][n] = cols[slot];
+      lv[wl][lane][n] = v;
+      ++n;
+    }
+  }
+  unsigned used = 0;
+  const int half = lane >> 4, hl = lane & 15;
+  for (int k = 0; k < kmax; ++k) {
+    if (lane < 32) {
+      if (hl == 0) {
+        for (int b = 0; b < 16; ++b) cnt[wl][half][b] = 0;
+      }
+    }
+    __syncwarp();
+    // lanes past their entries read column 0 (bank pair 0)
+    const unsigned pad = __ballot_sync(0xffffffffu, k >= n);
+    if (hl == 0) {
+      const unsigned mine = half ? (pad >> 16) : (pad & 0xffffu);
+      if (mine) cnt[wl][half][0] += 1;
+    }
+    __syncwarp();
+    uint16_t pc = 0;
+    float pv = 0.f;
+    for (int i = 0; i < 16; ++i) {
+      if (hl == i && k < n) {
+        int best = -1, bc = 1 << 30;
+        for (int e = 0; e < n; ++e) {
+          if (used & (1u << e)) continue;
+          const int c = cnt[wl][half][lc[wl][lane][e] & 15];
+          if (c < bc) { bc = c; best = e; }
+        }
+        used |= 1u << best;
+        pc = lc[wl][lane][best];
+        pv = lv[wl][lane][best];
+        cnt[wl][half][pc & 15] += 1;
+      }
+      __syncwarp();
+    }
+    const size_t slot = (size_t)slot_index(o + k, lane);
+    cols[slot] = k < n ? pc : (uint16_t)0;
+    vals[slot] = k < n ? pv : 0.f;
   }
 }
 
@@ -444,6 +517,11 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
                                              (int)nch, R, C, (uint16_t*)T->rows.ptr,
                                              (uint16_t*)T->cols.ptr, (float*)T->vals.ptr);
   FITSNE_CHECK_LAUNCH();
+  if (ctx->tiled_bank_order) {
+    k_slab_bankorder<<<nb(nslabs, kBankWarps), kBankWarps * 32, 0, st>>>(
+        slab_off, nslabs, (uint16_t*)T->cols.ptr, (float*)T->vals.ptr);
+    FITSNE_CHECK_LAUNCH();
+  }
 
   // host: compact tile list, header blobs, static schedule balanced on cost
   std::vector<int32_t> h_nslab(ntd), h_sb(ntd);
@@ -629,18 +707,21 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
       : "memory");
 }
 
-// bulk prefetch of [p, p + bytes) into L2 (16-byte granularity)
-__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
-  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+// L2 eviction policy for the Y chunks, which every row block re-reads while
+// the slot stream passes through L2 once
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
 }
 
-__device__ __forceinline__ void prefetch_tile(const TileLoad& d, const uint16_t* cols, const float* vals) {
-  const char* c = reinterpret_cast<const char*>(cols + (size_t)d.g0 * 32);
-  const char* v = reinterpret_cast<const char*>(vals + (size_t)d.g0 * 32);
-  const size_t cb = (size_t)d.ng * 64, vb = (size_t)d.ng * 128;
-  constexpr size_t kPiece = 1 << 16;
-  for (size_t o = 0; o < cb; o += kPiece) prefetch_l2(c + o, (uint32_t)(cb - o < kPiece ? cb - o : kPiece));
-  for (size_t o = 0; o < vb; o += kPiece) prefetch_l2(v + o, (uint32_t)(vb - o < kPiece ? vb - o : kPiece));
+__device__ __forceinline__ void bulk_g2s_hint(void* dst, const void* src, uint32_t bytes, uint64_t* b,
+                                              uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, "
+      "[%3], %4;" ::"r"(smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(b)), "l"(pol)
+      : "memory");
 }
 
 // consumer-only barrier (the producer warp never joins it)
@@ -691,11 +772,9 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   if (warp == kTiledConsumers) {
     // ---------------- producer ----------------
     if (lane == 0) {
-      // the slot streams of the first tiles go to L2 ahead of the consumers
-      for (int t = t0; t < t1 && t < t0 + kTiledPrefetch; ++t) prefetch_tile(tiles[t], cols, vals);
+      const uint64_t pol_y = policy_evict_last();
       for (int t = t0; t < t1; ++t) {
         const int it = t - t0, b = it % kTiledStages;
-        if (t + kTiledPrefetch < t1) prefetch_tile(tiles[t + kTiledPrefetch], cols, vals);
         if (it >= kTiledStages) mbar_wait(&empty[b], (uint32_t)(((it / kTiledStages) - 1) & 1));
         const TileLoad d = tiles[t];
         unsigned char* st = ring + (size_t)b * stage_sz;
@@ -709,7 +788,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         if (cnt & 1) cdst[cnt - 1] = Y[c0 + cnt - 1];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(&full[b], cbytes + (uint32_t)d.hdr_bytes);
-        if (cbytes) bulk_g2s(cdst, Y + c0, cbytes, &full[b]);
+        if (cbytes) bulk_g2s_hint(cdst, Y + c0, cbytes, &full[b], pol_y);
         bulk_g2s(hdst, hdr + d.hdr_off, (uint32_t)d.hdr_bytes, &full[b]);
       }
     }
@@ -718,8 +797,9 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
 
   // ---------------- consumers ----------------
   // Work split: consumer warps take equal runs of the tile's slot groups; a
-  // slab cut by a run boundary is shared by two warps and flushed atomically,
-  // every other slab belongs to one warp.  Across tiles, consumers are at most
+  // slab cut by a run boundary is shared by two or more warps, which add
+  // their partials to the output with L2 vector reductions; every other slab
+  // belongs to one warp and is flushed into shared memory.  Across tiles, consumers are at most
   // one tile apart (the producer refills a stage only after every consumer
   // released it), so even and odd tiles accumulate into separate arrays and
   // those flushes are plain shared-memory read-modify-writes.
@@ -773,8 +853,10 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       auto flush_row = [&]() {
         if (row == 0xFFFF) return;
         if (shared_slab) {
-          atomicAdd(&accp[row].x, ax);
-          atomicAdd(&accp[row].y, ay);
+          // rows of a slab cut by a warp-range boundary are updated by two or
+          // more warps of this tile: add straight to the output with a vector
+          // reduction in L2 instead of a shared-memory compare-and-swap loop
+          atomicAdd(fattr + r0 + row, make_float2(ax, ay));
         } else {
           float2 v = accp[row];
           v.x += ax;
@@ -782,15 +864,6 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
           accp[row] = v;
         }
       };
-      const uint16_t* cp = cols + (size_t)(g0 + lo) * 32 + lane;
-      const float* vp = vals + (size_t)(g0 + lo) * 32 + lane;
-      unsigned short cA[kTiledU], cB[kTiledU];
-      float pA[kTiledU], pB[kTiledU];
-#pragma unroll
-      for (int u = 0; u < kTiledU; ++u) {
-        cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
-        pA[u] = __ldcs(vp + u * 32);
-      }
       // one group: slab boundary check (warp-uniform), gather, accumulate
       auto step = [&](int gg, unsigned short c, float p) {
         if (gg == s_end) {
@@ -810,6 +883,15 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         ay += w * dy;
         if (KL) kl += p * __logf(q);
       };
+      const uint16_t* cp = cols + (size_t)slot_index(g0 + lo, lane);
+      const float* vp = vals + (size_t)slot_index(g0 + lo, lane);
+      unsigned short cA[kTiledU], cB[kTiledU];
+      float pA[kTiledU], pB[kTiledU];
+#pragma unroll
+      for (int u = 0; u < kTiledU; ++u) {
+        cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
+        pA[u] = __ldcs(vp + u * 32);
+      }
       int g = lo;
       for (; g + kTiledU <= hi; g += kTiledU) {
         // prefetch the next step (reads past hi stay inside the padded arrays)

@@ -32,7 +32,8 @@ def timed(fn, steps=20):
 def main():
     args = [a for a in sys.argv[1:] if not a.startswith("--")]
     ncu = "--ncu" in sys.argv
-    shapes = [tuple(int(x) for x in a.split(",")) for a in args] or [(4096, 8192, 0)]
+    shapes = [tuple(int(x) for x in a.split(",")) for a in args] or [(2048, 10240, 0)]
+    shapes = [sh if len(sh) == 4 else (*sh, 1) for sh in shapes]  # R, C, ctas, bank order
     n = 1_300_000
     t0 = time.time()
     P, Y = synth.c3(device="cuda", n=n)
@@ -45,8 +46,8 @@ def main():
     print(f"inputs {time.time() - t0:.1f}s", flush=True)
     f = torch.zeros_like(y)
     g = torch.empty_like(y)
-    configs = ([] if ncu else [(0, 0, 0, 0)]) + [(2, *s) for s in shapes]
-    for mode, R, C, ctas in configs:
+    configs = ([] if ncu else [(0, 0, 0, 0, 0)]) + [(2, *s) for s in shapes]
+    for mode, R, C, ctas, bank in configs:
         ctx = _lib.Context(0, 2, torch.float32, 3, 50, 1.0)
         _lib.check(ctx.lib.fitsne_set_option(ctx.h, 5, mode), "opt")
         if mode:
@@ -54,6 +55,7 @@ def main():
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 6, R), "opt")
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 7, C), "opt")
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 8, ctas), "opt")
+            _lib.check(ctx.lib.fitsne_set_option(ctx.h, 9, bank), "opt")
         ctx.set_affinities(csr)
 
         def rows():
@@ -80,7 +82,7 @@ def main():
             break
         t_rows = timed(rows)
         t_grad = timed(grad)
-        print(f"mode {mode} R {R:5d} C {C:5d} ctas {ctas:4d}: first call {build * 1e3:8.1f} ms  "
+        print(f"mode {mode} R {R:5d} C {C:5d} ctas {ctas:4d} bank {bank}: first call {build * 1e3:8.1f} ms  "
               f"spmv {t_rows * 1e3:7.1f} us  gradient {t_grad * 1e3:7.1f} us", flush=True)
         del ctx
 
