@@ -441,8 +441,7 @@ def run_ours(args):
     if breakdown:
         line["breakdown_ms"] = breakdown
     if args.full_run:
-        line["full_run"] = full_run(P, dt, dev)
-        line["full_run_no_reorder"] = full_run(P, dt, dev, reorder=False)
+        line["full_run"] = full_run(P, dt, dev, reorder=False)
     print(json.dumps(line), flush=True)
 
 

@@ -646,8 +646,9 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
-    FITSNE_TRY(make_grid(ctx, Y, n, ctx->side));
+    // the SpMV needs no grid: queue it before the bbox readback blocks the host
     FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
+    FITSNE_TRY(make_grid(ctx, Y, n, ctx->side));
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
@@ -675,9 +676,10 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
-    FITSNE_TRY(make_grid(ctx, Yin, n, ctx->side));
-    // SpMV + KL partials on st, spread + FFT on the side stream
+    // SpMV + KL partials on st (queued before the bbox readback blocks the
+    // host), spread + FFT on the side stream
     FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
+    FITSNE_TRY(make_grid(ctx, Yin, n, ctx->side));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));

@@ -364,13 +364,17 @@ static int tiled_grid(const fitsne_ctx* ctx) {
   return ctx->num_sms;
 }
 
+// Build temporaries come from the stream-ordered pool (no device-wide sync
+// on free, memory reused by the next build).
 struct TmpBufs {
+  cudaStream_t st;
   std::vector<void*> ptrs;
-  ~TmpBufs() { for (void* p : ptrs) cudaFree(p); }
+  explicit TmpBufs(cudaStream_t s) : st(s) {}
+  ~TmpBufs() { for (void* p : ptrs) cudaFreeAsync(p, st); }
   template <typename T>
   int alloc(T** out, size_t count) {
     void* p = nullptr;
-    if (cudaMalloc(&p, std::max<size_t>(count, 1) * sizeof(T)) != cudaSuccess) {
+    if (cudaMallocAsync(&p, std::max<size_t>(count, 1) * sizeof(T), st) != cudaSuccess) {
       cudaGetLastError();
       set_error("device allocation failed while tiling P");
       return FITSNE_ENOMEM;
@@ -405,7 +409,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     set_error("P too large for the tiled layout");
     return FITSNE_ETOOBIG;
   }
-  TmpBufs tmp;
+  TmpBufs tmp(st);
   // rows must list their columns in ascending order (one segment per row and
   // chunk); sort a copy if the registered CSR does not
   const int32_t* col = ctx->col;

@@ -80,10 +80,28 @@ def main():
             rows()
             torch.cuda.synchronize()
             break
+        zc = __import__("ctypes").c_double()
+
+        def kl():
+            _lib.check(ctx.lib.fitsne_kl(ctx.h, _lib.ptr(y), 1.0, __import__("ctypes").byref(zc),
+                                         ctx.stream), "kl")
+        vel = torch.zeros_like(y)
+        gains = torch.ones_like(y)
+        y2 = y.clone()
+        kd = torch.zeros(1, dtype=torch.float64, device=y.device)
+        stt = torch.zeros(1, dtype=torch.int32, device=y.device)
+
+        def iterate():
+            _lib.check(ctx.lib.fitsne_iterate(ctx.h, _lib.ptr(y), _lib.ptr(y2), _lib.ptr(vel),
+                                              _lib.ptr(gains), 1.0, 0.5, 200.0, _lib.ptr(kd),
+                                              _lib.ptr(stt), ctx.stream), "iterate")
         t_rows = timed(rows)
         t_grad = timed(grad)
+        t_kl = timed(kl)
+        t_it = timed(iterate)
         print(f"mode {mode} R {R:5d} C {C:5d} ctas {ctas:4d} bank {bank}: first call {build * 1e3:8.1f} ms  "
-              f"spmv {t_rows * 1e3:7.1f} us  gradient {t_grad * 1e3:7.1f} us", flush=True)
+              f"spmv {t_rows * 1e3:7.1f} us  gradient {t_grad * 1e3:7.1f} us  kl {t_kl * 1e3:7.1f} us  "
+              f"iterate {t_it * 1e3:7.1f} us", flush=True)
         del ctx
 
 
