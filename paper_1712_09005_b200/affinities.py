@@ -23,7 +23,13 @@ from dataclasses import dataclass
 import numpy as np
 import torch
 
-__all__ = ["SparseAffinities", "DeviceCSR", "device_csr", "csr_from_full"]
+__all__ = ["SparseAffinities", "DeviceCSR", "device_csr", "csr_from_full", "to_csr", "from_csr",
+           "save_affinities", "load_affinities", "FORMAT", "FORMAT_VERSION"]
+
+# on-disk format of P: a versioned .npz holding the full
+# symmetric CSR (both triangles) so the oracle and the GPU box read the same P
+FORMAT = "fitsne-b200-csr"
+FORMAT_VERSION = 1
 
 
 @dataclass
@@ -188,3 +194,78 @@ def permute_csr(csr: DeviceCSR, perm: torch.Tensor, inv: torch.Tensor) -> Device
     new_col = inv[col[src].long()].to(torch.int32)
     new_val = val[src]
     return DeviceCSR(new_rowptr, new_col.contiguous(), new_val.contiguous(), 0, n, csr.ordered_total)
+
+
+# ----------------------------------------------------------------------------- host CSR / files
+def to_csr(P):
+    """Full symmetric CSR on the host: (n, rowptr int64, col int32, val float64).
+
+    Rows list their columns in ascending order (the layout fitsne_set_affinities
+    and the tiled build expect)."""
+    if hasattr(P, "rows") and hasattr(P, "cols") and hasattr(P, "values"):
+        n = int(P.n)
+        r0 = np.asarray(P.rows, dtype=np.int64)
+        c0 = np.asarray(P.cols, dtype=np.int64)
+        v0 = np.asarray(P.values, dtype=np.float64)
+        r = np.concatenate([r0, c0])
+        c = np.concatenate([c0, r0])
+        v = np.concatenate([v0, v0])
+    else:
+        import scipy.sparse as sp
+        if not sp.issparse(P):
+            raise TypeError("affinities must be a SparseAffinities-like object or a scipy.sparse matrix")
+        coo = P.tocoo()
+        if coo.shape[0] != coo.shape[1]:
+            raise ValueError("affinity matrix must be square")
+        n = coo.shape[0]
+        r, c, v = coo.row.astype(np.int64), coo.col.astype(np.int64), coo.data.astype(np.float64)
+    order = np.lexsort((c, r))
+    r, c, v = r[order], c[order], v[order]
+    rowptr = np.zeros(n + 1, dtype=np.int64)
+    np.cumsum(np.bincount(r, minlength=n), out=rowptr[1:])
+    return n, rowptr, c.astype(np.int32), v
+
+
+def from_csr(n, rowptr, col, val) -> SparseAffinities:
+    """SparseAffinities (upper-triangle pairs) from a full symmetric CSR.
+
+    Raises ValueError unless the CSR is symmetric (every (i, j, p) has its
+    (j, i, p)) with an empty diagonal -- the invariants of the reference type
+    (affinities.py:78-104)."""
+    rowptr = np.asarray(rowptr, dtype=np.int64)
+    col = np.asarray(col, dtype=np.int64)
+    val = np.asarray(val, dtype=np.float64)
+    if rowptr.shape != (int(n) + 1,) or rowptr[0] != 0 or rowptr[-1] != col.size or col.size != val.size:
+        raise ValueError("malformed CSR")
+    row = np.repeat(np.arange(int(n), dtype=np.int64), np.diff(rowptr))
+    if np.any(row == col):
+        raise ValueError("affinities have a non-empty diagonal")
+    up = row < col
+    lo = ~up
+    ku = np.lexsort((col[up], row[up]))
+    kl = np.lexsort((row[lo], col[lo]))
+    ru, cu, vu = row[up][ku], col[up][ku], val[up][ku]
+    if not (np.array_equal(ru, col[lo][kl]) and np.array_equal(cu, row[lo][kl])
+            and np.array_equal(vu, val[lo][kl])):
+        raise ValueError("affinities are not symmetric")
+    return SparseAffinities(n=int(n), rows=ru, cols=cu, values=vu)
+
+
+def save_affinities(path, P, y0=None) -> None:
+    """Write P (and optionally the initial embedding Y0) as a versioned .npz."""
+    n, rowptr, col, val = to_csr(P)
+    extra = {} if y0 is None else {"y0": np.asarray(y0, dtype=np.float64)}
+    np.savez(path, format=np.array(FORMAT), version=np.array(FORMAT_VERSION, dtype=np.int64),
+             n=np.array(n, dtype=np.int64), rowptr=rowptr, col=col, val=val, **extra)
+
+
+def load_affinities(path):
+    """(SparseAffinities, Y0 or None) from a file written by save_affinities."""
+    with np.load(path, allow_pickle=False) as z:
+        if "format" not in z.files or str(z["format"]) != FORMAT:
+            raise ValueError(f"{path}: not a {FORMAT} file")
+        if int(z["version"]) != FORMAT_VERSION:
+            raise ValueError(f"{path}: format version {int(z['version'])}, expected {FORMAT_VERSION}")
+        P = from_csr(int(z["n"]), z["rowptr"], z["col"], z["val"])
+        y0 = np.array(z["y0"]) if "y0" in z.files else None
+    return P, y0
