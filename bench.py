@@ -401,10 +401,15 @@ def run_ours(args):
     for _ in range(3):
         api()
     torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    ms_e2e = timed(api, args.steps, stream)
-    wall_e2e = (time.perf_counter() - t0) / args.steps * 1e3
-    ms_e2e = max(ms_e2e, wall_e2e)
+    # each call ends with a host sync, so host jitter lands in the timing:
+    # three K-step runs, the median one is reported
+    runs = []
+    for _ in range(3):
+        t0 = time.perf_counter()
+        ms_ev = timed(api, args.steps, stream)
+        wall_e2e = (time.perf_counter() - t0) / args.steps * 1e3
+        runs.append(max(ms_ev, wall_e2e))
+    ms_e2e = sorted(runs)[1]
 
     cpu = None
     if not args.no_cpu_baseline and rank == 0:
@@ -432,6 +437,8 @@ def run_ours(args):
                      "traffic": traffic_from_profiles(traffic_key)},
         "cpu_baseline": cpu,
         "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
+                "api": "optimizer.gradient(P, Y_pinned_host, out=pinned_host) -> fitsne_gradient_host",
+                "timing": "median of 3 runs of K steps (max of CUDA-event and wall time per run)",
                 "h2d_bytes_per_step": int(y_host.numel() * y_host.element_size()),
                 "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
         "gpu_launches": launches_per_step * args.steps,

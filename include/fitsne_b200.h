@@ -91,7 +91,8 @@ enum fitsne_option {
   FITSNE_OPT_TILE_ROWS = 6,
   FITSNE_OPT_TILE_COLS = 7,
   FITSNE_OPT_TILED_CTAS = 8,
-  FITSNE_OPT_TILED_BANK_ORDER = 9
+  FITSNE_OPT_TILED_BANK_ORDER = 9,
+  FITSNE_OPT_HOST_PIECES = 10
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -99,11 +100,14 @@ enum fitsne_option {
  *   is staged in shared memory by bulk copies; 2 = tiled whenever applicable.
  *   The tiled copy is built on first use after fitsne_set_affinities.
  *   FITSNE_OPT_TILE_ROWS / FITSNE_OPT_TILE_COLS: tile shape (rows per row
- *   block, default 2048; points per column chunk, default 10240); both even and
+ *   block, default 3072; points per column chunk, default 8192); both even and
  *   <= 16384.  Shapes whose shared-memory footprint (24 rows + 16 cols + 4.3
  *   rows bytes) exceeds 226 KiB use the CSR kernel.  FITSNE_OPT_TILED_CTAS:
- *   persistent grid of the tiled kernel (default 0 = 13/16 of the SMs when the
- *   repulsion runs concurrently on the side stream, else one CTA per SM). */
+ *   persistent grid of the tiled kernel (default 0 = 7/8 of the SMs when the
+ *   repulsion runs concurrently on the side stream, else one CTA per SM).
+ *   FITSNE_OPT_HOST_PIECES: fitsne_gradient_host schedule; 0 (default) = copy
+ *   in, gradient, copy out; 1 = tiled SpMV in row pieces on a high-priority
+ *   stream with each piece's combine + copy-out overlapping later pieces. */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
  * only for its alignment): out[0..5] = {in use (0/1), tiles, slabs, slot
@@ -171,6 +175,15 @@ int fitsne_attractive(fitsne_ctx* ctx, const void* Y_full, void* out, void* stre
  * Single-GPU (registered rows must be all rows).  grad (n, s); z_host optional. */
 int fitsne_gradient(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, double* z_host,
                     void* stream);
+
+/* --- a10 with HOST buffers: the reference's gradient() call shape (numpy in,
+ * numpy out; optimizer.py:248-262).  Y_host (n, s) and grad_host (n, s) in the
+ * context dtype, pinned for full PCIe speed.  Copies Y in on `stream`, runs the
+ * gradient with the attractive SpMV split into row pieces and copies each
+ * piece of the gradient out while the later pieces still run.  Returns when
+ * grad_host is written. */
+int fitsne_gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host,
+                         void* stream);
 
 /* --- a12: _kl_given_z (optimizer.py:265-275) over the registered rows. */
 int fitsne_kl(fitsne_ctx* ctx, const void* Y_full, double z, double* kl_host, void* stream);

@@ -102,17 +102,44 @@ def as_points(x, dims=None):
 _pinned: dict = {}
 
 
-def _pinned_buffer(shape, dtype):
+def _pinned_buffer(shape, dtype, tag="in"):
     """Reusable pinned staging buffer (cudaHostAlloc is far too slow per call)."""
     n = 1
     for s in shape:
         n *= int(s)
-    key = dtype
+    key = (tag, dtype)
     buf = _pinned.get(key)
     if buf is None or buf.numel() < n:
         buf = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)
         _pinned[key] = buf
     return buf[:n].view(shape)
+
+
+def host_input(x, dtype: torch.dtype) -> torch.Tensor:
+    """Contiguous CPU tensor of ``dtype`` holding ``x`` (a host array): the
+    caller's own tensor when it already qualifies, else a pinned staging copy."""
+    if isinstance(x, torch.Tensor):
+        t = x.detach()
+        if t.dtype == dtype and t.is_contiguous():
+            return t
+        buf = _pinned_buffer(tuple(t.shape), dtype, "in")
+        buf.copy_(t)
+        return buf
+    a = np.asarray(x)
+    buf = _pinned_buffer(a.shape, dtype, "in")
+    buf.numpy()[...] = a
+    return buf
+
+
+def host_output(shape, dtype: torch.dtype, out=None) -> torch.Tensor:
+    """Where a host-bound result is written: ``out`` when it is a contiguous
+    CPU tensor of ``dtype``, else a pinned staging buffer."""
+    if out is not None:
+        if tuple(out.shape) != tuple(shape):
+            raise ValueError("out has the wrong shape")
+        if not out.is_cuda and out.dtype == dtype and out.is_contiguous():
+            return out
+    return _pinned_buffer(tuple(shape), dtype, "out")
 
 
 def output(t: torch.Tensor, device_result, like=None, out=None):

@@ -70,6 +70,7 @@ _SIGS = {
     "fitsne_set_affinities": (_int, [_vp, _vp, _vp, _vp, _i64, _i64, _i64, _i64]),
     "fitsne_attractive": (_int, [_vp, _vp, _vp, _vp]),
     "fitsne_gradient": (_int, [_vp, _vp, _dbl, _vp, C.POINTER(_dbl), _vp]),
+    "fitsne_gradient_host": (_int, [_vp, _vp, _dbl, _vp, _vp]),
     "fitsne_kl": (_int, [_vp, _vp, _dbl, C.POINTER(_dbl), _vp]),
     "fitsne_step": (_int, [_vp, _vp, _vp, _vp, _vp, _i64, _dbl, _dbl, _vp]),
     "fitsne_iterate": (_int, [_vp, _vp, _vp, _vp, _vp, _dbl, _dbl, _dbl, _vp, _vp, _vp]),

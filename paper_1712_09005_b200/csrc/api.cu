@@ -119,12 +119,19 @@ int fitsne_destroy(fitsne_ctx* c) {
   cudaSetDevice(c->device);
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&c->accum, &c->fbuf, &c->sbuf, &c->pot, &c->tw, &c->zpart, &c->bbox_part,
-                    &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf};
+                    &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf,
+                    &c->hy, &c->hg};
   for (DevBuf* b : bufs) release(*b);
   free_tiled(c);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->ev_bbox) cudaEventDestroy(c->ev_bbox);
   if (c->side) cudaStreamDestroy(c->side);
+  for (cudaEvent_t e : c->ev_piece)
+    if (e) cudaEventDestroy(e);
+  if (c->ev_out) cudaEventDestroy(c->ev_out);
+  if (c->out) cudaStreamDestroy(c->out);
+  if (c->hp) cudaStreamDestroy(c->hp);
   if (c->h_grid) cudaFreeHost(c->h_grid);
   if (c->h_scal) cudaFreeHost(c->h_scal);
   if (c->h_status) cudaFreeHost(c->h_status);
@@ -192,6 +199,11 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     const int C = option == FITSNE_OPT_TILE_COLS ? value : ctx->tile_cols;
     ctx->tile_rows = R;
     ctx->tile_cols = C;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_HOST_PIECES) {
+    if (value < 0 || value > 1) { set_error("host pieces must be 0 or 1"); return FITSNE_EINVAL; }
+    ctx->host_pieces = value;
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_TILED_BANK_ORDER) {
@@ -382,6 +394,21 @@ int fitsne_gradient(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, do
     *z_host = ctx->h_scal[0];
   }
   return FITSNE_OK;
+}
+
+int fitsne_gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host,
+                         void* stream) {
+  CTX_CHECK(ctx);
+  cudaStream_t st = S_(stream);
+  if (!ctx->rowptr) { set_error("no affinities registered"); return FITSNE_EINVAL; }
+  if (ctx->row_begin != 0 || ctx->n_rows != ctx->n_total) {
+    set_error("fitsne_gradient_host needs all rows registered (use the sharded stages)");
+    return FITSNE_EINVAL;
+  }
+  if (!Y_host || !grad_host) { set_error("null buffer"); return FITSNE_EINVAL; }
+  if (!(alpha >= 1.0)) { set_error("exaggeration alpha must be >= 1"); return FITSNE_EINVAL; }
+  if (ctx->n_total < 2) { set_error("repulsion needs at least two points"); return FITSNE_EINVAL; }
+  return gradient_host(ctx, Y_host, alpha, grad_host, st);
 }
 
 int fitsne_kl(fitsne_ctx* ctx, const void* Y_full, double z, double* kl_host, void* stream) {

@@ -641,14 +641,16 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
     FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
   } else {
-    // bbox + grid readback first (tiny), then the SpMV on st and spread + FFT
-    // on the side stream, which fill the SM slots the SpMV leaves
+    // bbox kernels first on the side stream (dispatched ahead of the SpMV, so
+    // they get the whole GPU for a few microseconds), then the SpMV on st,
+    // then -- once the 40-byte bbox readback lands -- spread + FFT on the side
+    // stream, which fill the SM slots the SpMV leaves
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
-    // the SpMV needs no grid: queue it before the bbox readback blocks the host
+    FITSNE_TRY(bbox_launch(ctx, Y, n, ctx->side));
     FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
-    FITSNE_TRY(make_grid(ctx, Y, n, ctx->side));
+    FITSNE_TRY(make_grid_finish(ctx, ctx->side));
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
@@ -659,6 +661,73 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
                                         nullptr, nullptr, clear, st);
   return launch_combine<double, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
                                        nullptr, nullptr, clear, st);
+}
+
+// Gradient with host buffers (fitsne_gradient_host).  Y is copied in on st;
+// the attractive SpMV runs as kTiledPieces launches over consecutive row
+// ranges on a high-priority stream while grid + spread + FFT run on the side stream; on the
+// copy-out stream the combine of piece k (F_rep gather + 4 (alpha F_attr -
+// F_rep)) and its device-to-host copy start as soon as SpMV piece k is done,
+// so the gradient leaves the device while the later pieces still run.
+int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host, cudaStream_t st) {
+  const int64_t n = ctx->n_total;
+  const size_t row_bytes = dsize(ctx->dtype) * (size_t)ctx->dims;
+  const size_t bytes = row_bytes * (size_t)n;
+  FITSNE_TRY(ensure(ctx->hy, bytes));
+  FITSNE_TRY(ensure(ctx->hg, bytes));
+  void* y = ctx->hy.ptr;
+  unsigned char* g = (unsigned char*)ctx->hg.ptr;
+  FITSNE_CUDA(cudaMemcpyAsync(y, Y_host, bytes, cudaMemcpyHostToDevice, st));
+  if (ctx->host_pieces == 0 || ctx->overlap == 0 || !tiled_usable(ctx, y, st)) {
+    FITSNE_TRY(gradient_overlapped(ctx, y, alpha, g, st));
+    FITSNE_CUDA(cudaMemcpyAsync(grad_host, g, bytes, cudaMemcpyDeviceToHost, st));
+    FITSNE_CUDA(cudaStreamSynchronize(st));
+    return FITSNE_OK;
+  }
+  FITSNE_TRY(side_stream(ctx));
+  if (!ctx->out) {
+    // the SpMV pieces run on a high-priority stream: when piece q drains, the
+    // block scheduler hands the freed SMs to piece q + 1 before the pending
+    // spread / FFT blocks of the side stream
+    int lo = 0, hi = 0;
+    FITSNE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FITSNE_CUDA(cudaStreamCreateWithPriority(&ctx->hp, cudaStreamNonBlocking, hi));
+    FITSNE_CUDA(cudaStreamCreateWithFlags(&ctx->out, cudaStreamNonBlocking));
+    for (cudaEvent_t& e : ctx->ev_piece) FITSNE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  }
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
+  FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
+  FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_in, 0));
+  FITSNE_CUDA(cudaStreamWaitEvent(ctx->hp, ctx->ev_in, 0));
+  void* attr = nullptr;
+  FITSNE_TRY(bbox_launch(ctx, y, n, ctx->side));
+  for (int q = 0; q < kTiledPieces; ++q) {
+    FITSNE_TRY(attract_tiled_piece(ctx, y, q, ctx->hp, &attr));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_piece[q], ctx->hp));
+  }
+  FITSNE_TRY(make_grid_finish(ctx, ctx->side));
+  FITSNE_TRY(spread_tsne(ctx, y, n, nullptr, ctx->side));
+  FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+  FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_done, 0));
+  int64_t rows[kTiledPieces + 1];
+  tiled_piece_rows(ctx, rows);
+  for (int q = 0; q < kTiledPieces; ++q) {
+    const int64_t r0 = rows[q], nr = rows[q + 1] - rows[q];
+    FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_piece[q], 0));
+    if (nr <= 0) continue;
+    const size_t off = row_bytes * (size_t)r0;
+    FITSNE_TRY((launch_combine<float, false>(ctx, (const unsigned char*)y + off, nr,
+                                             (unsigned char*)attr + off, alpha, g + off, 0, 0,
+                                             nullptr, nullptr, nullptr, nullptr, true, ctx->out)));
+    FITSNE_CUDA(cudaMemcpyAsync((unsigned char*)grad_host + off, g + off, row_bytes * (size_t)nr,
+                                cudaMemcpyDeviceToHost, ctx->out));
+  }
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_out, ctx->out));
+  FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_out, 0));
+  FITSNE_CUDA(cudaStreamSynchronize(ctx->out));
+  return FITSNE_OK;
 }
 
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
@@ -676,10 +745,11 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
     FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
-    // SpMV + KL partials on st (queued before the bbox readback blocks the
-    // host), spread + FFT on the side stream
+    // bbox on the side stream, SpMV + KL partials on st (queued before the
+    // bbox readback blocks the host), spread + FFT on the side stream
+    FITSNE_TRY(bbox_launch(ctx, Yin, n, ctx->side));
     FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
-    FITSNE_TRY(make_grid(ctx, Yin, n, ctx->side));
+    FITSNE_TRY(make_grid_finish(ctx, ctx->side));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));

@@ -136,13 +136,21 @@ struct fitsne_ctx {
   int overlap = 1;                 // 0 serial, 1 SpMV || repulsion, 2 same + priority repulsion
   int spmv_blocks_per_sm = 0;      // >0: persistent SpMV grid in the overlap modes
   int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable
-  int tile_rows = 2048, tile_cols = 10240, tiled_ctas = 0;
+  int tile_rows = 3072, tile_cols = 8192, tiled_ctas = 0;
   int tiled_bank_order = 1;        // bank-aware slot order inside slabs (tiled build)
+  int host_pieces = 0;             // fitsne_gradient_host: SpMV row pieces + overlapped copy-out
   fitsne::TiledP* tiled = nullptr; // built lazily from the registered CSR
   double* kl_part = nullptr;       // where the last SpMV left its KL partials
   int kl_nparts = 0;
   cudaStream_t side = nullptr;     // repulsion stream (overlaps the attractive SpMV)
   cudaEvent_t ev_in = nullptr, ev_done = nullptr;
+  cudaEvent_t ev_bbox = nullptr;   // bbox readback landed (bbox_launch / bbox_wait)
+  // host-buffer gradient (fitsne_gradient_host): copy-out stream, one event
+  // per SpMV row piece, device copies of Y and the gradient
+  cudaStream_t out = nullptr, hp = nullptr;
+  cudaEvent_t ev_piece[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t ev_out = nullptr;
+  fitsne::DevBuf hy, hg;
   double raw_bbox[4] = {0, 0, 0, 0};  // unpadded min/max of the last grid's points
 
   fitsne_grid* h_grid = nullptr;  // pinned mirror

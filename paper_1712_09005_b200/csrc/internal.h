@@ -11,6 +11,12 @@ int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host,
                  cudaStream_t st);
 int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st);
 int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
+// make_grid split around other launches: bbox kernels + readback queued on st
+// (bbox_launch), then the host waits for the readback only and installs the
+// grid for work queued on st (make_grid_finish)
+int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
+int bbox_wait(fitsne_ctx* ctx, double* bbox_host);
+int make_grid_finish(fitsne_ctx* ctx, cudaStream_t st);
 
 // repulsion pipeline ------------------------------------------------------------
 // spread of the t-SNE charges (1, y_0[, y_1]) into ctx->accum (or `accum`)
@@ -67,6 +73,14 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 // out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
 int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st);
 void free_tiled(fitsne_ctx* ctx);
+// The tiled SpMV as kTiledPieces launches over consecutive row ranges (each
+// over the whole persistent grid), so a consumer can start on the rows of
+// piece k while piece k + 1 runs.  Row range of piece k: [rows[k], rows[k+1]).
+constexpr int kTiledPieces = 4;
+int attract_tiled_piece(fitsne_ctx* ctx, const void* Y, int piece, cudaStream_t st, void** fattr);
+void tiled_piece_rows(const fitsne_ctx* ctx, int64_t* rows);
+// fitsne_gradient_host (attract.cu)
+int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host, cudaStream_t st);
 int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st);
 
 int read_scalars(fitsne_ctx* ctx, int count, cudaStream_t st);  // scal[0..count) -> h_scal

@@ -119,7 +119,11 @@ __global__ void k_bbox_final(const double* __restrict__ part, int nblk, const in
   }
 }
 
-int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, cudaStream_t st) {
+// Bounding box in two halves: bbox_launch queues the min/max kernels and the
+// 40-byte readback on st (and records ctx->ev_bbox); bbox_wait blocks the host
+// on that event only, so work queued on other streams in between (the
+// attractive SpMV) is dispatched behind the bbox blocks, not ahead of them.
+int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
   const int S = ctx->dims;
   int nblk = (int)std::min<int64_t>(std::max<int64_t>((n + kBlock - 1) / kBlock, 1), 4 * ctx->num_sms);
   FITSNE_TRY(ensure(ctx->bbox_part, sizeof(double) * (size_t)nblk * 2 * S + 64));
@@ -141,13 +145,34 @@ int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, c
   FITSNE_CHECK_LAUNCH();
   FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * (2 * S + 1),
                               cudaMemcpyDeviceToHost, st));
-  FITSNE_CUDA(cudaStreamSynchronize(st));
+  if (!ctx->ev_bbox) FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_bbox, cudaEventDisableTiming));
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_bbox, st));
+  return FITSNE_OK;
+}
+
+int bbox_wait(fitsne_ctx* ctx, double* bbox_host) {
+  const int S = ctx->dims;
+  FITSNE_CUDA(cudaEventSynchronize(ctx->ev_bbox));
   if (ctx->h_scal[8 + 2 * S] != 0.0) {
     set_error("points must be finite");
     return FITSNE_ENONFINITE;
   }
   for (int d = 0; d < 2 * S; ++d) bbox_host[d] = ctx->h_scal[8 + d];
   return FITSNE_OK;
+}
+
+int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, cudaStream_t st) {
+  FITSNE_TRY(bbox_launch(ctx, Y, n, st));
+  return bbox_wait(ctx, bbox_host);
+}
+
+// make_grid in two halves (see bbox_launch)
+int make_grid_finish(fitsne_ctx* ctx, cudaStream_t st) {
+  double bbox[4];
+  FITSNE_TRY(bbox_wait(ctx, bbox));
+  fitsne_grid g;
+  FITSNE_TRY(grid_from_bbox(ctx, bbox, &g));
+  return install_grid(ctx, g, st);
 }
 
 // Exact restatement of make_grid's scalar formulas (nbody.py:131-143).  Host
@@ -640,16 +665,16 @@ template <typename T>
 __global__ void __launch_bounds__(256)
 k_spec_cols(const typename C2<T>::type* __restrict__ Sbuf, GridArgs g,
             const typename C2<T>::type* __restrict__ tw, FftPlan pl,
-            typename C2<T>::type* __restrict__ Khat) {
+            typename C2<T>::type* __restrict__ Khat, int cpb) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = g.L, n = g.n, H = L / 2 + 1;
   const int PL = plen(L);
   V* s_tw = reinterpret_cast<V*>(smem_raw);
   V* a = s_tw + L;
-  V* b = a + (size_t)kSpecCols * PL;
-  const int ky0 = blockIdx.x * kSpecCols;
-  const int nc = min(kSpecCols, H - ky0);
+  V* b = a + (size_t)cpb * PL;
+  const int ky0 = blockIdx.x * cpb;  // cpb <= kSpecCols columns per block
+  const int nc = min(cpb, H - ky0);
   stage_twiddles(s_tw, tw, L);
   // each row i contributes kSpecCols consecutive spectrum columns (32 B)
   for (int x = threadIdx.x; x < L; x += blockDim.x) {
@@ -1009,9 +1034,14 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
         (int64_t)accum_elems(gr));
     FITSNE_CHECK_LAUNCH();
     if (pair0 == 0) {
-      size_t smem_s = sizeof(V) * ((size_t)L + 2 * (size_t)kSpecCols * plen(L));
+      // columns per block: as many as fit in shared memory (long transforms
+      // take fewer)
+      int cpb = kSpecCols;
+      auto smem_spec = [&](int c) { return sizeof(V) * ((size_t)L + 2 * (size_t)c * plen(L)); };
+      while (cpb > 1 && smem_spec(cpb) > 227 * 1024) cpb /= 2;
+      const size_t smem_s = smem_spec(cpb);
       FITSNE_TRY(set_smem<T>((const void*)k_spec_cols<T>, smem_s));
-      k_spec_cols<T><<<(H + kSpecCols - 1) / kSpecCols, 256, smem_s, st>>>(Sb, g, tw, pl, Kh);
+      k_spec_cols<T><<<(H + cpb - 1) / cpb, 256, smem_s, st>>>(Sb, g, tw, pl, Kh, cpb);
       FITSNE_CHECK_LAUNCH();
     }
     size_t smem_c = sizeof(V) * ((size_t)L + 2 * (size_t)npair * plen(L));

@@ -67,7 +67,8 @@ __host__ __device__ inline int64_t slot_index(int64_t g, int lane) { return g * 
 static constexpr int kTiledStages = 2;            // chunk + header ring depth
 
 struct TiledP {
-  DevBuf tiles, sched, slab_off, rows, hdr, cols, vals, fattr, part;
+  DevBuf tiles, sched, psched, slab_off, rows, hdr, cols, vals, fattr, part;
+  int64_t piece_rows[kTiledPieces + 1] = {};  // row ranges of the piece schedules
   int64_t ntiles = 0, nslabs = 0, nslots = 0, nseg = 0;
   int hdr_max = 0;  // largest header blob (bytes)
   int R = 0, C = 0, grid = 0;
@@ -102,8 +103,8 @@ static int alloc_exact(DevBuf& b, size_t bytes) {
 void free_tiled(fitsne_ctx* ctx) {
   if (!ctx->tiled) return;
   TiledP* t = ctx->tiled;
-  DevBuf* bufs[] = {&t->tiles, &t->sched, &t->slab_off, &t->rows, &t->hdr, &t->cols, &t->vals,
-                    &t->fattr, &t->part};
+  DevBuf* bufs[] = {&t->tiles, &t->sched, &t->psched, &t->slab_off, &t->rows, &t->hdr, &t->cols,
+                    &t->vals, &t->fattr, &t->part};
   for (DevBuf* b : bufs) release_buf(*b);
   delete t;
   ctx->tiled = nullptr;
@@ -354,13 +355,13 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
   for (int64_t k = lane; k < (int64_t)ns * 32; k += 32) hr[k] = rows[(int64_t)sb * 32 + k];
 }
 
-// Persistent grid: with the overlapped schedule about 1/5 of the SMs stay free
+// Persistent grid: with the overlapped schedule 1/8 of the SMs stay free
 // for the spread / FFT stages running concurrently on the side stream (the
 // tiled kernel fills an SM: 1024 threads x 64 registers, ~210 KB of shared
 // memory); serial schedules use every SM.
 static int tiled_grid(const fitsne_ctx* ctx) {
   if (ctx->tiled_ctas > 0) return ctx->tiled_ctas;
-  if (ctx->overlap != 0) return std::max(1, (ctx->num_sms * 13) / 16);
+  if (ctx->overlap != 0) return std::max(1, (ctx->num_sms * 7) / 8);
   return ctx->num_sms;
 }
 
@@ -586,22 +587,51 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     FITSNE_CUDA(cudaStreamSynchronize(st));
   }
   const int grid = tiled_grid(ctx);
-  std::vector<int32_t> sched(grid + 1, (int32_t)nt);
-  double total = 0;
-  for (double c : cost) total += c;
-  {
+  // static schedule of tiles [ta, tb) over the persistent grid: contiguous
+  // runs of the row-block-major order balanced on cost
+  auto balance = [&](int64_t ta, int64_t tb, int32_t* sched) {
+    double total = 0;
+    for (int64_t t = ta; t < tb; ++t) total += cost[t];
     double acc = 0;
     int k = 1;
-    sched[0] = 0;
-    for (int64_t t = 0; t < nt && k < grid; ++t) {
+    sched[0] = (int32_t)ta;
+    for (int64_t t = ta; t < tb && k < grid; ++t) {
       acc += cost[t];
       while (k < grid && acc >= total * k / grid) sched[k++] = (int32_t)(t + 1);
     }
-    for (; k < grid; ++k) sched[k] = (int32_t)nt;
-    sched[grid] = (int32_t)nt;
+    for (; k <= grid; ++k) sched[k] = (int32_t)tb;
+  };
+  std::vector<int32_t> sched(grid + 1), psched((size_t)kTiledPieces * (grid + 1));
+  balance(0, nt, sched.data());
+  // piece schedules: row blocks split in kTiledPieces near-equal-cost ranges
+  {
+    const int64_t nrb = (n_rows + R - 1) / R;
+    std::vector<double> rb_cost(nrb, 0.0);
+    for (int64_t t = 0; t < nt; ++t) rb_cost[t_dense[t] / nch] += cost[t];
+    double total = 0;
+    for (double c : rb_cost) total += c;
+    std::vector<int64_t> rb_cut(kTiledPieces + 1, nrb);
+    rb_cut[0] = 0;
+    double acc = 0;
+    int k = 1;
+    for (int64_t b = 0; b < nrb && k < kTiledPieces; ++b) {
+      acc += rb_cost[b];
+      while (k < kTiledPieces && acc >= total * k / kTiledPieces) rb_cut[k++] = b + 1;
+    }
+    int64_t t = 0;
+    for (int q = 0; q < kTiledPieces; ++q) {
+      const int64_t ta = t;
+      while (t < nt && t_dense[t] / nch < rb_cut[q + 1]) ++t;
+      balance(ta, t, psched.data() + (size_t)q * (grid + 1));
+      T->piece_rows[q] = std::min<int64_t>(rb_cut[q] * R, n_rows);
+    }
+    T->piece_rows[kTiledPieces] = n_rows;
   }
   FITSNE_TRY(alloc_exact(T->tiles, sizeof(TileLoad) * (size_t)std::max<int64_t>(nt, 1)));
   FITSNE_TRY(alloc_exact(T->sched, sizeof(int32_t) * (grid + 1)));
+  FITSNE_TRY(alloc_exact(T->psched, sizeof(int32_t) * psched.size()));
+  FITSNE_CUDA(cudaMemcpyAsync(T->psched.ptr, psched.data(), sizeof(int32_t) * psched.size(),
+                              cudaMemcpyHostToDevice, st));
   FITSNE_CUDA(cudaMemcpyAsync(T->tiles.ptr, tiles.data(), sizeof(TileLoad) * nt, cudaMemcpyHostToDevice, st));
   FITSNE_CUDA(cudaMemcpyAsync(T->sched.ptr, sched.data(), sizeof(int32_t) * (grid + 1),
                               cudaMemcpyHostToDevice, st));
@@ -662,8 +692,8 @@ bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
     // keep the CSR kernel for this P; release what the attempt allocated
     cudaStreamSynchronize(st);
     cudaGetLastError();
-    DevBuf* bufs[] = {&T->tiles, &T->sched, &T->slab_off, &T->rows, &T->hdr, &T->cols, &T->vals,
-                      &T->fattr, &T->part};
+    DevBuf* bufs[] = {&T->tiles, &T->sched, &T->psched, &T->slab_off, &T->rows, &T->hdr, &T->cols,
+                      &T->vals, &T->fattr, &T->part};
     for (DevBuf* b : bufs) release_buf(*b);
     T->failed = true;
     return false;
@@ -952,8 +982,8 @@ __global__ void k_tiled_finish(float2* __restrict__ fattr, int64_t n, const floa
 
 // Runs the tiled SpMV: F_attr accumulates into the tiled copy's zeroed buffer
 // (*fattr_out; the consumer must clear it), KL partials -> T->part[0, grid).
-int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** fattr_out,
-                  double** part_out, int* nparts) {
+static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched,
+                        cudaStream_t st) {
   TiledP* T = ctx->tiled;
   const size_t smem = tiled_smem(T->R, T->C, T->hdr_max);
   const int stage_sz = (int)stage_bytes(T->C, T->hdr_max);
@@ -969,7 +999,7 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
   }
   double* part = (double*)T->part.ptr;
 #define TILED_ARGS                                                                                  \
-  (const TileLoad*)T->tiles.ptr, (const int32_t*)T->sched.ptr, (const unsigned char*)T->hdr.ptr,    \
+  (const TileLoad*)T->tiles.ptr, sched, (const unsigned char*)T->hdr.ptr,    \
       (const uint16_t*)T->cols.ptr, (const float*)T->vals.ptr, (const float2*)Y, ctx->row_begin,    \
       ctx->n_rows, ctx->n_total, T->R, T->C, stage_sz, (float2*)T->fattr.ptr, part
   if (kl)
@@ -978,10 +1008,30 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
     k_attract_tiled<false><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
 #undef TILED_ARGS
   FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** fattr_out,
+                  double** part_out, int* nparts) {
+  TiledP* T = ctx->tiled;
+  double* part = (double*)T->part.ptr;
+  FITSNE_TRY(launch_tiled(ctx, Y, kl, (const int32_t*)T->sched.ptr, st));
   *fattr_out = T->fattr.ptr;
   if (part_out) *part_out = part;
   if (nparts) *nparts = T->grid;
   return FITSNE_OK;
+}
+
+int attract_tiled_piece(fitsne_ctx* ctx, const void* Y, int piece, cudaStream_t st, void** fattr_out) {
+  TiledP* T = ctx->tiled;
+  FITSNE_TRY(launch_tiled(ctx, Y, false, (const int32_t*)T->psched.ptr + (size_t)piece * (T->grid + 1),
+                          st));
+  *fattr_out = T->fattr.ptr;
+  return FITSNE_OK;
+}
+
+void tiled_piece_rows(const fitsne_ctx* ctx, int64_t* rows) {
+  for (int q = 0; q <= kTiledPieces; ++q) rows[q] = ctx->tiled->piece_rows[q];
 }
 
 int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st) {

@@ -242,6 +242,9 @@ def gradient(P, Y, alpha: float = 1.0, min_intervals: int = 20, points_per_inter
         raise ValueError("embedding shape does not match the affinities")
     n = _check_embedding(Y)
     method = _resolve_method(method, n)
+    if method == "fft" and not A.is_device_input(Y) and (out is None or not out.is_cuda):
+        return _gradient_host(P, Y, alpha, min_intervals, points_per_interval, dtype,
+                              intervals_per_integer, out)
     y, dev, dt = _embedding(Y, dtype)
     ctx, _ = _ctx_with_P(P, dev, y.shape[1], dt, points_per_interval, min_intervals,
                          intervals_per_integer)
@@ -261,6 +264,28 @@ def gradient(P, Y, alpha: float = 1.0, min_intervals: int = 20, points_per_inter
     if g is out:
         return out
     return A.output(g, A.is_device_input(Y) and out is None, like=Y, out=out)
+
+
+def _gradient_host(P, Y, alpha, min_intervals, points_per_interval, dtype, intervals_per_integer,
+                   out):
+    """Host arrays in and out (the reference's numpy convention): one
+    fitsne_gradient_host call copies Y in, computes, and copies the gradient
+    out piece by piece while the SpMV still runs."""
+    dev = A.device_of(Y)
+    dt = A.compute_dtype(Y, dtype)
+    yh = A.host_input(Y, dt)
+    ctx, _ = _ctx_with_P(P, dev, yh.shape[1], dt, points_per_interval, min_intervals,
+                         intervals_per_integer)
+    gh = A.host_output(yh.shape, dt, out)
+    _lib.check(ctx.lib.fitsne_gradient_host(ctx.h, _lib.ptr(yh), float(alpha), _lib.ptr(gh),
+                                            ctx.stream), "fitsne_gradient_host")
+    if out is not None:
+        if gh is not out:
+            out.copy_(gh)
+        return out
+    if isinstance(Y, torch.Tensor):
+        return gh.clone()
+    return gh.numpy().astype(np.float64)
 
 
 def _scratch(ctx, name, like):

@@ -283,6 +283,28 @@ class TestLargeProperties:
         assert rel_l2(rep.forces.cpu().numpy(), f) <= 1e-3
         assert abs(rep.z - z) <= 1e-4 * z
 
+    @pytest.mark.parametrize("dtype,span", [("float32", 860.0), ("float64", 428.0)])
+    def test_largest_grid(self, fs, dtype, span):
+        """The widest embedding each dtype supports (fp32: L = 5184, fp64:
+        L = 2592), where the spectrum stage takes fewer columns per block."""
+        _, _, opt, _ = fs
+        rng = np.random.default_rng(21)
+        # 40 blobs spread over [0, span]^2 (a late-iteration t-SNE layout)
+        c = rng.uniform(0, span, (40, 2))
+        c[:2] = [[0.0, 0.0], [span, span]]
+        y = c[rng.integers(0, 40, 20_000)] + 3.0 * rng.standard_normal((20_000, 2))
+        y = np.clip(y, 0.0, span).astype(np.float32 if dtype == "float32" else np.float64)
+        rep = opt.compute_repulsive(torch.from_numpy(y).cuda(), 50, 3, "fft")
+        f, z, _, _ = O.repulsion(y.astype(np.float64), 50, 3, "fft")
+        assert rel_l2(rep.forces.cpu().numpy(), f) <= TOL[dtype]
+        assert abs(rep.z - z) <= 1e-4 * z
+
+    def test_grid_too_large(self, fs):
+        _, _, opt, _ = fs
+        y = np.array([[0.0, 0.0], [2000.0, 1.0], [5.0, 7.0]])
+        with pytest.raises(ValueError, match="FFT"):
+            opt.compute_repulsive(y, 50, 3, "fft")
+
 
 # ----------------------------------------------------------------------------- errors
 class TestErrors:

@@ -136,6 +136,54 @@ def test_tiled_kl_and_gradient(cuda):
     assert rel_l2(res[2][1], want) <= 1e-3
 
 
+@pytest.mark.parametrize("pieces", [0, 1])
+@pytest.mark.parametrize("shape", [(128, 512, 5), (64, 256, 0), (2048, 4096, 2)])
+def test_gradient_host_pieces(cuda, shape, pieces):
+    """fitsne_gradient_host (pinned host Y in, host gradient out; with pieces
+    the tiled SpMV runs in row pieces with the copy-out overlapped) equals the
+    device-buffer gradient up to float atomics order (rel-L2 1e-5), and the
+    oracle to 1e-3."""
+    from paper_1712_09005_b200 import _lib
+    n = 5003
+    rr, cc, v, Y = _graph(n, 30, seed=11)
+    csr = _csr(n, rr, cc, v)
+    y32 = Y.astype(np.float32)
+    ctx = _ctx(2, *shape)
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 10, pieces), "set_option")
+    ctx.set_affinities(csr)
+    y = torch.from_numpy(y32).cuda()
+    g = torch.empty_like(y)
+    _lib.check(ctx.lib.fitsne_gradient(ctx.h, _lib.ptr(y), 4.0, _lib.ptr(g), None, ctx.stream), "grad")
+    torch.cuda.synchronize()
+    yh = torch.from_numpy(y32).pin_memory()
+    for _ in range(2):  # the accumulator is consumed and cleared piece by piece
+        gh = torch.full_like(yh, float("nan")).pin_memory()
+        _lib.check(ctx.lib.fitsne_gradient_host(ctx.h, _lib.ptr(yh), 4.0, _lib.ptr(gh), ctx.stream),
+                   "gradient_host")
+        assert np.isfinite(gh.numpy()).all()
+        assert rel_l2(gh.numpy().astype(np.float64), g.cpu().numpy().astype(np.float64)) <= 1e-5
+    want = O.grad(rr, cc, v, y32.astype(np.float64), 4.0, min_intervals=20, p=3)
+    assert rel_l2(gh.numpy().astype(np.float64), want) <= 1e-3
+
+
+def test_public_gradient_host_arrays(cuda):
+    """optimizer.gradient with numpy / CPU-tensor inputs takes the host path;
+    results match the CUDA-tensor call."""
+    from paper_1712_09005_b200 import optimizer, affinities
+    n = 40_000
+    rr, cc, v, Y = _graph(n, 60, seed=5, clustered=False)
+    P = affinities.SparseAffinities(n=n, rows=rr, cols=cc, values=v)
+    y32 = Y.astype(np.float32)
+    dev = optimizer.gradient(P, torch.from_numpy(y32).cuda(), 2.0, 50, 3, "fft").cpu().numpy()
+    host_np = optimizer.gradient(P, y32, 2.0, 50, 3, "fft", dtype="float32")
+    assert host_np.dtype == np.float64
+    assert rel_l2(host_np, dev.astype(np.float64)) <= 1e-5
+    out = torch.empty((n, 2), dtype=torch.float32).pin_memory()
+    r = optimizer.gradient(P, torch.from_numpy(y32).pin_memory(), 2.0, 50, 3, "fft", out=out)
+    assert r is out
+    assert rel_l2(out.numpy().astype(np.float64), dev.astype(np.float64)) <= 1e-5
+
+
 def test_tiled_run_tsne_matches_csr(cuda):
     """The fused iteration (SpMV + KL + update) with the tiled kernel tracks
     the CSR kernel's trajectory over the first iterations."""

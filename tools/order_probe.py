@@ -78,6 +78,28 @@ def main():
         lp = (xc.double() @ Vc[:3].T).float()
         key[m] = (cl << 40) | morton(lp, 13)
     orders["cluster_localpc3"] = torch.argsort(key)
+    # Morton order of a short t-SNE run from the PCA start (an ordering
+    # computed from P itself: the embedding places graph neighbours together)
+    for iters in (100, 300):
+        ctx = _lib.Context(0, 2, torch.float32, 3, 50, 1.0)
+        ctx.set_affinities(base)
+        y0 = Y.clone() * 0.01
+        y1 = torch.empty_like(y0)
+        vel = torch.zeros_like(y0)
+        gains = torch.ones_like(y0)
+        kd = torch.zeros(1, dtype=torch.float64, device="cuda")
+        stt = torch.zeros(1, dtype=torch.int32, device="cuda")
+        tt = time.time()
+        for it in range(iters):
+            _lib.check(ctx.lib.fitsne_iterate(ctx.h, _lib.ptr(y0), _lib.ptr(y1), _lib.ptr(vel),
+                                              _lib.ptr(gains), 12.0, 0.5, float(n) / 12.0,
+                                              _lib.ptr(kd), _lib.ptr(stt), ctx.stream), "iterate")
+            y0, y1 = y1, y0
+        torch.cuda.synchronize()
+        print(f"tsne{iters}: {time.time() - tt:.2f}s span {(y0.max(0).values - y0.min(0).values).tolist()}",
+              flush=True)
+        orders[f"morton_tsne{iters}"] = torch.argsort(morton(y0, 16))
+        del ctx
 
     ctxs = {}
     for mode in (0, 2):
