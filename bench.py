@@ -64,7 +64,7 @@ def parse():
                     help="also time the complete 1000-iteration C3 t-SNE run (run_tsne, fused "
                          "device iterations, late exaggeration 4 from 750) and report it")
     ap.add_argument("--seed", type=int, default=3)
-    ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2],
+    ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2, 3],
                     help="0 direct atomics, 1 auto (default), 2 box-sorted")
     ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2],
                     help="0 serial, 1 (default) SpMV || repulsion, 2 + priority repulsion stream")

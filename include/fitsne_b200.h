@@ -80,8 +80,11 @@ int fitsne_set_interp(fitsne_ctx* ctx, int points_per_interval, int min_interval
 
 /* Implementation switches (no reference counterpart; for A/B tests).
  *   FITSNE_OPT_SORTED_SPREAD: 0 = one atomic per point and node; 1 (default)
- *   = box-sorted segmented spread (p = 3) when the points crowd into few boxes
- *   (>= 128 points per occupied box); 2 = always box-sorted. */
+ *   = band spread for fp32 2-D p = 3 (points binned by box row, then sorted
+ *   by box per block, one reduction per node per box run), otherwise the
+ *   box-sorted segmented spread (p = 3) when the points crowd into few boxes
+ *   (>= 128 points per occupied box); 2 = always box-sorted; 3 = band spread
+ *   whenever it applies. */
 enum fitsne_option {
   FITSNE_OPT_SORTED_SPREAD = 1,
   FITSNE_OPT_OVERLAP = 2,

@@ -152,7 +152,7 @@ int fitsne_set_interp(fitsne_ctx* ctx, int p, int min_int, double ipi) {
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
   CTX_CHECK(ctx);
   if (option == FITSNE_OPT_SORTED_SPREAD) {
-    if (value < 0 || value > 2) { set_error("sorted spread mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    if (value < 0 || value > 3) { set_error("spread mode must be 0, 1, 2 or 3"); return FITSNE_EINVAL; }
     ctx->sorted_spread = value;
     return FITSNE_OK;
   }

@@ -1,0 +1,291 @@
+// Band spread: the t-SNE charge spreading (_spread, nbody.py:233-251; the
+// unit, y_0 and y_1 charges of _fft_repulsion_sums, optimizer.py:206-210) for
+// fp32 2-D embeddings with p = 3, built for running beside the attractive
+// SpMV on the few SMs it leaves free.
+//
+// A direct scatter issues 9 vector reductions per point (one per node), each
+// a separate L2 transaction: on ~20 SMs that is LSU-bound (~1 transaction per
+// clock per SM) and took ~340 us at N = 1.3M.  Here the points are first
+// binned by box row (the x cell) with a counting sort whose histograms live
+// in shared memory (<= 864 bins: one global write per bin and block), so a
+// block of the reduce pass sees a contiguous piece of one or a few box rows.
+// It counting-sorts its piece again by box inside shared memory (key = row
+// offset x n_int + y cell, native 32-bit shared atomics), and each thread then
+// walks 8 consecutive sorted points, summing the 9 x 3 node contributions of
+// a box in registers and flushing one vector reduction per node when the box
+// changes.  Crowded boxes -- the case that serialises direct atomics -- cost
+// ~1 transaction per node per 8 points.
+//
+// Cells and weights come from box_weights3_f32 exactly as in k_spread_tsne
+// (bit-exact cells); only the summation order differs.
+#include <cub/cub.cuh>
+
+#include "common.cuh"
+#include "internal.h"
+
+namespace fitsne {
+
+static constexpr int kBandBlock = 256;
+static constexpr int kBandPts = 4096;                 // points per count / scatter block
+static constexpr int kBandChunk = 2048;               // sorted points per reduce block
+static constexpr int kBandRun = kBandChunk / kBandBlock;  // sorted points per reduce thread
+static constexpr int kBandKeys = 4096;                // (box rows in a chunk) x n_int
+static constexpr int kBandMaxRows = 1024;             // n_int bound (fp32: n_int <= 864)
+static constexpr int kBandSmem = kBandChunk * 16 + kBandKeys * 4 + kBandChunk * 4;
+
+__device__ __forceinline__ int band_cell(float y, const GridArgs& g, int d, float* w) {
+  return box_weights3_f32(y, g.lo[d], g.h[d], g.lo_f[d], g.invh_f[d], g.guard[d], g.n_int, w);
+}
+
+// cell and offset u (the same arithmetic as box_weights3_f32, which derives
+// its three weights from u), so the reduce pass can keep u instead of
+// recomputing the cell
+__device__ __forceinline__ int band_cell_u(float x, const GridArgs& g, int d, float* u_out) {
+  const float t = (x - g.lo_f[d]) * g.invh_f[d];
+  const float r = t * (1.0f / 3.0f);
+  const float q = floorf(r);
+  const float fr = r - q;
+  int c;
+  float u;
+  if (fr > g.guard[d] && fr < 1.0f - g.guard[d] && t >= 0.0f) {
+    c = (int)q;
+    if (c > g.n_int - 1) c = g.n_int - 1;
+    u = t - (float)(3 * c) - 0.5f;
+  } else {
+    double wd[3];
+    c = box_weights((double)x, g.lo[d], g.h[d], g.n_int, 3, wd);
+    const double td = __ddiv_rn(__dsub_rn((double)x, g.lo[d]), g.h[d]);
+    u = (float)__dsub_rn(__dsub_rn(td, (double)(c * 3)), 0.5);
+  }
+  *u_out = u;
+  return c;
+}
+
+// box_weights3_f32's weights from u
+__device__ __forceinline__ void band_weights(float u, float* w) {
+  const float d1 = u - 1.0f, d2 = u - 2.0f;
+  w[0] = 0.5f * d1 * d2;
+  w[1] = -u * d2;
+  w[2] = 0.5f * u * d1;
+}
+
+// per-block histogram of box rows -> counts[row * nblk + block]
+__global__ void __launch_bounds__(kBandBlock)
+k_band_count(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* __restrict__ counts) {
+  __shared__ uint32_t hist[kBandMaxRows];
+  for (int r = threadIdx.x; r < g.n_int; r += kBandBlock) hist[r] = 0;
+  __syncthreads();
+  const int64_t p0 = blockIdx.x * (int64_t)kBandPts;
+  const int64_t p1 = min(n, p0 + kBandPts);
+  for (int64_t i = p0 + threadIdx.x; i < p1; i += kBandBlock) {
+    float w[3];
+    atomicAdd(&hist[band_cell(Y[i].x, g, 0, w)], 1u);
+  }
+  __syncthreads();
+  for (int r = threadIdx.x; r < g.n_int; r += kBandBlock)
+    counts[(size_t)r * gridDim.x + blockIdx.x] = hist[r];
+}
+
+// scatter the points into box-row order (offsets = exclusive scan of counts)
+__global__ void __launch_bounds__(kBandBlock)
+k_band_scatter(const float2* __restrict__ Y, int64_t n, GridArgs g,
+               const uint32_t* __restrict__ offsets, float2* __restrict__ sorted) {
+  __shared__ uint32_t base[kBandMaxRows];
+  for (int r = threadIdx.x; r < g.n_int; r += kBandBlock)
+    base[r] = offsets[(size_t)r * gridDim.x + blockIdx.x];
+  __syncthreads();
+  const int64_t p0 = blockIdx.x * (int64_t)kBandPts;
+  const int64_t p1 = min(n, p0 + kBandPts);
+  for (int64_t i = p0 + threadIdx.x; i < p1; i += kBandBlock) {
+    const float2 y = Y[i];
+    float w[3];
+    sorted[atomicAdd(&base[band_cell(y.x, g, 0, w)], 1u)] = y;
+  }
+}
+
+// 9 vector reductions of one box's (or one point's) 27 node sums
+__device__ __forceinline__ void band_flush(float* __restrict__ acc, int nn, int cx, int cy,
+                                           const float (&s)[3][3][3]) {
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const int64_t rowbase = ((int64_t)cx * 3 + a) * nn + (int64_t)cy * 3;
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+      atomicAdd(reinterpret_cast<float4*>(acc + (rowbase + b) * kNodeSlots),
+                make_float4(s[a][b][0], s[a][b][1], s[a][b][2], 0.f));
+  }
+}
+
+// reduce pass over the box-row-sorted points: in-block counting sort by box,
+// then per-thread runs of kBandRun sorted points with one flush per box
+__global__ void __launch_bounds__(kBandBlock)
+k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __restrict__ acc) {
+  // dynamic shared memory (kBandSmem bytes): hist, points, (u_x, u_y), order, keys
+  extern __shared__ __align__(16) unsigned char band_smem[];
+  float2* pts = reinterpret_cast<float2*>(band_smem);
+  float2* uvs = pts + kBandChunk;
+  uint32_t* hist = reinterpret_cast<uint32_t*>(uvs + kBandChunk);
+  uint16_t* order = reinterpret_cast<uint16_t*>(hist + kBandKeys);
+  uint16_t* keyof = order + kBandChunk;
+  __shared__ uint32_t part[kBandBlock];
+  __shared__ int s_cx0, s_direct;
+  const int tid = threadIdx.x, lane = tid & 31;
+  const int64_t c0 = blockIdx.x * (int64_t)kBandChunk;
+  const int cnt = (int)min((int64_t)kBandChunk, n - c0);
+  const int nn = g.n, ni = g.n_int;
+  if (tid == 0) {
+    float w[3];
+    const int a = band_cell(ys[c0].x, g, 0, w);
+    const int b = band_cell(ys[c0 + cnt - 1].x, g, 0, w);
+    s_cx0 = a;
+    s_direct = (b - a + 1) * ni > kBandKeys;  // piece spans too many rows: direct scatter
+  }
+  for (int k = tid; k < kBandKeys; k += kBandBlock) hist[k] = 0;
+  __syncthreads();
+  const int cx0 = s_cx0;
+  if (s_direct) {
+    for (int k = tid; k < cnt; k += kBandBlock) {
+      const float2 y = ys[c0 + k];
+      float wx[3], wy[3], s[3][3][3];
+      const int cx = band_cell(y.x, g, 0, wx), cy = band_cell(y.y, g, 1, wy);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const float w = wx[a] * wy[b];
+          s[a][b][0] = w;
+          s[a][b][1] = w * y.x;
+          s[a][b][2] = w * y.y;
+        }
+      band_flush(acc, nn, cx, cy, s);
+    }
+    return;
+  }
+  // keys + histogram (shared atomics)
+  for (int k = tid; k < cnt; k += kBandBlock) {
+    const float2 y = ys[c0 + k];
+    float2 uv;
+    const int cx = band_cell_u(y.x, g, 0, &uv.x), cy = band_cell_u(y.y, g, 1, &uv.y);
+    const int key = (cx - cx0) * ni + cy;
+    pts[k] = y;
+    uvs[k] = uv;
+    keyof[k] = (uint16_t)key;
+    atomicAdd(&hist[key], 1u);
+  }
+  __syncthreads();
+  // exclusive scan of hist: kBandKeys / kBandBlock = 16 entries per thread
+  constexpr int E = kBandKeys / kBandBlock;
+  uint32_t loc[E], run = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    loc[e] = run;
+    run += hist[tid * E + e];
+  }
+  part[tid] = run;
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t v[kBandBlock / 32], t = 0;
+#pragma unroll
+    for (int j = 0; j < kBandBlock / 32; ++j) {
+      v[j] = part[tid * (kBandBlock / 32) + j];
+      t += v[j];
+    }
+    uint32_t x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    uint32_t ex = x - t;
+#pragma unroll
+    for (int j = 0; j < kBandBlock / 32; ++j) {
+      const uint32_t vj = v[j];
+      part[tid * (kBandBlock / 32) + j] = ex;
+      ex += vj;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) hist[tid * E + e] = loc[e] + part[tid];
+  __syncthreads();
+  // scatter local indices into box order
+  for (int k = tid; k < cnt; k += kBandBlock) {
+    order[atomicAdd(&hist[keyof[k]], 1u)] = (uint16_t)k;
+  }
+  __syncthreads();
+  // runs of kBandRun sorted points per thread: register sums per box
+  const int s0 = tid * kBandRun, s1 = min(cnt, s0 + kBandRun);
+  float s[3][3][3];
+  int cur = -1, ccx = 0, ccy = 0;
+  for (int q = s0; q < s1; ++q) {
+    const int k = order[q];
+    const int key = keyof[k];
+    const float2 y = pts[k];
+    const float2 uv = uvs[k];
+    float wx[3], wy[3];
+    band_weights(uv.x, wx);
+    band_weights(uv.y, wy);
+    if (key != cur) {
+      if (cur >= 0) band_flush(acc, nn, ccx, ccy, s);
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) s[a][b][0] = s[a][b][1] = s[a][b][2] = 0.f;
+      cur = key;
+      ccx = cx0 + key / ni;
+      ccy = key - (ccx - cx0) * ni;
+    }
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const float w = wx[a] * wy[b];
+        s[a][b][0] += w;
+        s[a][b][1] += w * y.x;
+        s[a][b][2] += w * y.y;
+      }
+  }
+  if (cur >= 0) band_flush(acc, nn, ccx, ccy, s);
+}
+
+bool band_spread_applies(const fitsne_ctx* ctx, int64_t n) {
+  return ctx->dtype == FITSNE_F32 && ctx->dims == 2 && ctx->grid.points_per_interval == 3 &&
+         ctx->grid.n_intervals <= kBandMaxRows && n > 0 && n < (1LL << 31);
+}
+
+int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
+  const GridArgs g = grid_args(ctx->grid);
+  const int nblk = (int)((n + kBandPts - 1) / kBandPts);
+  const size_t ncount = (size_t)g.n_int * nblk;
+  size_t scan_bytes = 0;
+  FITSNE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr,
+                                            (uint32_t*)nullptr, (int)ncount, st));
+  // scratch: counts, offsets, cub temp, sorted points (16-byte aligned)
+  const size_t off_counts = 0;
+  const size_t off_offsets = off_counts + ((sizeof(uint32_t) * ncount + 255) & ~(size_t)255);
+  const size_t off_tmp = off_offsets + ((sizeof(uint32_t) * ncount + 255) & ~(size_t)255);
+  const size_t off_sorted = off_tmp + ((scan_bytes + 255) & ~(size_t)255);
+  FITSNE_TRY(ensure(ctx->sortbuf, off_sorted + sizeof(float2) * (size_t)n));
+  unsigned char* base = (unsigned char*)ctx->sortbuf.ptr;
+  uint32_t* counts = (uint32_t*)(base + off_counts);
+  uint32_t* offsets = (uint32_t*)(base + off_offsets);
+  float2* sorted = (float2*)(base + off_sorted);
+  k_band_count<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, counts);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_CUDA(cub::DeviceScan::ExclusiveSum(base + off_tmp, scan_bytes, counts, offsets, (int)ncount,
+                                            st));
+  k_band_scatter<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, offsets, sorted);
+  FITSNE_CHECK_LAUNCH();
+  const int nred = (int)((n + kBandChunk - 1) / kBandChunk);
+  static thread_local int configured = -1;
+  if (configured != ctx->device) {
+    FITSNE_CUDA(cudaFuncSetAttribute(k_band_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     kBandSmem));
+    configured = ctx->device;
+  }
+  k_band_reduce<<<nred, kBandBlock, kBandSmem, st>>>(sorted, n, g, (float*)accum);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+}  // namespace fitsne

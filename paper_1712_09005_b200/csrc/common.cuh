@@ -131,8 +131,9 @@ struct fitsne_ctx {
   fitsne::DevBuf part;      // per-block partial sums (double)
   fitsne::DevBuf gen;       // generic scratch
   fitsne::DevBuf sortbuf;   // box sort keys / values / histograms
-  int sorted_spread = 1;      // box-sorted spread (p = 3): 0 never, 1 when crowded, 2 always
+  int sorted_spread = 1;      // 0 direct scatter, 1 auto (band spread for fp32 2-D p = 3, else box-sorted when crowded), 2 box-sorted, 3 band
   int spread_replicas = 4;    // replicas of the internal spread accumulator (power of two)
+  int accum_live_reps = 4;    // replicas the last spread into the internal accumulator wrote
   int overlap = 1;                 // 0 serial, 1 SpMV || repulsion, 2 same + priority repulsion
   int spmv_blocks_per_sm = 0;      // >0: persistent SpMV grid in the overlap modes
   int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable

@@ -73,6 +73,9 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 // out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
 int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st);
 void free_tiled(fitsne_ctx* ctx);
+// band spread (bandspread.cu): fp32, 2-D, p = 3, n_int <= 1024
+bool band_spread_applies(const fitsne_ctx* ctx, int64_t n);
+int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
 // The tiled SpMV as kTiledPieces launches over consecutive row ranges (each
 // over the whole persistent grid), so a consumer can start on the rows of
 // piece k while piece k + 1 runs.  Row range of piece k: [rows[k], rows[k+1]).

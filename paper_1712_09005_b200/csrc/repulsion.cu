@@ -369,6 +369,13 @@ static int accum_reps(fitsne_ctx* ctx, const void* accum) {
   return (accum == nullptr || accum == ctx->accum.ptr) ? ctx->spread_replicas : 1;
 }
 
+// replicas the FFT stage must read (and clear): the spread paths that add
+// into replica 0 only leave the others at zero
+static int accum_reps_live(fitsne_ctx* ctx, const void* accum) {
+  const int r = accum_reps(ctx, accum);
+  return r > 1 ? std::min(r, ctx->accum_live_reps) : r;
+}
+
 static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
   size_t bytes = accum_elems(ctx->grid) * dsize(ctx->dtype) * (size_t)ctx->spread_replicas;
   if (ctx->accum.cap < bytes) {
@@ -403,10 +410,24 @@ int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
     }
     use_sorted = (double)n / occ >= 128.0;
   }
-  if (n > 0 && use_sorted && spread_sorted(ctx, Y, n, accum, st) == FITSNE_OK) {
+  const bool internal = accum == ctx->accum.ptr;
+  // band spread: the fp32 2-D p = 3 default (binning by box row + in-block
+  // box sort; no same-address contention, ~1 L2 transaction per node per box
+  // run instead of one per point)
+  const bool use_band = (ctx->sorted_spread == 3 || (ctx->sorted_spread == 1)) &&
+                        band_spread_applies(ctx, n);
+  if (use_band) {
+    FITSNE_TRY(spread_band(ctx, Y, n, accum, st));
+    if (internal) ctx->accum_live_reps = 1;
     ctx->accum_clean = false;
     return FITSNE_OK;
   }
+  if (n > 0 && use_sorted && spread_sorted(ctx, Y, n, accum, st) == FITSNE_OK) {
+    if (internal) ctx->accum_live_reps = 1;
+    ctx->accum_clean = false;
+    return FITSNE_OK;
+  }
+  if (internal) ctx->accum_live_reps = nrep;
   if (n > 0) {
     if (ctx->dtype == FITSNE_F32) {
       if (ctx->dims == 1) launch_spread_tsne<float, 1>((const float*)Y, n, g, (float*)accum, nrep, rstride, st);
@@ -1030,7 +1051,7 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
     size_t smem_r = sizeof(V) * ((size_t)L + 2 * (size_t)(merged ? nd + 1 : std::max(nd, 1)) * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
     k_rows_forward<T, MODE><<<merged ? n : 2 * n, 256, smem_r, st>>>(
-        accum, coeffs, ncol, pair0, npair, F, Sb, g, tw, pl, merged, accum_reps(ctx, accum),
+        accum, coeffs, ncol, pair0, npair, F, Sb, g, tw, pl, merged, accum_reps_live(ctx, accum),
         (int64_t)accum_elems(gr));
     FITSNE_CHECK_LAUNCH();
     if (pair0 == 0) {

@@ -16,12 +16,14 @@ from oracle import fitsne_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _spread(y, dtype, sorted_on, dims):
+def _spread(y, dtype, sorted_on, dims, mode=None):
     from paper_1712_09005_b200 import _lib
     dt = torch.float32 if dtype == "float32" else torch.float64
     yt = torch.from_numpy(np.ascontiguousarray(y)).to(device=0, dtype=dt)
     ctx = _lib.Context(0, dims, dt, 3, 50)
-    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, 2 if sorted_on else 0))
+    if mode is None:
+        mode = 2 if sorted_on else 0
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, mode))
     g = _lib.Grid()
     _lib.check(ctx.lib.fitsne_make_grid(ctx.h, _lib.ptr(yt), yt.shape[0], C.byref(g), ctx.stream))
     acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=dt, device=0)
@@ -77,3 +79,39 @@ def test_sorted_spread_large_grid_radix_path(cuda, dtype):
     tol = 1e-12 if dtype == "float64" else 5e-4
     for c in range(3):
         assert rel_inf(a[:, c], ref[:, c]) <= tol, c
+
+
+BAND_CASES = dict(CASES)
+BAND_CASES.update({
+    # sparse rows: sorted pieces span many box rows (direct-scatter fallback blocks)
+    "uniform_sparse": lambda rng, d: rng.uniform(-60, 60, (5_000, d)),
+    # power-law blob sizes, one blob holding most points (crowded boxes)
+    "crowded": lambda rng, d: np.concatenate([c + s * rng.standard_normal((m, d)) for c, s, m in zip(
+        rng.uniform(-80, 80, (12, d)), rng.uniform(0.05, 3, 12),
+        [300_000, 1000, 5, 1, 7000, 2, 50_000, 3, 11, 900, 1, 4000])]),
+    "odd_count": lambda rng, d: rng.normal(0, 5, (2049 * 3 + 17, d)),
+})
+
+
+@pytest.mark.parametrize("case", list(BAND_CASES))
+def test_band_spread_matches_bincount(cuda, case):
+    """Band spread (mode 3; the fp32 2-D p = 3 default): box-row counting sort
+    + in-block box sort + per-thread box runs, vs the oracle's bincount and the
+    direct scatter."""
+    rng = np.random.default_rng(17)
+    y = BAND_CASES[case](rng, 2).astype(np.float32).astype(np.float64)
+    a, g = _spread(y, "float32", False, 2, mode=3)
+    b, _ = _spread(y, "float32", False, 2, mode=0)
+    ref = _oracle(y, g, 2)
+    for c in range(3):
+        assert rel_inf(a[:, c], ref[:, c]) <= 1e-4, c
+        assert rel_inf(b[:, c], ref[:, c]) <= 1e-4, c
+
+
+def test_band_spread_is_the_fp32_default(cuda):
+    rng = np.random.default_rng(3)
+    y = BAND_CASES["blobs"](rng, 2).astype(np.float32).astype(np.float64)
+    a, g = _spread(y, "float32", False, 2, mode=1)
+    ref = _oracle(y, g, 2)
+    for c in range(3):
+        assert rel_inf(a[:, c], ref[:, c]) <= 1e-4, c

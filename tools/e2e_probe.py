@@ -55,14 +55,20 @@ def main():
         _lib.check(ctx.lib.fitsne_gradient_host(ctx.h, _lib.ptr(yh), 1.0, _lib.ptr(gh), ctx.stream), "h")
 
     from torch.profiler import ProfilerActivity, profile
-    modes = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:]] or [(1, 1)]
+    modes = [tuple(int(x) for x in a.split(",")) for a in sys.argv[1:] if "," in a] or [(1, 1)]
     runs = []
-    for sm, om in modes:
-        def setm(sm=sm, om=om):
+    for md in modes:
+        sm, om = md[0], md[1]
+        reps = md[2] if len(md) > 2 else 4
+
+        def setm(sm=sm, om=om, reps=reps):
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, sm), "opt")
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, om), "opt")
-        runs.append((f"dev spread{sm} overlap{om}", setm, dev))
-    runs.append(("host", lambda: (_lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, 1), "o"), _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, 1), "o")), host))
+            _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, reps), "opt")
+        runs.append((f"dev spread{sm} overlap{om} reps{reps}", setm, dev))
+    if "--host" in sys.argv:
+        runs.append(("host", lambda: (_lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, 1), "o"),
+                                      _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, 1), "o")), host))
     for name, setm, fn in runs:
         setm()
         print(f"{name}: {wall(fn):.3f} ms")
@@ -81,6 +87,8 @@ def main():
 
     def pieces(v):
         return lambda: _lib.check(ctx.lib.fitsne_set_option(ctx.h, 10, v), "o")
+    if "--host" not in sys.argv:
+        return
     for name, fn in (("device", dev), ("h2d", h2d), ("d2h", d2h), ("seq", seq), ("host", host),
                      ("api", api), ("pieces1", pieces(1)), ("host", host), ("pieces0", pieces(0)),
                      ("host", host), ("device", dev), ("api", api)):
