@@ -187,7 +187,7 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
         T phi[4];
         point_gather<T, S, P>(ym, g, pot, phi);
 #pragma unroll
-        for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d);
+        for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d, g);
       }
 #pragma unroll
       for (int d = 0; d < S; ++d) {
@@ -459,7 +459,7 @@ k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
       T phi[4];
       point_gather<T, S, P>(ym, gr, pot, phi);
 #pragma unroll
-      for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d);
+      for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d, gr);
     }
     const int mcount = (n - t * 32 < 32) ? (int)(n - t * 32) : 32;
     for (int m = 0; m < mcount; ++m) {
@@ -556,7 +556,7 @@ k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ 
 #pragma unroll
     for (int d = 0; d < S; ++d) {
       const int64_t o = i * S + d;
-      const T gd = (T)4 * (alpha * at[d] - frep_from_phi<T, S>(yi, phi, Z, d));
+      const T gd = (T)4 * (alpha * at[d] - frep_from_phi<T, S>(yi, phi, Z, d, g));
       if (!STEP) {
         grad[o] = gd;
       } else {

@@ -154,8 +154,8 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
         for (int b = 0; b < 3; ++b) {
           const float w = wx[a] * wy[b];
           s[a][b][0] = w;
-          s[a][b][1] = w * y.x;
-          s[a][b][2] = w * y.y;
+          s[a][b][1] = w * (y.x - g.cf[0]);
+          s[a][b][2] = w * (y.y - g.cf[1]);
         }
       band_flush(acc, nn, cx, cy, s);
     }
@@ -241,8 +241,8 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
       for (int b = 0; b < 3; ++b) {
         const float w = wx[a] * wy[b];
         s[a][b][0] += w;
-        s[a][b][1] += w * y.x;
-        s[a][b][2] += w * y.y;
+        s[a][b][1] += w * (y.x - g.cf[0]);
+        s[a][b][2] += w * (y.y - g.cf[1]);
       }
   }
   if (cur >= 0) band_flush(acc, nn, ccx, ccy, s);

@@ -50,6 +50,11 @@ struct GridArgs {
   float lo_f[2];    // fp32 copies for the guarded fp32 box estimate
   float invh_f[2];
   float guard[2];   // margin in units of t/p (>= 0.5 disables the fast path)
+  // centre of the grid: the t-SNE y charges are spread as (y - c) so fp32
+  // potentials do not carry |y| ~ span (the repulsion is translation
+  // invariant; F = (y_i - c) K2*1 - K2*(y - c) = y_i K2*1 - K2*y)
+  double c[2];
+  float cf[2];
   int dims;
   int n_int;
   int p;
@@ -74,6 +79,8 @@ inline GridArgs grid_args(const fitsne_grid& g) {
                     : 1.0;
     double gd = 4.0 * et / (g.points_per_interval > 0 ? g.points_per_interval : 3) + 1e-3;
     a.guard[d] = gd > 0.5 ? 0.5f : (float)gd;
+    a.c[d] = 0.5 * (g.lo[d] + g.hi[d]);
+    a.cf[d] = (float)a.c[d];
   }
   a.dims = g.dims;
   a.n_int = g.n_intervals;
@@ -299,6 +306,13 @@ __device__ __forceinline__ int box_weights3_f32(float x, double lo, double h, fl
   w[1] = -u * d2;
   w[2] = 0.5f * u * d1;
   return c;
+}
+
+// grid centre in the working precision (float: cf, double: c)
+template <typename W>
+__device__ __forceinline__ W gcentre(const GridArgs& g, int d) {
+  if constexpr (sizeof(W) == 4) return g.cf[d];
+  else return g.c[d];
 }
 
 // block-wide reductions ------------------------------------------------------

@@ -153,11 +153,15 @@ __device__ __forceinline__ void point_gather(const T (&yi)[S], const GridArgs& g
   }
 }
 
-// F_rep_i = (y_i (phi_0 - 1) - (phi_{1+d} - y_d)) / Z  (optimizer.py:206-210, 244)
+// F_rep_i = (y_i (phi_0 - 1) - (phi_{1+d} - y_d)) / Z  (optimizer.py:206-210, 244),
+// with the y charges spread centred (phi_{1+d} = K2 * (y_d - c_d)): the same
+// value, y_i K2*1 - K2*y, without the fp32 cancellation of two |y|-sized terms
 template <typename T, int S>
-__device__ __forceinline__ T frep_from_phi(const T (&yi)[S], const T (&phi)[4], T Z, int d) {
+__device__ __forceinline__ T frep_from_phi(const T (&yi)[S], const T (&phi)[4], T Z, int d,
+                                           const GridArgs& g) {
   const T h4 = phi[0] - (T)1;
-  return (yi[d] * h4 - (phi[1 + d] - yi[d])) / Z;
+  const T yc = yi[d] - gcentre<T>(g, d);
+  return (yc * h4 - (phi[1 + d] - yc)) / Z;
 }
 
 }  // namespace fitsne

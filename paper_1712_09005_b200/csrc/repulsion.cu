@@ -302,6 +302,7 @@ __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T*
     const int cy = box_weights3_f32(yy.y, g.lo[1], g.h[1], g.lo_f[1], g.invh_f[1], g.guard[1],
                                     g.n_int, wy);
     const int64_t nn = g.n;
+    const float cyx = yy.x - g.cf[0], cyy = yy.y - g.cf[1];  // centred charges
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int64_t rowbase = ((int64_t)cx * 3 + a) * nn + (int64_t)cy * 3;
@@ -309,7 +310,7 @@ __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T*
       for (int b = 0; b < 3; ++b) {
         const float w = wx[a] * wy[b];
         atomicAdd(reinterpret_cast<float4*>(acc + (rowbase + b) * kNodeSlots),
-                  make_float4(w, w * yy.x, w * yy.y, 0.f));
+                  make_float4(w, w * cyx, w * cyy, 0.f));
       }
     }
     return;
@@ -324,10 +325,10 @@ __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T*
       double w = pi.w[0][a];
       T* dst = acc + node * kNodeSlots;
       if constexpr (sizeof(T) == 4) {
-        atomicAdd(reinterpret_cast<float2*>(dst), make_float2((float)w, (float)(w * y[0])));
+        atomicAdd(reinterpret_cast<float2*>(dst), make_float2((float)w, (float)(w * (y[0] - g.c[0]))));
       } else {
         atomicAdd((double*)dst, w);
-        atomicAdd((double*)dst + 1, w * y[0]);
+        atomicAdd((double*)dst + 1, w * (y[0] - g.c[0]));
       }
     }
   } else {
@@ -339,11 +340,11 @@ __global__ void k_spread_tsne(const T* __restrict__ Y, int64_t n, GridArgs g, T*
         T* dst = acc + (rowbase + b) * kNodeSlots;
         if constexpr (sizeof(T) == 4) {
           atomicAdd(reinterpret_cast<float4*>(dst),
-                    make_float4((float)w, (float)(w * y[0]), (float)(w * y[1]), 0.f));
+                    make_float4((float)w, (float)(w * (y[0] - g.c[0])), (float)(w * (y[1] - g.c[1])), 0.f));
         } else {
           atomicAdd((double*)dst, w);
-          atomicAdd((double*)dst + 1, w * y[0]);
-          atomicAdd((double*)dst + 2, w * y[1]);
+          atomicAdd((double*)dst + 1, w * (y[0] - g.c[0]));
+          atomicAdd((double*)dst + 2, w * (y[1] - g.c[1]));
         }
       }
     }
@@ -1151,10 +1152,12 @@ __global__ void k_gather_tsne(const T* __restrict__ Y, int64_t n, GridArgs g,
   T h4 = phi[0] - (T)1;
 #pragma unroll
   for (int d = 0; d < S; ++d) {
-    T yc = (T)y[d];
-    T hc = phi[1 + d] - yc;
+    // phi[1 + d] = K2 * (y_d - c_d) (centred charges)
+    const T yc = (T)(y[d] - g.c[d]);
+    const T hc = phi[1 + d] - yc;
     forces[i * S + d] = (yc * h4 - hc) / Z;
-    if (k2out) k2out[i * (S + 1) + d] = hc;
+    // the reference's k2[:, d] = K2 * y_d - y_d
+    if (k2out) k2out[i * (S + 1) + d] = (T)((double)phi[1 + d] + g.c[d] * (double)phi[0] - y[d]);
   }
   if (k2out) k2out[i * (S + 1) + S] = h4;
   if (k1out) k1out[i] = phi[3] - (T)1;

@@ -272,8 +272,8 @@ k_spread_sorted(const T* __restrict__ Y, const uint32_t* __restrict__ keys,
           const W w = wx[a] * wy[b];
           const int m = (S == 2) ? a * 3 + b : a;
           v[m * (NV / NN) + 0] = (T)w;
-          v[m * (NV / NN) + 1] = (T)(w * (W)y[0]);
-          if (S == 2) v[m * (NV / NN) + 2] = (T)(w * (W)y[S - 1]);
+          v[m * (NV / NN) + 1] = (T)(w * ((W)y[0] - gcentre<W>(g, 0)));
+          if (S == 2) v[m * (NV / NN) + 2] = (T)(w * ((W)y[S - 1] - gcentre<W>(g, S - 1)));
         }
     }
     // carry from the previous step joins lane 0's segment if the key continues
@@ -493,8 +493,8 @@ k_box_reduce(const T* __restrict__ ysorted, const uint32_t* __restrict__ offsets
         const int m = (S == 2) ? a * 3 + bb : a;
         const W w = wx[a] * wy[bb];
         v[m][0] += w;
-        v[m][1] += w * (W)y[0];
-        if (S == 2) v[m][2] += w * (W)y[S - 1];
+        v[m][1] += w * ((W)y[0] - gcentre<W>(g, 0));
+        if (S == 2) v[m][2] += w * ((W)y[S - 1] - gcentre<W>(g, S - 1));
       }
   }
 #pragma unroll

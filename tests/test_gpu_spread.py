@@ -29,7 +29,15 @@ def _spread(y, dtype, sorted_on, dims, mode=None):
     acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=dt, device=0)
     _lib.check(ctx.lib.fitsne_spread_tsne(ctx.h, _lib.ptr(yt), yt.shape[0], _lib.ptr(acc), ctx.stream))
     torch.cuda.synchronize()
-    return acc.reshape(-1, 4).cpu().numpy().astype(np.float64), g
+    a = acc.reshape(-1, 4).cpu().numpy().astype(np.float64)
+    # the y channels are spread centred on the grid (y - c, c = (lo + hi) / 2
+    # in the working precision): add c * (unit channel) back for the
+    # reference's bincount layout
+    for d in range(dims):
+        c = 0.5 * (g.lo[d] + g.hi[d])
+        c = float(np.float32(c)) if dtype == "float32" else c
+        a[:, 1 + d] += c * a[:, 0]
+    return a, g
 
 
 def _oracle(y, g, dims):
