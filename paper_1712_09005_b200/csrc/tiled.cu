@@ -66,6 +66,14 @@ static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot 
 __host__ __device__ inline int64_t slot_index(int64_t g, int lane) { return g * 32 + lane; }
 static constexpr int kTiledStages = 2;            // chunk + header ring depth
 
+// First group of consumer warp w's run in a tile of ng groups: equal shares
+// (group granularity: all consumers meet at every tile, so the longest run
+// sets the pace).  32-bit unsigned arithmetic (a tile holds < 2^32 / 32
+// groups; a 64-bit division was ~90 instructions per warp and tile).
+__host__ __device__ inline int tiled_run_lo(int ng, int w) {
+  return (int)(((uint32_t)ng * (uint32_t)w) / (uint32_t)kTiledConsumers);
+}
+
 struct TiledP {
   DevBuf tiles, sched, psched, slab_off, rows, hdr, cols, vals, fattr, part;
   int64_t piece_rows[kTiledPieces + 1] = {};  // row ranges of the piece schedules
@@ -343,7 +351,7 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
   {
     // consumer warp `lane` starts at group ng * lane / kTiledConsumers: the
     // last slab whose offset is <= that group
-    const uint32_t lo = (uint32_t)(((uint64_t)ng * (uint32_t)lane) / kTiledConsumers);
+    const uint32_t lo = (uint32_t)tiled_run_lo((int)ng, lane);  // as the kernel
     int a = 0, z = ns;
     while (z - a > 1) {
       const int m = (a + z) >> 1;
@@ -875,8 +883,8 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       consumer_sync();
     }
     float2* accp = acc + (size_t)(it & 1) * R;
-    const int lo = (int)(((int64_t)ng * warp) / kTiledConsumers);
-    const int hi = (int)(((int64_t)ng * (warp + 1)) / kTiledConsumers);
+    const int lo = tiled_run_lo(ng, warp);
+    const int hi = tiled_run_lo(ng, warp + 1);
     if (lo < hi) {
       int s = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
       int s_end = (int)goff[s + 1];
