@@ -95,7 +95,8 @@ enum fitsne_option {
   FITSNE_OPT_TILE_COLS = 7,
   FITSNE_OPT_TILED_CTAS = 8,
   FITSNE_OPT_TILED_BANK_ORDER = 9,
-  FITSNE_OPT_HOST_PIECES = 10
+  FITSNE_OPT_HOST_PIECES = 10,
+  FITSNE_OPT_FFT_COLS = 11
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -110,7 +111,9 @@ enum fitsne_option {
  *   repulsion runs concurrently on the side stream, else one CTA per SM).
  *   FITSNE_OPT_HOST_PIECES: fitsne_gradient_host schedule; 0 (default) = copy
  *   in, gradient, copy out; 1 = tiled SpMV in row pieces on a high-priority
- *   stream with each piece's combine + copy-out overlapping later pieces. */
+ *   stream with each piece's combine + copy-out overlapping later pieces.
+ *   FITSNE_OPT_FFT_COLS: adjacent columns per block of the column FFT stage
+ *   (1, 2 = default, 4; fewer when shared memory does not fit). */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
  * only for its alignment): out[0..5] = {in use (0/1), tiles, slabs, slot

@@ -201,6 +201,11 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     ctx->tile_cols = C;
     return FITSNE_OK;
   }
+  if (option == FITSNE_OPT_FFT_COLS) {
+    if (value != 1 && value != 2 && value != 4) { set_error("FFT columns per block must be 1, 2 or 4"); return FITSNE_EINVAL; }
+    ctx->cols_per_block = value;
+    return FITSNE_OK;
+  }
   if (option == FITSNE_OPT_HOST_PIECES) {
     if (value < 0 || value > 1) { set_error("host pieces must be 0 or 1"); return FITSNE_EINVAL; }
     ctx->host_pieces = value;

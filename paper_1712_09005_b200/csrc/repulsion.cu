@@ -725,71 +725,80 @@ k_spec_cols(const typename C2<T>::type* __restrict__ Sbuf, GridArgs g,
 // Data column stage: one block per column c in [0, L): forward FFT of the
 // pairs, multiply by the kernel spectrum of column min(c, L-c) (+ Parseval
 // partial of the unit-charge pair for t-SNE), inverse FFT.
+constexpr int kColsMax = 4;  // columns per k_cols block (upper bound)
+
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restrict__ Khat,
        GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int kern,
-       int with_k1, double* __restrict__ zpart) {
+       int with_k1, double* __restrict__ zpart, int cpb) {
+  // cpb (<= kColsMax) adjacent columns per block: the strided column reads
+  // then use whole 32-byte sectors instead of 8 bytes of each
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int L = g.L, n = g.n;
   const int PL = plen(L);
+  const int col0 = blockIdx.x * cpb;
+  const int nc = min(cpb, L - col0);
+  const int nsig = nc * npair;  // signal c * npair + q: column col0 + c, pair q
   V* s_tw = reinterpret_cast<V*>(smem_raw);
   V* a = s_tw + L;
-  V* b = a + (size_t)npair * PL;
-  const int col = blockIdx.x;
-  const V* Kc = Khat + (size_t)(col <= L - col ? col : L - col) * L;
+  V* b = a + (size_t)cpb * npair * PL;
   stage_twiddles(s_tw, tw, L);
-  // strided column loads: 4 in flight per thread
   for (int q = 0; q < npair; ++q)
-    for (int x0 = threadIdx.x; x0 < L; x0 += 4 * blockDim.x) {
-      V z[4];
+    for (int x0 = threadIdx.x; x0 < L; x0 += 2 * blockDim.x) {
+      V z[2][kColsMax];
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 2; ++u) {
         const int x = x0 + u * blockDim.x;
-        z[u].x = 0; z[u].y = 0;
-        if (x < n) z[u] = F[((size_t)q * n + x) * L + col];
+#pragma unroll
+        for (int c = 0; c < kColsMax; ++c) {
+          z[u][c].x = 0;
+          z[u][c].y = 0;
+          if (x < n && c < nc) z[u][c] = F[((size_t)q * n + x) * L + col0 + c];
+        }
       }
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
+      for (int u = 0; u < 2; ++u) {
         const int x = x0 + u * blockDim.x;
-        if (x < L) a[(size_t)q * PL + pidx(x)] = z[u];
+        if (x >= L) continue;
+#pragma unroll
+        for (int c = 0; c < kColsMax; ++c)
+          if (c < nc) a[(size_t)(c * npair + q) * PL + pidx(x)] = z[u][c];
       }
     }
-  V* fr = block_fft<V, T>(a, b, pl, npair, PL, s_tw, false);
+  V* fr = block_fft<V, T>(a, b, pl, nsig, PL, s_tw, false);
   V* other = (fr == a) ? b : a;
-  double zacc = 0.0;
-  for (int k0 = threadIdx.x; k0 < L; k0 += 2 * blockDim.x) {
-    V kk[2];
+  double zacc[kColsMax];
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int k = k0 + u * blockDim.x;
-      if (k < L) kk[u] = __ldg(Kc + k);
-    }
+  for (int c = 0; c < kColsMax; ++c) zacc[c] = 0.0;
 #pragma unroll
-    for (int u = 0; u < 2; ++u) {
-      const int k = k0 + u * blockDim.x;
-      if (k >= L) continue;
+  for (int c = 0; c < kColsMax; ++c) {
+    if (c >= nc) continue;
+    const int col = col0 + c;
+    const V* Kc = Khat + (size_t)(col <= L - col ? col : L - col) * L;
+    for (int k = threadIdx.x; k < L; k += blockDim.x) {
+      const V kk = __ldg(Kc + k);
       for (int q = 0; q < npair; ++q) {
-        V* p = fr + (size_t)q * PL + pidx(k);
+        V* p = fr + (size_t)(c * npair + q) * PL + pidx(k);
         const V v = *p;
         V o;
         if (MODE == MODE_TSNE) {
           if (q == 0) {
-            o.x = v.x * kk[u].y;
-            o.y = v.y * kk[u].y;
+            o.x = v.x * kk.y;
+            o.y = v.y * kk.y;
           } else {
-            zacc += (double)kk[u].x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
+            zacc[c] += (double)kk.x * ((double)v.x * (double)v.x + (double)v.y * (double)v.y);
             if (with_k1) {  // v * (K2 + i K1)
-              o.x = v.x * kk[u].y - v.y * kk[u].x;
-              o.y = v.x * kk[u].x + v.y * kk[u].y;
+              o.x = v.x * kk.y - v.y * kk.x;
+              o.y = v.x * kk.x + v.y * kk.y;
             } else {
-              o.x = v.x * kk[u].y;
-              o.y = v.y * kk[u].y;
+              o.x = v.x * kk.y;
+              o.y = v.y * kk.y;
             }
           }
         } else {
-          const T m = (kern == FITSNE_CAUCHY) ? kk[u].x : kk[u].y;
+          const T m = (kern == FITSNE_CAUCHY) ? kk.x : kk.y;
           o.x = v.x * m;
           o.y = v.y * m;
         }
@@ -797,19 +806,24 @@ k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restr
       }
     }
   }
-  V* ir = block_fft<V, T>(fr, other, pl, npair, PL, s_tw, true);
+  V* ir = block_fft<V, T>(fr, other, pl, nsig, PL, s_tw, true);
   for (int q = 0; q < npair; ++q)
     for (int x = threadIdx.x; x < n; x += blockDim.x)
-      F[((size_t)q * n + x) * L + col] = ir[(size_t)q * PL + pidx(x)];
+#pragma unroll
+      for (int c = 0; c < kColsMax; ++c)
+        if (c < nc) F[((size_t)q * n + x) * L + col0 + c] = ir[(size_t)(c * npair + q) * PL + pidx(x)];
   if (MODE == MODE_TSNE) {
-    __shared__ double red[32];
-    zacc = warp_sum(zacc);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = zacc;
+    __shared__ double red[kColsMax][32];
+#pragma unroll
+    for (int c = 0; c < kColsMax; ++c) {
+      const double zs = warp_sum(zacc[c]);
+      if ((threadIdx.x & 31) == 0) red[c][threadIdx.x >> 5] = zs;
+    }
     __syncthreads();
-    if (threadIdx.x == 0) {
+    if (threadIdx.x < nc) {
       double s = 0;
-      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += red[w];
-      zpart[col] = s;
+      for (int w = 0; w < (int)(blockDim.x + 31) / 32; ++w) s += red[threadIdx.x][w];
+      zpart[col0 + threadIdx.x] = s;
     }
   }
 }
@@ -1066,9 +1080,15 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
       k_spec_cols<T><<<(H + cpb - 1) / cpb, 256, smem_s, st>>>(Sb, g, tw, pl, Kh, cpb);
       FITSNE_CHECK_LAUNCH();
     }
-    size_t smem_c = sizeof(V) * ((size_t)L + 2 * (size_t)npair * plen(L));
+    // adjacent columns per block: as many as fit (up to kColsMax, 2 for the
+    // t-SNE pair of signals keeps two blocks per SM at L ~ 1300)
+    auto smem_cols = [&](int c) { return sizeof(V) * ((size_t)L + 2 * (size_t)c * npair * plen(L)); };
+    int ccols = std::min(kColsMax, ctx->cols_per_block);
+    while (ccols > 1 && smem_cols(ccols) > 227 * 1024) ccols /= 2;
+    const size_t smem_c = smem_cols(ccols);
     FITSNE_TRY(set_smem<T>((const void*)k_cols<T, MODE>, smem_c));
-    k_cols<T, MODE><<<L, 256, smem_c, st>>>(F, Kh, g, tw, pl, npair, kern, with_k1 ? 1 : 0, zp);
+    k_cols<T, MODE><<<(L + ccols - 1) / ccols, 256, smem_c, st>>>(F, Kh, g, tw, pl, npair, kern,
+                                                                  with_k1 ? 1 : 0, zp, ccols);
     FITSNE_CHECK_LAUNCH();
     size_t smem_i = sizeof(V) * ((size_t)L + 2 * (size_t)npair * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_rows_inverse<T, MODE>, smem_i));

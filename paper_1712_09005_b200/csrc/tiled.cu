@@ -460,6 +460,15 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
   FITSNE_CUDA(cudaMemcpyAsync(&nseg, segstart + n_rows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
   FITSNE_CUDA(cudaStreamSynchronize(st));
   if (nseg <= 0) { set_error("empty P"); return FITSNE_EINVAL; }
+  // A graph without index locality (e.g. random kNN partners) leaves ~1
+  // entry per (row, chunk) segment: every tile would stage a whole Y chunk
+  // for a few hundred entries.  The row-per-warp CSR kernel is the right one
+  // there; keep the tiled layout for >= 2 entries per segment on average
+  // (C3's clustered kNN graph: 5.4).
+  if (ctx->tiled_spmv == 1 && nnz < 2 * nseg) {
+    set_error("P has no column locality for the tiled layout");
+    return FITSNE_EINVAL;
+  }
 
   int64_t* seg_begin;
   int32_t *seg_row, *seg_cnt;

@@ -123,3 +123,30 @@ def test_band_spread_is_the_fp32_default(cuda):
     ref = _oracle(y, g, 2)
     for c in range(3):
         assert rel_inf(a[:, c], ref[:, c]) <= 1e-4, c
+
+
+@pytest.mark.parametrize("dtype", ["float64", "float32"])
+@pytest.mark.parametrize("cols", [1, 2, 4])
+def test_fft_columns_per_block(cuda, dtype, cols):
+    """k_cols with 1, 2 or 4 adjacent columns per block (FITSNE_OPT_FFT_COLS)
+    gives the reference's repulsion (forces and Z) on grids of odd and even
+    FFT length."""
+    from paper_1712_09005_b200 import _lib
+    dt = torch.float32 if dtype == "float32" else torch.float64
+    rng = np.random.default_rng(cols)
+    for span in (37.0, 91.5):
+        y = rng.uniform(-span / 2, span / 2, (6000, 2))
+        y = y.astype(np.float32).astype(np.float64) if dtype == "float32" else y
+        yt = torch.from_numpy(y).to(device=0, dtype=dt)
+        ctx = _lib.Context(0, 2, dt, 3, 20)
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, 11, cols))
+        f = torch.empty_like(yt)
+        z = C.c_double()
+        _lib.check(ctx.lib.fitsne_repulsive(ctx.h, _lib.ptr(yt), yt.shape[0], _lib.ptr(f), C.byref(z),
+                                            None, None, ctx.stream))
+        torch.cuda.synchronize()
+        fo, zo, _, _ = O.repulsion(y, 20, 3, "fft")
+        tol = 1e-10 if dtype == "float64" else 1e-3
+        got = f.cpu().numpy().astype(np.float64)
+        assert np.linalg.norm(got - fo) <= tol * np.linalg.norm(fo)
+        assert abs(z.value - zo) <= 1e-6 * zo

@@ -11,6 +11,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--case", default="c4")
 ap.add_argument("--n", type=int, default=None)
 ap.add_argument("--reps", type=int, default=10)
+ap.add_argument("--tiled", type=int, default=1, help="FITSNE_OPT_TILED_SPMV (0 CSR, 1 auto, 2 force)")
 a = ap.parse_args()
 dev = 0
 if a.case == "c4":
@@ -34,6 +35,7 @@ torch.cuda.synchronize()
 print(f"{a.case}: N={n} nnz={csr.col.numel()} setup {time.time()-t0:.1f}s")
 yt = torch.from_numpy(y).to(device=dev, dtype=torch.float32)
 ctx = _lib.Context(dev, s, torch.float32, 3, 50)
+_lib.check(ctx.lib.fitsne_set_option(ctx.h, 5, a.tiled))
 ctx.set_affinities(csr)
 g = torch.empty_like(yt)
 def step():
