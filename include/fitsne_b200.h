@@ -113,7 +113,7 @@ enum fitsne_option {
  *   in, gradient, copy out; 1 = tiled SpMV in row pieces on a high-priority
  *   stream with each piece's combine + copy-out overlapping later pieces.
  *   FITSNE_OPT_FFT_COLS: adjacent columns per block of the column FFT stage
- *   (1, 2 = default, 4; fewer when shared memory does not fit). */
+ *   (1 = default, 2, 4; fewer when shared memory does not fit). */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
  * only for its alignment): out[0..5] = {in use (0/1), tiles, slabs, slot

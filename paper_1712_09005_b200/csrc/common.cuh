@@ -146,7 +146,7 @@ struct fitsne_ctx {
   int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable
   int tile_rows = 3072, tile_cols = 8192, tiled_ctas = 0;
   int tiled_bank_order = 1;        // bank-aware slot order inside slabs (tiled build)
-  int cols_per_block = 2;          // adjacent FFT columns per k_cols block (1, 2 or 4)
+  int cols_per_block = 1;          // adjacent FFT columns per k_cols block (1, 2 or 4)
   int host_pieces = 0;             // fitsne_gradient_host: SpMV row pieces + overlapped copy-out
   fitsne::TiledP* tiled = nullptr; // built lazily from the registered CSR
   double* kl_part = nullptr;       // where the last SpMV left its KL partials

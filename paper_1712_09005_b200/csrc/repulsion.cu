@@ -1080,8 +1080,9 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
       k_spec_cols<T><<<(H + cpb - 1) / cpb, 256, smem_s, st>>>(Sb, g, tw, pl, Kh, cpb);
       FITSNE_CHECK_LAUNCH();
     }
-    // adjacent columns per block: as many as fit (up to kColsMax, 2 for the
-    // t-SNE pair of signals keeps two blocks per SM at L ~ 1300)
+    // adjacent columns per block (FITSNE_OPT_FFT_COLS; 1 measured fastest at
+    // C3 beside the SpMV: 2 and 4 use whole sectors of the strided column
+    // reads but fewer blocks fit per SM)
     auto smem_cols = [&](int c) { return sizeof(V) * ((size_t)L + 2 * (size_t)c * npair * plen(L)); };
     int ccols = std::min(kColsMax, ctx->cols_per_block);
     while (ccols > 1 && smem_cols(ccols) > 227 * 1024) ccols /= 2;

@@ -60,12 +60,14 @@ def main():
     for md in modes:
         sm, om = md[0], md[1]
         reps = md[2] if len(md) > 2 else 4
+        cols = md[3] if len(md) > 3 else 2
 
-        def setm(sm=sm, om=om, reps=reps):
+        def setm(sm=sm, om=om, reps=reps, cols=cols):
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, sm), "opt")
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, om), "opt")
             _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, reps), "opt")
-        runs.append((f"dev spread{sm} overlap{om} reps{reps}", setm, dev))
+            _lib.check(ctx.lib.fitsne_set_option(ctx.h, 11, cols), "opt")
+        runs.append((f"dev spread{sm} overlap{om} reps{reps} cols{cols}", setm, dev))
     if "--host" in sys.argv:
         runs.append(("host", lambda: (_lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, 1), "o"),
                                       _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, 1), "o")), host))
