@@ -58,7 +58,10 @@ __host__ __device__ inline int hdr_bytes_for(int nslab) {
 
 static constexpr int kTiledThreads = 1024;  // 31 consumer warps + 1 producer warp
 static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
-static constexpr int kTiledU = 4;                 // groups per lane per pipeline step
+#ifndef FITSNE_TILED_U
+#define FITSNE_TILED_U 4
+#endif
+static constexpr int kTiledU = FITSNE_TILED_U;    // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
 
 // Slot layout: group-major, lane-minor (a warp reads one group's columns and
