@@ -15,7 +15,7 @@ from paper_1712_09005_b200 import optimizer  # noqa: E402
 def run(P, n_iter):
     cfg = optimizer.TsneConfig(
         dims=2, n_iter=n_iter, learning_rate=200.0, min_intervals=50, points_per_interval=3,
-        exaggeration=optimizer.ExaggerationSchedule(12.0, 250, 4.0, 750), seed=0, pca_dims=None,
+        exaggeration=optimizer.ExaggerationSchedule(12.0, 250, 4.0, 750 if n_iter >= 750 else n_iter), seed=0, pca_dims=None,
         repulsion_method="fft", dtype="float32", device=0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
