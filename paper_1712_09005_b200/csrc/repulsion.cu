@@ -39,7 +39,7 @@ static inline int grid_for(int64_t n, int block = kBlock) {
 // =============================================================================
 template <typename T, int S>
 __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ part,
-                       int* __restrict__ nonfinite) {
+                       int* __restrict__ nonfinite, double* __restrict__ out) {
   double mn[S], mx[S];
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
@@ -80,31 +80,33 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
     }
     if (bad) atomicOr(nonfinite, 1);
   }
-}
-
-// min/max are order-independent, so the fold is deterministic; out[2S] gets
-// the non-finite flag so one D2H copy returns everything.
-template <int S>
-__global__ void k_bbox_final(const double* __restrict__ part, int nblk, const int* __restrict__ flag,
-                             double* __restrict__ out) {
-  double mn[S], mx[S];
+  if (out == nullptr) return;
+  // last block to finish folds the partials (one launch instead of two on
+  // the repulsion chain's critical path); nonfinite[1] is the ticket
+  __shared__ bool last;
+  if (threadIdx.x == 0) {
+    __threadfence();
+    last = atomicAdd(nonfinite + 1, 1) == (int)gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
-  for (int b = threadIdx.x; b < nblk; b += blockDim.x) {
+  for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
 #pragma unroll
     for (int d = 0; d < S; ++d) {
-      mn[d] = fmin(mn[d], part[b * 2 * S + d]);
-      mx[d] = fmax(mx[d], part[b * 2 * S + S + d]);
+      mn[d] = fmin(mn[d], __ldcg(part + b * 2 * S + d));
+      mx[d] = fmax(mx[d], __ldcg(part + b * 2 * S + S + d));
     }
   }
-  __shared__ double smn[32][S], smx[32][S];
 #pragma unroll
   for (int d = 0; d < S; ++d)
     for (int o = 16; o > 0; o >>= 1) {
       mn[d] = fmin(mn[d], __shfl_xor_sync(0xffffffffu, mn[d], o));
       mx[d] = fmax(mx[d], __shfl_xor_sync(0xffffffffu, mx[d], o));
     }
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  __syncthreads();
   if (lane == 0)
 #pragma unroll
     for (int d = 0; d < S; ++d) { smn[wid][d] = mn[d]; smx[wid][d] = mx[d]; }
@@ -115,9 +117,11 @@ __global__ void k_bbox_final(const double* __restrict__ part, int nblk, const in
       for (int d = 0; d < S; ++d) { mn[d] = fmin(mn[d], smn[w][d]); mx[d] = fmax(mx[d], smx[w][d]); }
 #pragma unroll
     for (int d = 0; d < S; ++d) { out[d] = mn[d]; out[S + d] = mx[d]; }
-    out[2 * S] = (double)flag[0];
+    out[2 * S] = (double)__ldcg(nonfinite);
+    nonfinite[1] = 0;  // ticket reset for the next launch
   }
 }
+
 
 // Bounding box in two halves: bbox_launch queues the min/max kernels and the
 // 40-byte readback on st (and records ctx->ev_bbox); bbox_wait blocks the host
@@ -131,17 +135,15 @@ int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
   double* part = (double*)ctx->bbox_part.ptr;
   double* outd = part + (size_t)nblk * 2 * S;
   int* flag = (int*)ctx->counter.ptr;
-  FITSNE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int), st));
+  // flag[0]: non-finite, flag[1]: last-block ticket (k_bbox folds the partials)
+  FITSNE_CUDA(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
   if (ctx->dtype == FITSNE_F32) {
-    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag);
-    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag);
+    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd);
+    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd);
   } else {
-    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag);
-    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag);
+    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd);
+    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd);
   }
-  FITSNE_CHECK_LAUNCH();
-  if (S == 1) k_bbox_final<1><<<1, 256, 0, st>>>(part, nblk, flag, outd);
-  else k_bbox_final<2><<<1, 256, 0, st>>>(part, nblk, flag, outd);
   FITSNE_CHECK_LAUNCH();
   FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * (2 * S + 1),
                               cudaMemcpyDeviceToHost, st));
