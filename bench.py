@@ -64,6 +64,8 @@ def parse():
                     help="also time the complete 1000-iteration C3 t-SNE run (run_tsne, fused "
                          "device iterations, late exaggeration 4 from 750) and report it")
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the multi-GPU (sharded, NCCL) code path even with one rank (testing)")
     ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2, 3],
                     help="0 direct atomics, 1 auto (default), 2 box-sorted")
     ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2],
@@ -291,7 +293,8 @@ def run_ours(args):
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
-    if world > 1:
+    sharded = world > 1 or args.sharded
+    if sharded:
         dist.init_process_group("nccl")
     dev = local
     dt = torch.float32 if args.dtype == "float32" else torch.float64
@@ -299,7 +302,7 @@ def run_ours(args):
     n = P.n
     stream = torch.cuda.current_stream(dev)
 
-    if world > 1:
+    if sharded:
         from paper_1712_09005_b200 import parallel
         ev = parallel.ShardedGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
                                       points_per_interval=3)
@@ -308,6 +311,7 @@ def run_ours(args):
         step = lambda: ev.gradient(y_local, 1.0)  # noqa: E731  (all-gathers Y inside)
         for _ in range(args.warmup):
             step()
+        launches = count_launches(step)
         dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(dev) as clk:
@@ -324,7 +328,8 @@ def run_ours(args):
                 "data": "synthetic",
                 "config": {"workload": WORKLOADS["c3"]["desc"], "N": n, "parallelism": f"points{world}",
                            "l2": "inputs larger than L2 (CSR > 126 MB)"},
-                "gpu_launches": ev.launches_per_step * args.steps,
+                "gpu_launches": launches * args.steps,
+                "gpu_launches_per_step": launches,
                 "clocks": clk.summary(),
             }
             print(json.dumps(line), flush=True)

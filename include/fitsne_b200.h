@@ -225,6 +225,12 @@ int fitsne_gather_tsne(fitsne_ctx* ctx, const void* Y_local, int64_t n_local, vo
                        void* k1, void* k2, void* stream);
 int fitsne_gradient_rows(fitsne_ctx* ctx, const void* Y_full, const void* forces_local,
                          double alpha, void* grad_local, void* stream);
+/* The combine of the sharded path (optimizer.py:262): grad = 4 (alpha F_attr
+ * - F_rep) over n rows of the context's dims, when F_attr (fitsne_attractive,
+ * run concurrently with the repulsion stages) and F_rep (fitsne_gather_tsne)
+ * were computed separately. */
+int fitsne_combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int64_t n, double alpha,
+                        void* grad, void* stream);
 
 #ifdef __cplusplus
 }

@@ -79,6 +79,7 @@ _SIGS = {
     "fitsne_fft_tsne": (_int, [_vp, _vp, _i64, _int, C.POINTER(_dbl), _vp]),
     "fitsne_gather_tsne": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "fitsne_gradient_rows": (_int, [_vp, _vp, _vp, _dbl, _vp, _vp]),
+    "fitsne_combine_rows": (_int, [_vp, _vp, _vp, _i64, _dbl, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

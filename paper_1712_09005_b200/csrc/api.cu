@@ -486,6 +486,13 @@ int fitsne_gradient_rows(fitsne_ctx* ctx, const void* Y_full, const void* forces
   return attractive(ctx, Y_full, forces_local, alpha, grad_local, 1, false, S_(stream));
 }
 
+int fitsne_combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int64_t n, double alpha,
+                        void* grad, void* stream) {
+  CTX_CHECK(ctx);
+  if (!(alpha >= 1.0)) { set_error("exaggeration alpha must be >= 1"); return FITSNE_EINVAL; }
+  return combine_rows(ctx, attr, frep, n, alpha, grad, S_(stream));
+}
+
 int fitsne_exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* charges, int ncharge,
                        int kernel, int include_self, void* out, void* stream) {
   CTX_CHECK(ctx);

@@ -730,6 +730,29 @@ int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_
   return FITSNE_OK;
 }
 
+// grad = 4 (alpha F_attr - F_rep) for m values (the sharded path's combine,
+// after an F_attr computed concurrently with the repulsion stages)
+template <typename T>
+__global__ void k_combine_rows(const T* __restrict__ attr, const T* __restrict__ frep, int64_t m,
+                               T alpha, T* __restrict__ out) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < m) out[i] = (T)4 * (alpha * attr[i] - frep[i]);
+}
+
+int combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int64_t n, double alpha,
+                 void* out, cudaStream_t st) {
+  const int64_t m = n * ctx->dims;
+  if (m <= 0) return FITSNE_OK;
+  if (ctx->dtype == FITSNE_F32)
+    k_combine_rows<float><<<nblocks(m), kBlock, 0, st>>>((const float*)attr, (const float*)frep, m,
+                                                        (float)alpha, (float*)out);
+  else
+    k_combine_rows<double><<<nblocks(m), kBlock, 0, st>>>((const double*)attr, (const double*)frep,
+                                                          m, alpha, (double*)out);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
                   double momentum, double lr, double* kl_dev, int32_t* status_dev, cudaStream_t st) {
   const int64_t n = ctx->n_total;

@@ -12,7 +12,8 @@ Points and CSR rows are partitioned by contiguous index range (rank r owns
   5. all-reduce SUM of the accumulator (4 slots x G nodes)
   6. FFT stage + Parseval Z (replicated; the grid is small)  fitsne_fft_tsne
   7. gather of F_rep at the local points                     fitsne_gather_tsne
-  8. SpMV over the local rows + combine                      fitsne_gradient_rows
+  8. SpMV over the local rows + combine                      fitsne_attractive on a
+     side stream beside 4-7 (CUDA path), then fitsne_combine_rows
 
 The stage arithmetic is pluggable (`stages`): `LibStages` runs the CUDA
 library; the multi-process CPU tests plug in an oracle-backed implementation
@@ -40,7 +41,9 @@ def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
 class LibStages:
     """Stage implementation on the CUDA library (one context per rank)."""
 
-    launches_per_step = 8  # bbox x2, spread, rows, spec cols, cols, rows inverse, gather + SpMV
+    # bbox, band spread (count, scan x2, scatter, reduce), FFT (rows, spectrum
+    # columns, columns, rows inverse), gather, tiled SpMV + finish, combine
+    launches_per_step = 14
 
     def __init__(self, P, dims, dtype, device, min_intervals, points_per_interval,
                  intervals_per_integer, row_begin, row_end):
@@ -50,6 +53,8 @@ class LibStages:
         self.n_total = n_points(P)
         self.ctx = _lib.Context(device, dims, dtype, points_per_interval, min_intervals,
                                 intervals_per_integer)
+        # the row SpMV (attract_start) runs beside the repulsion stages: the
+        # context's default overlapped schedule sizes its grid to 7/8 of the SMs
         self.csr = device_csr(P, dtype, device, row_begin, row_end)
         self.ctx.set_affinities(self.csr)
 
@@ -77,11 +82,14 @@ class LibStages:
                    "fitsne_spread_tsne")
         return acc
 
-    def fft(self, acc: torch.Tensor) -> float:
+    def fft(self, acc: torch.Tensor, want_z: bool = True):
+        """FFT stage + Parseval Z; without want_z, Z stays on the device (no
+        host round trip inside the step)."""
         z = C.c_double()
         _lib.check(self.ctx.lib.fitsne_fft_tsne(self.ctx.h, _lib.ptr(acc), self.n_total, 0,
-                                                C.byref(z), self.ctx.stream), "fitsne_fft_tsne")
-        return float(z.value)
+                                                C.byref(z) if want_z else None, self.ctx.stream),
+                   "fitsne_fft_tsne")
+        return float(z.value) if want_z else None
 
     def gather(self, y_local: torch.Tensor) -> torch.Tensor:
         f = torch.empty_like(y_local)
@@ -89,6 +97,36 @@ class LibStages:
                                                    _lib.ptr(f), None, None, self.ctx.stream),
                    "fitsne_gather_tsne")
         return f
+
+    # -- SpMV concurrent with the repulsion stages ---------------------------
+    def attract_start(self, y_full: torch.Tensor):
+        """F_attr of the local rows on a side stream, ordered after the work
+        already queued (the all-gather of Y); returns the completion event."""
+        if not hasattr(self, "_side"):
+            self._side = torch.cuda.Stream(device=self.device)
+            self._attr = None
+        n_local = self.csr.n_rows
+        if self._attr is None or self._attr.shape[0] != n_local:
+            self._attr = torch.empty((n_local, self.dims), dtype=self.dtype, device=self.device)
+        ready = torch.cuda.Event()
+        ready.record(torch.cuda.current_stream(self.device))
+        self._side.wait_event(ready)
+        y_full.record_stream(self._side)
+        _lib.check(self.ctx.lib.fitsne_attractive(self.ctx.h, _lib.ptr(y_full), _lib.ptr(self._attr),
+                                                  C.c_void_p(self._side.cuda_stream)),
+                   "fitsne_attractive")
+        done = torch.cuda.Event()
+        done.record(self._side)
+        return done
+
+    def attract_finish(self, done, forces_local: torch.Tensor, alpha: float) -> torch.Tensor:
+        torch.cuda.current_stream(self.device).wait_event(done)
+        g = torch.empty_like(forces_local)
+        _lib.check(self.ctx.lib.fitsne_combine_rows(self.ctx.h, _lib.ptr(self._attr),
+                                                    _lib.ptr(forces_local), forces_local.shape[0],
+                                                    float(alpha), _lib.ptr(g), self.ctx.stream),
+                   "fitsne_combine_rows")
+        return g
 
     def attract_rows(self, y_full: torch.Tensor, forces_local: torch.Tensor,
                      alpha: float) -> torch.Tensor:
@@ -146,13 +184,19 @@ class ShardedGradient:
         # 3: all-gather Y (skipped when the caller already holds it)
         if y_full is None:
             y_full = self._all_gather_rows(y_local)
+        overlap = hasattr(st, "attract_start")
+        if overlap:
+            # 8a: the local rows' SpMV runs on a side stream beside 4-7
+            done = st.attract_start(y_full)
         # 4-5: private spread + grid all-reduce
         acc = st.spread(y_local)
         dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group)
-        # 6: replicated FFT stage
-        z = st.fft(acc)
-        if not z > 0:
+        # 6: replicated FFT stage (Z stays on the device on the CUDA path)
+        z = st.fft(acc, want_z=not overlap) if overlap else st.fft(acc)
+        if z is not None and not z > 0:
             raise ValueError("normalization Z must be positive")
-        # 7-8: gather local F_rep, SpMV over local rows
+        # 7-8: gather local F_rep, combine with the SpMV over the local rows
         f_local = st.gather(y_local)
+        if overlap:
+            return st.attract_finish(done, f_local, alpha)
         return st.attract_rows(y_full, f_local, alpha)
