@@ -243,3 +243,49 @@ def test_tiled_unsorted_rows(cuda):
     for shape in ((64, 128, 0), (512, 1024, 9)):
         got = _attr(_ctx(2, *shape), pcsr, y)
         assert rel_l2(got, want) <= 1e-5
+
+
+def test_random_graph_keeps_csr_kernel(cuda):
+    """Auto mode: a P without column locality (random partners, ~1 entry per
+    (row, chunk) segment) stays on the CSR kernel even above 2^22 entries;
+    forced tiling still works and agrees."""
+    from paper_1712_09005_b200 import _lib
+    n, k = 600_000, 8  # 16 entries per row over 74 chunks of 8192 points
+    rr, cc, v, Y = _graph(n, k, seed=31, clustered=False)
+    assert 2 * rr.size >= (1 << 22)
+    csr = _csr(n, rr, cc, v)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    st = (C.c_int64 * 6)()
+    ctx = _ctx(1, 3072, 8192)
+    ctx.set_affinities(csr)
+    _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), st, ctx.stream), "stats")
+    assert st[0] == 0
+    auto = _attr(ctx, csr, y)
+    forced = _attr(_ctx(2, 3072, 8192), csr, y)
+    want = O.attraction(rr, cc, v, Y.astype(np.float32).astype(np.float64))
+    assert rel_l2(auto, want) <= 1e-5
+    assert rel_l2(forced, want) <= 1e-5
+
+
+@pytest.mark.parametrize("dtype,tol", [("float32", 1e-3), ("float64", 1e-5)])
+def test_one_dim_gradient_at_scale(cuda, dtype, tol):
+    """1-D embedding (config C5's path: 1-D grid, single-block FFT), N = 200k
+    clustered points, random kNN-like P: gradient vs the oracle."""
+    from paper_1712_09005_b200 import optimizer
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    rng = np.random.default_rng(41)
+    n, k = 200_000, 15
+    c = rng.uniform(-150, 150, 30)
+    y = (c[rng.integers(0, 30, n)] + 3.0 * rng.standard_normal(n))[:, None]
+    r = np.repeat(np.arange(n), k)
+    cc = rng.integers(0, n - 1, n * k)
+    cc = cc + (cc >= r)
+    key = np.unique(np.minimum(r, cc) * n + np.maximum(r, cc))
+    vals = rng.exponential(1.0, key.size)
+    vals /= 2 * vals.sum()
+    P = SparseAffinities(n=n, rows=key // n, cols=key % n, values=vals)
+    yd = y.astype(np.float32).astype(np.float64) if dtype == "float32" else y
+    g = optimizer.gradient(P, torch.from_numpy(yd).to(device=0, dtype=getattr(torch, dtype)), 12.0,
+                           50, 3, "fft").double().cpu().numpy()
+    want = O.grad(P.rows, P.cols, P.values, yd, 12.0, 50, 3, "fft")
+    assert rel_l2(g, want) <= tol
