@@ -129,6 +129,11 @@ int fitsne_make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, fitsne_grid* gri
  * calls fitsne_grid_from_bbox on every rank).  bbox_host = {min_0..min_{s-1},
  * max_0..max_{s-1}}. */
 int fitsne_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, void* stream);
+/* The same into DEVICE memory, stream-ordered, no host sync (multi-GPU: the
+ * ranks all-reduce it on the device and read it back once):
+ * bbox_dev[0 .. 2s] = {min_0..min_{s-1}, -max_0..-max_{s-1}, -nonfinite}, so a
+ * single MIN all-reduce combines every field. */
+int fitsne_bbox_device(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_dev, void* stream);
 int fitsne_grid_from_bbox(fitsne_ctx* ctx, const double* bbox_host, fitsne_grid* grid_host);
 /* Install an explicit grid (nbody.InterpGrid built by the caller). */
 int fitsne_set_grid(fitsne_ctx* ctx, const fitsne_grid* grid_host);

@@ -57,6 +57,7 @@ _SIGS = {
     "fitsne_tiled_stats": (_int, [_vp, _vp, _vp, _vp]),
     "fitsne_make_grid": (_int, [_vp, _vp, _i64, C.POINTER(Grid), _vp]),
     "fitsne_bbox": (_int, [_vp, _vp, _i64, C.POINTER(_dbl), _vp]),
+    "fitsne_bbox_device": (_int, [_vp, _vp, _i64, _vp, _vp]),
     "fitsne_grid_from_bbox": (_int, [_vp, C.POINTER(_dbl), C.POINTER(Grid)]),
     "fitsne_set_grid": (_int, [_vp, C.POINTER(Grid)]),
     "fitsne_point_interp": (_int, [_vp, _vp, _i64, _vp, _vp, _vp]),

@@ -248,6 +248,22 @@ int fitsne_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host, vo
   return compute_bbox(ctx, Y, n, bbox_host, S_(stream));
 }
 
+__global__ void k_bbox_empty(double* out, int S) {
+  for (int d = 0; d < S; ++d) { out[d] = INFINITY; out[S + d] = INFINITY; }  // -max = +inf
+  out[2 * S] = 0.0;
+}
+
+int fitsne_bbox_device(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_dev, void* stream) {
+  CTX_CHECK(ctx);
+  if (!bbox_dev) { set_error("null bbox buffer"); return FITSNE_EINVAL; }
+  if (n < 1) {
+    k_bbox_empty<<<1, 1, 0, S_(stream)>>>(bbox_dev, ctx->dims);
+    FITSNE_CHECK_LAUNCH();
+    return FITSNE_OK;
+  }
+  return bbox_device(ctx, Y, n, bbox_dev, S_(stream));
+}
+
 int fitsne_grid_from_bbox(fitsne_ctx* ctx, const double* bbox_host, fitsne_grid* grid_host) {
   CTX_CHECK(ctx);
   fitsne_grid g;

@@ -16,6 +16,7 @@ int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
 // grid for work queued on st (make_grid_finish)
 int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
 int bbox_wait(fitsne_ctx* ctx, double* bbox_host);
+int bbox_device(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, cudaStream_t st);
 int make_grid_finish(fitsne_ctx* ctx, cudaStream_t st);
 
 // repulsion pipeline ------------------------------------------------------------

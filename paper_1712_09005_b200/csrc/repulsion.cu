@@ -39,7 +39,7 @@ static inline int grid_for(int64_t n, int block = kBlock) {
 // =============================================================================
 template <typename T, int S>
 __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ part,
-                       int* __restrict__ nonfinite, double* __restrict__ out) {
+                       int* __restrict__ nonfinite, double* __restrict__ out, int negate_max) {
   double mn[S], mx[S];
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
@@ -115,9 +115,10 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
     for (int w = 1; w < (int)(blockDim.x + 31) / 32; ++w)
 #pragma unroll
       for (int d = 0; d < S; ++d) { mn[d] = fmin(mn[d], smn[w][d]); mx[d] = fmax(mx[d], smx[w][d]); }
+    const double sg = negate_max ? -1.0 : 1.0;
 #pragma unroll
-    for (int d = 0; d < S; ++d) { out[d] = mn[d]; out[S + d] = mx[d]; }
-    out[2 * S] = (double)__ldcg(nonfinite);
+    for (int d = 0; d < S; ++d) { out[d] = mn[d]; out[S + d] = sg * mx[d]; }
+    out[2 * S] = sg * (double)__ldcg(nonfinite);
     nonfinite[1] = 0;  // ticket reset for the next launch
   }
 }
@@ -127,24 +128,39 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
 // 40-byte readback on st (and records ctx->ev_bbox); bbox_wait blocks the host
 // on that event only, so work queued on other streams in between (the
 // attractive SpMV) is dispatched behind the bbox blocks, not ahead of them.
-int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
+// k_bbox into out_dev (null: ctx's readback buffer) on st; negate_max for the
+// MIN-all-reduce layout of fitsne_bbox_device
+static int bbox_kernels(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, int negate_max,
+                        cudaStream_t st, double** outd_used) {
   const int S = ctx->dims;
   int nblk = (int)std::min<int64_t>(std::max<int64_t>((n + kBlock - 1) / kBlock, 1), 4 * ctx->num_sms);
   FITSNE_TRY(ensure(ctx->bbox_part, sizeof(double) * (size_t)nblk * 2 * S + 64));
   FITSNE_TRY(ensure(ctx->counter, 64 * sizeof(int)));
   double* part = (double*)ctx->bbox_part.ptr;
-  double* outd = part + (size_t)nblk * 2 * S;
+  double* outd = out_dev ? out_dev : part + (size_t)nblk * 2 * S;
   int* flag = (int*)ctx->counter.ptr;
   // flag[0]: non-finite, flag[1]: last-block ticket (k_bbox folds the partials)
   FITSNE_CUDA(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
   if (ctx->dtype == FITSNE_F32) {
-    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd);
-    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd);
+    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max);
+    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max);
   } else {
-    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd);
-    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd);
+    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max);
+    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max);
   }
   FITSNE_CHECK_LAUNCH();
+  if (outd_used) *outd_used = outd;
+  return FITSNE_OK;
+}
+
+int bbox_device(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, cudaStream_t st) {
+  return bbox_kernels(ctx, Y, n, out_dev, 1, st, nullptr);
+}
+
+int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
+  const int S = ctx->dims;
+  double* outd = nullptr;
+  FITSNE_TRY(bbox_kernels(ctx, Y, n, nullptr, 0, st, &outd));
   FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * (2 * S + 1),
                               cudaMemcpyDeviceToHost, st));
   if (!ctx->ev_bbox) FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_bbox, cudaEventDisableTiming));

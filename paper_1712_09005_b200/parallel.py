@@ -4,8 +4,9 @@ Points and CSR rows are partitioned by contiguous index range (rank r owns
 [N r / R, N (r+1) / R)).  One evaluation of 4 (alpha F_attr - F_rep)
 (optimizer.py:248-262) for the local rows:
 
-  1. local bounding box                  fitsne_bbox
-  2. all-reduce MIN / MAX of the box     -> identical grid on every rank
+  1. local bounding box on the device    fitsne_bbox_device
+  2. one MIN all-reduce of {min, -max, -nonfinite} and one readback
+                                         -> identical grid on every rank
      (grid formulas nbody.py:131-143, fitsne_grid_from_bbox)
   3. all-gather of Y                     (needed by the row-partitioned SpMV)
   4. spread of the local points into a private accumulator   fitsne_spread_tsne
@@ -67,6 +68,24 @@ class LibStages:
         _lib.check(self.ctx.lib.fitsne_bbox(self.ctx.h, _lib.ptr(y_local), y_local.shape[0], out,
                                             self.ctx.stream), "fitsne_bbox")
         return np.array(out[:], dtype=np.float64)
+
+    def bbox_start(self, y_local: torch.Tensor) -> torch.Tensor:
+        """Local bounding box on the device as {min, -max, -nonfinite} (no
+        host sync; queued ahead of the SpMV so its blocks get the GPU first)."""
+        buf = torch.empty(2 * self.dims + 1, dtype=torch.float64, device=self.device)
+        _lib.check(self.ctx.lib.fitsne_bbox_device(self.ctx.h, _lib.ptr(y_local), y_local.shape[0],
+                                                   _lib.ptr(buf), self.ctx.stream),
+                   "fitsne_bbox_device")
+        return buf
+
+    def grid_finish(self, buf: torch.Tensor, group) -> None:
+        """One MIN all-reduce of the packed boxes, one readback, the grid."""
+        s = self.dims
+        dist.all_reduce(buf, op=dist.ReduceOp.MIN, group=group)
+        v = buf.cpu().numpy()
+        if -v[2 * s] > 0:
+            raise ValueError("points must be finite")
+        self.set_grid(np.concatenate([v[:s], -v[s:2 * s]]))
 
     def set_grid(self, bbox: np.ndarray) -> None:
         arr = (C.c_double * (2 * self.dims))(*bbox.tolist())
@@ -161,6 +180,12 @@ class ShardedGradient:
         return y_full[self.row_begin:self.row_end]
 
     def _all_gather_rows(self, y_local):
+        if self.world == 1:
+            return y_local.contiguous()
+        if min(self.counts) == max(self.counts):  # equal shards: gather in place
+            out = y_local.new_empty((self.n, self.dims))
+            dist.all_gather_into_tensor(out, y_local.contiguous(), group=self.group)
+            return out
         m = max(self.counts)
         pad = y_local.new_zeros((m, self.dims))
         pad[: y_local.shape[0]] = y_local
@@ -173,21 +198,28 @@ class ShardedGradient:
         if alpha < 1.0:
             raise ValueError("exaggeration alpha must be >= 1")
         st = self.stages
-        # 1-2: global bounding box -> identical grid everywhere
-        bb = st.bbox(y_local)
-        s = self.dims
-        lo = st.to_comm(bb[:s])
-        hi = st.to_comm(bb[s:])
-        dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
-        dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.group)
-        st.set_grid(np.concatenate([lo.cpu().numpy(), hi.cpu().numpy()]))
+        overlap = hasattr(st, "attract_start")
         # 3: all-gather Y (skipped when the caller already holds it)
         if y_full is None:
             y_full = self._all_gather_rows(y_local)
-        overlap = hasattr(st, "attract_start")
+        device_box = hasattr(st, "bbox_start")
+        if device_box:
+            box = st.bbox_start(y_local)  # 1: queued first, so it gets the whole GPU
         if overlap:
-            # 8a: the local rows' SpMV runs on a side stream beside 4-7
+            # 8a: the local rows' SpMV needs no grid: it runs on a side stream
+            # while the host waits for the global box and 4-7 are queued
             done = st.attract_start(y_full)
+        # 2: global bounding box -> identical grid everywhere
+        if device_box:
+            st.grid_finish(box, self.group)  # one all-reduce, one readback
+        else:
+            bb = st.bbox(y_local)
+            s = self.dims
+            lo = st.to_comm(bb[:s])
+            hi = st.to_comm(bb[s:])
+            dist.all_reduce(lo, op=dist.ReduceOp.MIN, group=self.group)
+            dist.all_reduce(hi, op=dist.ReduceOp.MAX, group=self.group)
+            st.set_grid(np.concatenate([lo.cpu().numpy(), hi.cpu().numpy()]))
         # 4-5: private spread + grid all-reduce
         acc = st.spread(y_local)
         dist.all_reduce(acc, op=dist.ReduceOp.SUM, group=self.group)
