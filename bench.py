@@ -316,9 +316,39 @@ def run_ours(args):
         torch.cuda.synchronize()
         with ClockSampler(dev) as clk:
             ms = timed(step, args.steps, stream)
-        t = torch.tensor([ms], device=dev)
+        # e2e per rank: this rank's Y rows from pinned host memory in, its
+        # gradient rows out, every step (max over ranks of the same timing)
+        st_ = ev.stages
+        yh = y_local.cpu().pin_memory()
+        gh = torch.empty_like(yh).pin_memory()
+        yd = torch.empty_like(y_local)
+
+        def e2e_step():
+            yd.copy_(yh, non_blocking=True)
+            gh.copy_(ev.gradient(yd, 1.0), non_blocking=True)
+            stream.synchronize()
+        for _ in range(2):
+            e2e_step()
+        dist.barrier()
+        t0w = time.perf_counter()
+        ms_e2e = timed(e2e_step, args.steps, stream)
+        ms_e2e = max(ms_e2e, (time.perf_counter() - t0w) / args.steps * 1e3)
+        # roofline: this rank's attractive SpMV alone (same kernel and grid as
+        # in the step), bytes of its rows
+        def spmv_only():
+            done = st_.attract_start(y_full)
+            stream.wait_event(done)
+        for _ in range(3):
+            spmv_only()
+        ms_spmv = timed(spmv_only, args.steps, stream)
+        es = 4 if dt == torch.float32 else 8
+        nnz_l = int(st_.csr.col.numel())
+        n_l = int(y_local.shape[0])
+        b_spmv = nnz_l * (4 + es) + 8 * (n_l + 1) + 3 * 2 * es * n_l
+        t = torch.tensor([ms, ms_e2e, ms_spmv], device=dev, dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+        ms, ms_e2e, ms_spmv = (float(x) for x in t.tolist())
+        peak, peak_src = peaks()
         if rank == 0:
             line = {
                 "metric": "t-SNE gradient evals/sec at N=1.3M 2-D", "value": 1e3 / ms,
@@ -328,6 +358,18 @@ def run_ours(args):
                 "data": "synthetic",
                 "config": {"workload": WORKLOADS["c3"]["desc"], "N": n, "parallelism": f"points{world}",
                            "l2": "inputs larger than L2 (CSR > 126 MB)"},
+                "roofline": {"kernel": "rank 0's local-row attractive SpMV (fitsne_attractive)",
+                             "bound": "hbm", "achieved": b_spmv / (ms_spmv * 1e-3) / 1e9,
+                             "peak": peak, "unit": "GB/s",
+                             "frac": b_spmv / (ms_spmv * 1e-3) / 1e9 / peak,
+                             "peak_source": peak_src, "algorithmic_bytes": b_spmv,
+                             "launch_ms": ms_spmv, "traffic": None},
+                "cpu_baseline": None,
+                "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
+                        "api": "parallel.ShardedGradient.gradient with this rank's rows copied in "
+                               "from pinned host memory and its gradient rows copied out",
+                        "h2d_bytes_per_step": int(yh.numel() * yh.element_size()) * world,
+                        "d2h_bytes_per_step": int(gh.numel() * gh.element_size()) * world},
                 "gpu_launches": launches * args.steps,
                 "gpu_launches_per_step": launches,
                 "clocks": clk.summary(),
