@@ -25,11 +25,17 @@
 
 namespace fitsne {
 
-static constexpr int kBandBlock = 256;
+#ifndef FITSNE_BAND_BLOCK
+#define FITSNE_BAND_BLOCK 256
+#endif
+#ifndef FITSNE_BAND_KEYS
+#define FITSNE_BAND_KEYS 2048
+#endif
+static constexpr int kBandBlock = FITSNE_BAND_BLOCK;
 static constexpr int kBandPts = 4096;                 // points per count / scatter block
 static constexpr int kBandChunk = 2048;               // sorted points per reduce block
 static constexpr int kBandRun = kBandChunk / kBandBlock;  // sorted points per reduce thread
-static constexpr int kBandKeys = 4096;                // (box rows in a chunk) x n_int
+static constexpr int kBandKeys = FITSNE_BAND_KEYS;    // (box rows in a chunk) x n_int; 2048 keeps 4 blocks / SM
 static constexpr int kBandMaxRows = 1024;             // n_int bound (fp32: n_int <= 864)
 static constexpr int kBandSmem = kBandChunk * 16 + kBandKeys * 4 + kBandChunk * 4;
 
