@@ -264,6 +264,27 @@ class TestLargeProperties:
         assert rel_l2(rep.forces.cpu().numpy(), f) <= 1e-3
         assert abs(rep.z - z) <= 1e-4 * z
 
+    def test_c2_interpolation_error_vs_exact(self, fs):
+        """Config 2 against the exact O(N^2) sums (the device k_exact kernel in
+        fp64 as the accuracy oracle): the fp32 FFT path's interpolation error
+        must not exceed the reference algorithm's own (oracle fp64 FFT vs the
+        same exact sums) by more than 10%."""
+        _, _, opt, _ = fs
+        rng = np.random.default_rng(2)
+        c = rng.uniform(-40, 40, (20, 2))
+        sizes = rng.multinomial(100_000, rng.dirichlet(np.ones(20)))
+        y = np.concatenate([c[i] + 1.5 * rng.standard_normal((s, 2)) for i, s in enumerate(sizes)])
+        y = y.astype(np.float32).astype(np.float64)
+        exact = opt.compute_repulsive(torch.from_numpy(y).cuda(), method="exact")
+        fe = exact.forces.cpu().numpy()
+        ours = opt.compute_repulsive(torch.from_numpy(y.astype(np.float32)).cuda(), 50, 3, "fft")
+        f_ref, z_ref, _, _ = O.repulsion(y, 50, 3, "fft")
+        err_ours = rel_l2(ours.forces.cpu().numpy(), fe)
+        err_ref = rel_l2(f_ref, fe)
+        assert 1e-3 < err_ref < 5e-2  # the interpolation error the reference itself makes
+        assert err_ours <= 1.1 * err_ref, (err_ours, err_ref)
+        assert abs(ours.z - exact.z) <= 1e-3 * exact.z
+
     def test_translation_invariance(self, fs):
         _, nbody, _, _ = fs
         rng = np.random.default_rng(13)
