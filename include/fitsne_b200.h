@@ -107,7 +107,7 @@ enum fitsne_option {
  *   block, default 3072; points per column chunk, default 8192); both even and
  *   <= 16384.  Shapes whose shared-memory footprint (24 rows + 16 cols + 4.3
  *   rows bytes) exceeds 226 KiB use the CSR kernel.  FITSNE_OPT_TILED_CTAS:
- *   persistent grid of the tiled kernel (default 0 = 7/8 of the SMs when the
+ *   persistent grid of the tiled kernel (default 0 = 11/12 of the SMs when the
  *   repulsion runs concurrently on the side stream, else one CTA per SM).
  *   FITSNE_OPT_HOST_PIECES: fitsne_gradient_host schedule; 0 (default) = copy
  *   in, gradient, copy out; 1 = tiled SpMV in row pieces on a high-priority

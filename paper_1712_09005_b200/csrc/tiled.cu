@@ -366,13 +366,15 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
   for (int64_t k = lane; k < (int64_t)ns * 32; k += 32) hr[k] = rows[(int64_t)sb * 32 + k];
 }
 
-// Persistent grid: with the overlapped schedule 1/8 of the SMs stay free
+// Persistent grid: with the overlapped schedule 1/12 of the SMs stay free
 // for the spread / FFT stages running concurrently on the side stream (the
-// tiled kernel fills an SM: 1024 threads x 64 registers, ~210 KB of shared
-// memory); serial schedules use every SM.
+// tiled kernel fills an SM: 1024 threads x 64 registers, ~218 KB of shared
+// memory); serial schedules use every SM.  At C3 the step time is flat from
+// ~120 to ~136 CTAs (the repulsion chain and the SpMV trade places as the
+// critical path); the SpMV is most efficient at the top of that range.
 static int tiled_grid(const fitsne_ctx* ctx) {
   if (ctx->tiled_ctas > 0) return ctx->tiled_ctas;
-  if (ctx->overlap != 0) return std::max(1, (ctx->num_sms * 7) / 8);
+  if (ctx->overlap != 0) return std::max(1, ctx->num_sms - ctx->num_sms / 12);
   return ctx->num_sms;
 }
 
