@@ -87,13 +87,13 @@ def _problem(n=1200, dims=2, seed=0):
     return y, rows, cols, vals
 
 
-def _worker(rank, world, port, dims, q):
+def _worker(rank, world, port, dims, q, n_points=1200):
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         from paper_1712_09005_b200.parallel import ShardedGradient, shard_range
-        y, rows, cols, vals = _problem(dims=dims)
+        y, rows, cols, vals = _problem(n=n_points, dims=dims)
         n = len(y)
         lo, hi = shard_range(n, rank, world)
 
@@ -126,19 +126,22 @@ def _free_port():
     return p
 
 
-@pytest.mark.parametrize("dims", [1, 2])
-def test_sharded_gradient_world2_matches_single_process(dims):
+@pytest.mark.parametrize("dims,world,n_points", [(1, 2, 1200), (2, 2, 1200), (2, 3, 1201)])
+def test_sharded_gradient_world2_matches_single_process(dims, world, n_points):
+    """world 2 (equal shards: all_gather_into_tensor) and world 3 with a
+    ragged last shard (padded all-gather)."""
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, dims, q)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, world, port, dims, q, n_points))
+             for r in range(world)]
     for p in procs:
         p.start()
     full = q.get(timeout=120)
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0
-    y, rows, cols, vals = _problem(dims=dims)
+    y, rows, cols, vals = _problem(n=n_points, dims=dims)
     ref = O.grad(rows, cols, vals, y, 12.0, 50, 3, "fft")
     # the shard's grid is the global one, so the only differences are summation order
     assert np.linalg.norm(full - ref) / np.linalg.norm(ref) <= 1e-10
