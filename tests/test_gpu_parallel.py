@@ -74,3 +74,33 @@ def test_lib_stages_tiled_overlap_matches_fused(nccl_group):
     # both fp32: same math, different summation order (F_rep gathered inside
     # the fused combine vs. a separate gather)
     assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 1e-4
+
+
+def test_bbox_device_packed_layout(cuda):
+    """fitsne_bbox_device: {min, -max, -nonfinite} on the device, matching
+    fitsne_bbox; empty input gives the MIN-identity; a NaN sets the flag."""
+    import ctypes as C
+    from paper_1712_09005_b200 import _lib
+    rng = np.random.default_rng(4)
+    for dtype in (torch.float32, torch.float64):
+        ctx = _lib.Context(0, 2, dtype, 3, 50)
+        y = torch.from_numpy(rng.normal(3.0, 7.0, (12345, 2))).to(device=0, dtype=dtype)
+        buf = torch.empty(5, dtype=torch.float64, device=0)
+        _lib.check(ctx.lib.fitsne_bbox_device(ctx.h, _lib.ptr(y), y.shape[0], _lib.ptr(buf),
+                                              ctx.stream), "bbox_device")
+        host = (C.c_double * 4)()
+        _lib.check(ctx.lib.fitsne_bbox(ctx.h, _lib.ptr(y), y.shape[0], host, ctx.stream), "bbox")
+        v = buf.cpu().numpy()
+        np.testing.assert_array_equal(v[:2], np.array(host[:2]))
+        np.testing.assert_array_equal(-v[2:4], np.array(host[2:4]))
+        assert v[4] == 0.0
+        yc = y.cpu().double().numpy()
+        np.testing.assert_array_equal(v[:2], yc.min(0))
+        np.testing.assert_array_equal(-v[2:4], yc.max(0))
+        _lib.check(ctx.lib.fitsne_bbox_device(ctx.h, _lib.ptr(y), 0, _lib.ptr(buf), ctx.stream), "e")
+        v = buf.cpu().numpy()
+        assert np.all(np.isinf(v[:4]) & (v[:4] > 0)) and v[4] == 0.0
+        y[17, 1] = float("nan")
+        _lib.check(ctx.lib.fitsne_bbox_device(ctx.h, _lib.ptr(y), y.shape[0], _lib.ptr(buf),
+                                              ctx.stream), "nan")
+        assert buf.cpu().numpy()[4] < 0
