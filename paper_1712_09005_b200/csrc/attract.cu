@@ -631,7 +631,23 @@ static int spmv_for_combine(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_
   return attractive(ctx, Y, nullptr, 1.0, *attr, 0, kl, st, false);
 }
 
-int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st) {
+// Copy-out stream, per-piece events and the high-priority SpMV-piece stream
+// of the host-buffer gradient (created on first use).  The pieces' stream is
+// high priority: when piece q drains, the block scheduler hands the freed
+// SMs to piece q + 1 before the pending spread / FFT blocks.
+static int out_stream(fitsne_ctx* ctx) {
+  if (ctx->out) return FITSNE_OK;
+  int lo = 0, hi = 0;
+  FITSNE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  FITSNE_CUDA(cudaStreamCreateWithPriority(&ctx->hp, cudaStreamNonBlocking, hi));
+  FITSNE_CUDA(cudaStreamCreateWithFlags(&ctx->out, cudaStreamNonBlocking));
+  for (cudaEvent_t& e : ctx->ev_piece) FITSNE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
+  return FITSNE_OK;
+}
+
+int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st,
+                        void* grad_host) {
   const int64_t n = ctx->n_total;
   void* attr = nullptr;
   bool clear = false;
@@ -656,6 +672,35 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
     FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
   }
+  if (grad_host) {
+    // host result: combine in point ranges, each range's device-to-host copy
+    // (copy stream) overlapping the next range's combine
+    FITSNE_TRY(out_stream(ctx));
+    const size_t row_bytes = dsize(ctx->dtype) * (size_t)ctx->dims;
+    constexpr int kParts = 4;
+    for (int q = 0; q < kParts; ++q) {
+      const int64_t r0 = n * q / kParts, nr = n * (q + 1) / kParts - r0;
+      if (nr <= 0) continue;
+      const size_t off = row_bytes * (size_t)r0;
+      if (ctx->dtype == FITSNE_F32)
+        FITSNE_TRY((launch_combine<float, false>(ctx, (const unsigned char*)Y + off, nr,
+                                                 (unsigned char*)attr + off, alpha,
+                                                 (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
+                                                 nullptr, nullptr, clear, st)));
+      else
+        FITSNE_TRY((launch_combine<double, false>(ctx, (const unsigned char*)Y + off, nr,
+                                                  (unsigned char*)attr + off, alpha,
+                                                  (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
+                                                  nullptr, nullptr, clear, st)));
+      FITSNE_CUDA(cudaEventRecord(ctx->ev_piece[q], st));
+      FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_piece[q], 0));
+      FITSNE_CUDA(cudaMemcpyAsync((unsigned char*)grad_host + off, (unsigned char*)grad + off,
+                                  row_bytes * (size_t)nr, cudaMemcpyDeviceToHost, ctx->out));
+    }
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_out, ctx->out));
+    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_out, 0));
+    return FITSNE_OK;
+  }
   if (ctx->dtype == FITSNE_F32)
     return launch_combine<float, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
                                         nullptr, nullptr, clear, st);
@@ -679,23 +724,13 @@ int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_
   unsigned char* g = (unsigned char*)ctx->hg.ptr;
   FITSNE_CUDA(cudaMemcpyAsync(y, Y_host, bytes, cudaMemcpyHostToDevice, st));
   if (ctx->host_pieces == 0 || ctx->overlap == 0 || !tiled_usable(ctx, y, st)) {
-    FITSNE_TRY(gradient_overlapped(ctx, y, alpha, g, st));
-    FITSNE_CUDA(cudaMemcpyAsync(grad_host, g, bytes, cudaMemcpyDeviceToHost, st));
+    // the combine runs in point ranges whose copy-out overlaps the next range
+    FITSNE_TRY(gradient_overlapped(ctx, y, alpha, g, st, grad_host));
     FITSNE_CUDA(cudaStreamSynchronize(st));
     return FITSNE_OK;
   }
   FITSNE_TRY(side_stream(ctx));
-  if (!ctx->out) {
-    // the SpMV pieces run on a high-priority stream: when piece q drains, the
-    // block scheduler hands the freed SMs to piece q + 1 before the pending
-    // spread / FFT blocks of the side stream
-    int lo = 0, hi = 0;
-    FITSNE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    FITSNE_CUDA(cudaStreamCreateWithPriority(&ctx->hp, cudaStreamNonBlocking, hi));
-    FITSNE_CUDA(cudaStreamCreateWithFlags(&ctx->out, cudaStreamNonBlocking));
-    for (cudaEvent_t& e : ctx->ev_piece) FITSNE_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_out, cudaEventDisableTiming));
-  }
+  FITSNE_TRY(out_stream(ctx));
   FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
   FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
   FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_in, 0));

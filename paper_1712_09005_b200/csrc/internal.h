@@ -58,7 +58,8 @@ int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gai
                 double momentum, double lr, cudaStream_t st);
 int nonfinite_count(fitsne_ctx* ctx, const void* x, int64_t count, int* out_host,
                     cudaStream_t st);
-int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st);
+int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st,
+                        void* grad_host = nullptr);
 int combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int64_t n, double alpha,
                  void* out, cudaStream_t st);
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains,
