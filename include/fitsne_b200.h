@@ -110,8 +110,10 @@ enum fitsne_option {
  *   persistent grid of the tiled kernel (default 0 = 11/12 of the SMs when the
  *   repulsion runs concurrently on the side stream, else one CTA per SM).
  *   FITSNE_OPT_HOST_PIECES: fitsne_gradient_host schedule; 0 (default) = copy
- *   in, gradient, copy out; 1 = tiled SpMV in row pieces on a high-priority
- *   stream with each piece's combine + copy-out overlapping later pieces.
+ *   in, gradient with the final combine in point ranges whose copy-out
+ *   overlaps the next range; 1 = tiled SpMV in row pieces on a high-priority
+ *   stream with each piece's combine + copy-out overlapping later pieces;
+ *   2 = copy in, gradient, one copy out.
  *   FITSNE_OPT_FFT_COLS: adjacent columns per block of the column FFT stage
  *   (1 = default, 2, 4; fewer when shared memory does not fit). */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);

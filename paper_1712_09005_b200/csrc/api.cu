@@ -207,7 +207,7 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_HOST_PIECES) {
-    if (value < 0 || value > 1) { set_error("host pieces must be 0 or 1"); return FITSNE_EINVAL; }
+    if (value < 0 || value > 2) { set_error("host schedule must be 0, 1 or 2"); return FITSNE_EINVAL; }
     ctx->host_pieces = value;
     return FITSNE_OK;
   }

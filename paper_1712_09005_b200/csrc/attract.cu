@@ -723,6 +723,12 @@ int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_
   void* y = ctx->hy.ptr;
   unsigned char* g = (unsigned char*)ctx->hg.ptr;
   FITSNE_CUDA(cudaMemcpyAsync(y, Y_host, bytes, cudaMemcpyHostToDevice, st));
+  if (ctx->host_pieces == 2) {  // plain: gradient, then one copy-out
+    FITSNE_TRY(gradient_overlapped(ctx, y, alpha, g, st));
+    FITSNE_CUDA(cudaMemcpyAsync(grad_host, g, bytes, cudaMemcpyDeviceToHost, st));
+    FITSNE_CUDA(cudaStreamSynchronize(st));
+    return FITSNE_OK;
+  }
   if (ctx->host_pieces == 0 || ctx->overlap == 0 || !tiled_usable(ctx, y, st)) {
     // the combine runs in point ranges whose copy-out overlaps the next range
     FITSNE_TRY(gradient_overlapped(ctx, y, alpha, g, st, grad_host));
