@@ -136,7 +136,7 @@ def test_tiled_kl_and_gradient(cuda):
     assert rel_l2(res[2][1], want) <= 1e-3
 
 
-@pytest.mark.parametrize("pieces", [0, 1])
+@pytest.mark.parametrize("pieces", [0, 1, 2])
 @pytest.mark.parametrize("shape", [(128, 512, 5), (64, 256, 0), (2048, 4096, 2)])
 def test_gradient_host_pieces(cuda, shape, pieces):
     """fitsne_gradient_host (pinned host Y in, host gradient out; with pieces
