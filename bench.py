@@ -14,12 +14,16 @@ libfitsne_b200 (sm_100a).
   roofline: the dominant kernel (the CSR SpMV, k_attract) timed alone with
           CUDA events; algorithmic bytes per launch / launch time vs the
           measured HBM copy bandwidth in MEASURED_PEAKS.json.
-  cpu_baseline: the CPU oracle (oracle/fitsne_oracle.py, the reference's
-          numpy/scipy algorithm) on the host cores, rank 0 / N=1 only.
+  cpu_baseline: one whole gradient evaluation of the reference's own CPU
+          path (fftsne.optimizer.gradient from baseline/_ref; the oracle port
+          when that is absent) on the host cores, rank 0 / N=1 only; its
+          result is also the parity check of the timed step ("check").
+  stages: spread / gather against their algorithmic bytes, and the FFT stage
+          beside cuFFT (torch.fft) doing the same transforms.
 
---impl reference runs the reference's CPU implementation (the oracle port of
-the pure-Python reference, which cannot be installed on the box) on the same
-config; under torchrun only rank 0 works.
+--impl reference runs the unmodified reference (baseline/_ref, installed with
+pip --target; numpy/scipy/numba on the host cores) on the same config, one
+whole gradient evaluation per step; under torchrun only rank 0 works.
 
 Multi-GPU (torchrun, N>1): points and CSR rows are sharded by contiguous index
 range; per step each rank spreads its points, the grid is all-reduced (NCCL),
@@ -203,23 +207,52 @@ def traffic_from_profiles(name="spmv"):
 
 
 # ----------------------------------------------------------------------------- CPU leg
-def cpu_gradient_sample(P, Y, min_int=50, p=3):
-    """Reference CPU algorithm (oracle port) for one gradient evaluation.
+def load_reference():
+    """The unmodified reference package (fftsne), installed into baseline/_ref
+    with `pip install --no-index --no-deps --target baseline/_ref` (see
+    DESIGN.md); None when it is not there (the oracle port stands in)."""
+    ref = ROOT / "baseline" / "_ref"
+    if not (ref / "fftsne" / "optimizer.py").exists():
+        return None
+    os.environ.setdefault("NUMBA_CACHE_DIR", "/tmp/numba_cache_fitsne_ref")
+    if str(ref) not in sys.path:
+        sys.path.insert(0, str(ref))
+    try:
+        import fftsne.affinities  # noqa: F401
+        import fftsne.optimizer  # noqa: F401
+        import fftsne
+        return fftsne
+    except Exception as e:  # noqa: BLE001 - report and use the port
+        print(f"reference import failed ({e!r}); using the oracle port", file=sys.stderr)
+        return None
 
-    Sample: the full repulsion (grid, 4 spread/FFT/gather passes) plus the
-    attractive pass over 1/8 of the stored pairs; the attractive time is scaled
-    by 8 (it is linear in the pair count).  Returns seconds per evaluation.
-    """
-    from oracle import fitsne_oracle as O
-    workers = os.cpu_count() or 1
-    t0 = time.perf_counter()
-    O.repulsion(Y, min_int, p, "fft", workers)
-    t_rep = time.perf_counter() - t0
-    m = P.rows.size // 8
-    t0 = time.perf_counter()
-    O.attraction(P.rows[:m], P.cols[:m], P.values[:m], Y)
-    t_att = time.perf_counter() - t0
-    return t_rep + 8.0 * t_att, workers
+
+class CpuGradient:
+    """One full gradient evaluation of the reference's CPU path on (P, Y64):
+    fftsne.optimizer.gradient(P, Y, 1.0, 50, 3, "fft", workers=cpu_count)
+    (optimizer.py:248-262) -- or, without baseline/_ref, the oracle port's
+    O.grad.  No sampling: every call is a whole evaluation."""
+
+    def __init__(self, P):
+        self.workers = os.cpu_count() or 1
+        self.ref = load_reference()
+        if self.ref is not None:
+            self.kind = "reference"
+            self.P = self.ref.affinities.SparseAffinities(int(P.n), P.rows, P.cols, P.values)
+            self.api = "fftsne.optimizer.gradient(P, Y, 1.0, 50, 3, 'fft', workers=cpu_count) from baseline/_ref"
+        else:
+            self.kind = "port"
+            self.P = P
+            self.api = "oracle.fitsne_oracle.grad (numpy/scipy port of the reference)"
+
+    def __call__(self, Y64):
+        t0 = time.perf_counter()
+        if self.ref is not None:
+            g = self.ref.optimizer.gradient(self.P, Y64, 1.0, 50, 3, "fft", workers=self.workers)
+        else:
+            from oracle import fitsne_oracle as O
+            g = O.grad(self.P.rows, self.P.cols, self.P.values, Y64, 1.0, 50, 3, "fft", self.workers)
+        return time.perf_counter() - t0, g
 
 
 def run_reference(args):
@@ -229,14 +262,14 @@ def run_reference(args):
         return
     dev = "cuda" if torch.cuda.is_available() else "cpu"
     P, Y, t_gen = make_inputs(args, dev)
+    Y64 = Y.astype(np.float32).astype(np.float64)  # the values the f32 GPU arm sees
+    cpu = CpuGradient(P)
     for _ in range(args.warmup):
-        cpu_gradient_sample(P, Y)
-    times = []
-    workers = 1
+        cpu(Y64)
+    t0 = time.perf_counter()
     for _ in range(args.steps):
-        t, workers = cpu_gradient_sample(P, Y)
-        times.append(t)
-    sec = float(np.mean(times))
+        cpu(Y64)
+    sec = (time.perf_counter() - t0) / args.steps
     val = 1.0 / sec
     line = {
         "impl": "reference",
@@ -244,15 +277,31 @@ def run_reference(args):
         "value": val, "unit": "grad_evals/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS["c3"]["desc"], "N": int(P.n),
-                   "nnz_full": int(2 * P.rows.size)},
-        "cpu_baseline": {"value": val, "unit": "grad_evals/s", "cores": workers, "kind": "port",
-                         "sample": "per step: full FFT repulsion (scipy.fft workers=cpu_count) + "
-                                   "attractive bincount pass over 1/8 of the stored pairs, x8"},
+        "config": workload_config(P),
+        "cpu_baseline": {"value": val, "unit": "grad_evals/s", "cores": cpu.workers,
+                         "kind": cpu.kind, "cpu_model": cpu_model(),
+                         "sample": "none: every step is one whole gradient evaluation, " + cpu.api},
         "e2e": {"value": val, "unit": "grad_evals/s", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def cpu_model():
+    try:
+        for ln in Path("/proc/cpuinfo").read_text().splitlines():
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
+def workload_config(P, **extra):
+    cfg = {"workload": WORKLOADS["c3"]["desc"], "N": int(P.n), "nnz_full": int(2 * P.rows.size),
+           "min_intervals": 50, "points_per_interval": 3, "alpha": 1.0}
+    cfg.update(extra)
+    return cfg
 
 
 # ----------------------------------------------------------------------------- ours
@@ -283,8 +332,8 @@ def count_launches(fn):
         evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
                and not e.name.startswith("Memcpy") and not e.name.startswith("Memset")]
         return len(evs)
-    except Exception:  # noqa: BLE001 - profiler unavailable: report the static count
-        return 9
+    except Exception:  # noqa: BLE001 - profiler unavailable: no count (never a guess)
+        return None
 
 
 def timed(fn, steps, stream):
@@ -372,8 +421,8 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dt == torch.float32 else "f64",
                 "data": "synthetic",
-                "config": {"workload": WORKLOADS["c3"]["desc"], "N": n, "parallelism": f"points{world}",
-                           "l2": "inputs larger than L2 (CSR > 126 MB)"},
+                "config": workload_config(P, parallelism=f"points{world}",
+                                          l2="inputs larger than L2 (CSR > 126 MB)"),
                 "roofline": {"kernel": "rank 0's local-row attractive SpMV (fitsne_attractive)",
                              "bound": "hbm", "achieved": b_spmv / (ms_spmv * 1e-3) / 1e9,
                              "peak": peak, "unit": "GB/s",
@@ -386,7 +435,7 @@ def run_ours(args):
                                "from pinned host memory and its gradient rows copied out",
                         "h2d_bytes_per_step": int(yh.numel() * yh.element_size()) * world,
                         "d2h_bytes_per_step": int(gh.numel() * gh.element_size()) * world},
-                "gpu_launches": launches * args.steps,
+                "gpu_launches": launches * args.steps if launches is not None else None,
                 "gpu_launches_per_step": launches,
                 "clocks": clk.summary(),
             }
@@ -503,38 +552,56 @@ def run_ours(args):
     stages["gather"]["bound"] = "9 random 16-B node reads per point from the L2-resident potentials"
 
 
+    # FFT stage against cuFFT (the north star's timing reference): the same
+    # five L x L transforms through torch.fft (cuFFT), and an R2C/C2R variant
+    stages["fft_conv"] = {"ms": breakdown["fft_conv"],
+                          "kernels": "k_rows_forward + k_spec_cols + k_cols + k_rows_inverse"}
+    stages["fft_conv"]["cufft"] = cufft_reference(int(gr.nodes_per_dim), int(gr.fft_len), dt,
+                                                  args.steps, stream)
+
+    # CPU baseline: one whole evaluation of the reference's CPU gradient on the
+    # same (P, Y) -- and the parity check of this run's gradient against it
     cpu = None
+    check = None
     if not args.no_cpu_baseline and rank == 0:
         Y64 = y.double().cpu().numpy()
-        sec, workers = cpu_gradient_sample(P, Y64)
-        cpu = {"value": 1.0 / sec, "unit": "grad_evals/s", "cores": workers, "kind": "port",
-               "sample": "one evaluation: full FFT repulsion (scipy.fft workers=cpu_count) + "
-                         "attractive bincount over 1/8 of the stored pairs, x8 (numpy: 1 thread)"}
+        ref = CpuGradient(P)
+        sec, g_ref = ref(Y64)
+        cpu = {"value": 1.0 / sec, "unit": "grad_evals/s", "cores": ref.workers, "kind": ref.kind,
+               "cpu_model": cpu_model(),
+               "sample": "one whole gradient evaluation on the same (P, Y): " + ref.api}
+        step()
+        torch.cuda.synchronize()
+        g_ours = g.double().cpu().numpy()
+        err = float(np.linalg.norm(g_ours - g_ref) / np.linalg.norm(g_ref))
+        bar = 1e-3 if dt == torch.float32 else 1e-5
+        check = {"vs": ref.api, "rel_l2": err, "bar": bar, "ok": err <= bar,
+                 "path": "the timed step (fitsne_gradient, production schedule)"}
 
     line = {
         "metric": "t-SNE gradient evals/sec at N=1.3M 2-D",
         "value": 1e3 / ms, "unit": "grad_evals/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if dt == torch.float32 else "f64", "data": "synthetic",
-        "config": {"workload": WORKLOADS["c3"]["desc"], "N": n, "nnz_full": nnz,
-                   "n_intervals": int(gr.n_intervals), "nodes_per_dim": int(gr.nodes_per_dim),
-                   "fft_len": int(gr.fft_len), "parallelism": "single",
-                   "l2": "inputs larger than L2 (CSR %.2f GB > 126 MB L2), no flush" %
-                         (nnz * (4 + es) / 1e9),
-                   "input_gen_s": round(t_gen, 1)},
+        "config": workload_config(
+            P, n_intervals=int(gr.n_intervals), nodes_per_dim=int(gr.nodes_per_dim),
+            fft_len=int(gr.fft_len), parallelism="single",
+            l2="inputs larger than L2 (CSR %.2f GB > 126 MB L2), no flush" % (nnz * (4 + es) / 1e9),
+            input_gen_s=round(t_gen, 1)),
         "roofline": {"kernel": spmv_kernel, "bound": "hbm",
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src, "algorithmic_bytes": b_spmv,
                      "launch_ms": ms_spmv, "share_of_step": ms_spmv / ms,
                      "traffic": traffic_from_profiles(traffic_key)},
         "cpu_baseline": cpu,
+        "check": check,
         "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
                 "api": "optimizer.gradient(P, Y_pinned_host, out=pinned_host) -> fitsne_gradient_host",
                 "timing": "median of 3 runs of K steps (max of CUDA-event and wall time per run); "
                           "host thread and pinned buffers on the GPU's NUMA-local cores",
                 "h2d_bytes_per_step": int(y_host.numel() * y_host.element_size()),
                 "d2h_bytes_per_step": int(y_host.numel() * y_host.element_size())},
-        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches": launches_per_step * args.steps if launches_per_step is not None else None,
         "gpu_launches_per_step": launches_per_step,
         "clocks": clocks,
     }
@@ -567,6 +634,46 @@ def full_run(P, dt, dev, n_iter=1000, reorder=True):
             "final_span": [float(s) for s in span],
             "reorder": bool(reorder),
             "note": "wall clock of run_tsne incl. one bbox readback per iteration"}
+
+
+def cufft_reference(n, L, dt, steps, stream):
+    """cuFFT (through torch.fft) doing the FFT work of one evaluation's
+    convolution stage at the same L: one spectrum transform of the packed
+    kernels (K1 + i K2), two forward transforms of the packed charge pairs,
+    two inverse transforms -- five L x L C2C transforms on pre-padded inputs
+    (transform time only).  R2C/C2R variant: two real kernel spectra, three
+    real charge channels forward, three potentials back."""
+    import torch
+    cd = torch.complex64 if dt == torch.float32 else torch.complex128
+    rd = torch.float32 if dt == torch.float32 else torch.float64
+    g = torch.Generator(device="cuda").manual_seed(0)
+    kern = torch.randn(L, L, dtype=cd, device="cuda", generator=g)
+    w = torch.zeros(2, L, L, dtype=cd, device="cuda")
+    w[:, :n, :n] = torch.randn(2, n, n, dtype=cd, device="cuda", generator=g)
+    kr = torch.randn(2, L, L, dtype=rd, device="cuda", generator=g)
+    wr = torch.zeros(3, L, L, dtype=rd, device="cuda")
+    wr[:, :n, :n] = torch.randn(3, n, n, dtype=rd, device="cuda", generator=g)
+    out = {}
+
+    def c2c():
+        kh = torch.fft.fft2(kern)
+        W = torch.fft.fft2(w)
+        torch.fft.ifft2(W)
+        return kh
+
+    def r2c():
+        kh = torch.fft.rfft2(kr)
+        W = torch.fft.rfft2(wr)
+        torch.fft.irfft2(W, s=(L, L))
+        return kh
+
+    for name, fn in (("c2c_5_transforms_ms", c2c), ("r2c_c2r_8_transforms_ms", r2c)):
+        for _ in range(3):
+            fn()
+        out[name] = timed(fn, steps, stream)
+    out["L"] = L
+    out["note"] = "torch.fft (cuFFT) on pre-padded L x L inputs; transform time only"
+    return out
 
 
 def stage_breakdown(ctx, y, n, dt, steps, stream):

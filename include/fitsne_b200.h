@@ -21,7 +21,7 @@
  *     fitsne_make_grid (the FFT length depends on the data, nbody.py:134).
  *   - Return value: FITSNE_OK or an error code; fitsne_last_error() gives a
  *     thread-local message.  The Python layer maps FITSNE_EINVAL/FITSNE_EOUTSIDE/
- *     FITSNE_EZ to ValueError and FITSNE_ENONFINITE to FloatingPointError,
+ *     FITSNE_EZ/FITSNE_EPOINTS to ValueError and FITSNE_ENONFINITE to FloatingPointError,
  *     exactly as the reference raises (optimizer.py:242-243, 310-313;
  *     nbody.py:127-128, 210-211).
  */
@@ -44,7 +44,10 @@ enum fitsne_status {
   FITSNE_ECUDA = 4,       /* CUDA runtime error */
   FITSNE_ENOMEM = 5,      /* device allocation failed */
   FITSNE_EOUTSIDE = 6,    /* point outside grid bounds -> ValueError (nbody.py:210) */
-  FITSNE_ETOOBIG = 7      /* grid larger than the FFT kernels support */
+  FITSNE_ETOOBIG = 7,     /* grid larger than the FFT kernels support */
+  FITSNE_EPOINTS = 8      /* non-finite point met while building the grid -> ValueError
+                             ("points must be finite", nbody.py:127-128); the fused
+                             iteration reports it for a diverged embedding */
 };
 
 enum fitsne_dtype { FITSNE_F32 = 0, FITSNE_F64 = 1 };

@@ -7,6 +7,8 @@ the device; CUDA tensors are used in place and results stay on the device).
 
 from __future__ import annotations
 
+import threading
+
 import numpy as np
 import torch
 
@@ -103,11 +105,13 @@ _pinned: dict = {}
 
 
 def _pinned_buffer(shape, dtype, tag="in"):
-    """Reusable pinned staging buffer (cudaHostAlloc is far too slow per call)."""
+    """Reusable pinned staging buffer (cudaHostAlloc is far too slow per call).
+    Keyed per thread like the library contexts (_lib.context), so concurrent
+    callers never share a staging buffer."""
     n = 1
     for s in shape:
         n *= int(s)
-    key = (tag, dtype)
+    key = (tag, dtype, threading.get_ident())
     buf = _pinned.get(key)
     if buf is None or buf.numel() < n:
         buf = torch.empty(max(n, 1), dtype=dtype, pin_memory=True)

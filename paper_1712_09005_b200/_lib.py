@@ -11,6 +11,7 @@ from __future__ import annotations
 import ctypes as C
 import os
 import threading
+import weakref
 from pathlib import Path
 
 import torch
@@ -19,7 +20,7 @@ _PKG = Path(__file__).resolve().parent
 # FITSNE_LIB selects another in-tree build of the library (A/B experiments)
 LIB_PATH = _PKG / os.environ.get("FITSNE_LIB", "libfitsne_b200.so")
 
-OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG = range(8)
+OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG, EPOINTS = range(9)
 F32, F64 = 0, 1
 CAUCHY, CAUCHY_SQUARED = 0, 1
 
@@ -124,7 +125,7 @@ def check(rc: int, what: str = "") -> None:
     if rc == OK:
         return
     msg = last_error() or what
-    if rc in (EINVAL, EOUTSIDE, EZ, ETOOBIG):
+    if rc in (EINVAL, EOUTSIDE, EZ, ETOOBIG, EPOINTS):
         raise ValueError(msg)
     if rc == ENONFINITE:
         raise FloatingPointError(msg)
@@ -168,7 +169,7 @@ class Context:
             check(self.lib.fitsne_create(C.byref(h), device, dims, self.code, p, min_intervals,
                                          self.ipi), "fitsne_create")
         self.h = h
-        self._P_refs = None
+        self._P_ref = None  # weak reference to the registered DeviceCSR
 
     def __del__(self):
         try:
@@ -184,15 +185,26 @@ class Context:
 
     def set_affinities(self, csr):
         """Register a DeviceCSR with this context (no-op if it is already the
-        registered one; the context keeps a strong reference, so identity
-        cannot be confused with a freed object)."""
-        if csr is self._P_refs:
+        registered one).  The context holds the CSR weakly: when the caller's
+        P (which owns the cached CSR) goes away, the library is told to forget
+        the device pointers and frees its tiled copy of P."""
+        cur = self._P_ref() if self._P_ref is not None else None
+        if csr is cur:
             return
         check(self.lib.fitsne_set_affinities(self.h, ptr(csr.rowptr), ptr(csr.col), ptr(csr.val),
                                              csr.n_rows, csr.row_begin, csr.n_total,
                                              csr.col.numel()),
               "fitsne_set_affinities")
-        self._P_refs = csr  # keep the device arrays alive while registered
+        self._P_ref = weakref.ref(csr, self._released)
+
+    def _released(self, wr):
+        if self._P_ref is wr and getattr(self, "h", None) and _lib is not None:
+            self._P_ref = None
+            try:
+                with torch.cuda.device(self.device):
+                    _lib.fitsne_set_affinities(self.h, None, None, None, 0, 0, 0, 0)
+            except Exception:  # noqa: BLE001 - interpreter shutdown
+                pass
 
 
 _contexts: dict = {}

@@ -78,6 +78,13 @@ def _coo_full(P, device):
     """(rows, cols, vals) of the full symmetric matrix on the device."""
     if hasattr(P, "rows") and hasattr(P, "cols") and hasattr(P, "values"):
         n = int(P.n)
+        if isinstance(P.rows, torch.Tensor):
+            # device-resident upper COO (e.g. a P built on the GPU, too large
+            # to round-trip through host memory)
+            r = P.rows.to(device=device, dtype=torch.int64)
+            c = P.cols.to(device=device, dtype=torch.int64)
+            v = P.values.to(device=device, dtype=torch.float64)
+            return n, torch.cat([r, c]), torch.cat([c, r]), torch.cat([v, v])
         r = torch.as_tensor(np.asarray(P.rows, dtype=np.int64)).to(device)
         c = torch.as_tensor(np.asarray(P.cols, dtype=np.int64)).to(device)
         v = torch.as_tensor(np.asarray(P.values, dtype=np.float64)).to(device)
@@ -134,10 +141,35 @@ def _cache_slot(P):
         return slot
 
 
+def _addr(a):
+    if isinstance(a, torch.Tensor):
+        return int(a.data_ptr())
+    try:
+        return int(np.asarray(a).__array_interface__["data"][0])
+    except Exception:  # noqa: BLE001 - not a numpy-compatible buffer
+        return id(a)
+
+
+def _sample_sum(a):
+    """Checksum of ~1024 evenly spaced entries (cheap: called on every use)."""
+    if isinstance(a, torch.Tensor):
+        return float(a[:: max(1, a.numel() // 1024)].double().sum().item()) if a.numel() else 0.0
+    a = np.asarray(a)
+    if a.size == 0:
+        return 0.0
+    return float(a[:: max(1, a.size // 1024)].sum())
+
+
 def _fingerprint(P):
+    """Identity of P's contents for the device cache.  P is treated as
+    immutable (as the reference's pure functions read it afresh on every
+    call): replaced arrays are seen through their buffers, and in-place edits
+    through a sampled checksum of the values (edits that miss every sampled
+    entry are not detected)."""
     if hasattr(P, "rows"):
-        return (int(P.n), len(P.rows), id(P.rows), id(P.cols), id(P.values))
-    return (P.shape, P.nnz, id(P))
+        return (int(P.n), len(P.rows), _addr(P.rows), _addr(P.cols), _addr(P.values),
+                _sample_sum(P.values), _sample_sum(P.cols))
+    return (P.shape, P.nnz, id(P), _sample_sum(getattr(P, "data", np.zeros(0))))
 
 
 def device_csr(P, dtype: torch.dtype, device: int, row_begin: int = 0, row_end=None) -> DeviceCSR:

@@ -45,15 +45,34 @@ def stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
+def _compile(src: str, obj: Path) -> tuple[int, str]:
+    flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+    cmd = [nvcc(), *flags, "-c", "-o", str(obj), str(CSRC / src)]
+    res = subprocess.run(cmd, capture_output=True, text=True)
+    return res.returncode, f"== {src}\n" + (res.stdout or "") + (res.stderr or "")
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     if not force and not stale():
         return LIB
+    # one nvcc per translation unit, in parallel, then one link
+    import tempfile
+    from concurrent.futures import ThreadPoolExecutor
     tmp = LIB.with_suffix(".so.tmp")
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", str(tmp), *[str(CSRC / s) for s in SOURCES]]
-    res = subprocess.run(cmd, capture_output=True, text=True)
-    log = (res.stdout or "") + (res.stderr or "")
+    with tempfile.TemporaryDirectory(prefix="fitsne_build_") as td:
+        objs = [Path(td) / (Path(s).stem + ".o") for s in SOURCES]
+        with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
+            results = list(ex.map(_compile, SOURCES, objs))
+        log = "".join(r[1] for r in results)
+        rc = max(r[0] for r in results)
+        if rc == 0:
+            cmd = [nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-cudart", "static",
+                   "-o", str(tmp), *[str(o) for o in objs]]
+            res = subprocess.run(cmd, capture_output=True, text=True)
+            log += "== link\n" + (res.stdout or "") + (res.stderr or "")
+            rc = res.returncode
     (PKG / "build.log").write_text(log)
-    if res.returncode != 0:
+    if rc != 0:
         sys.stderr.write(log)
         raise RuntimeError("nvcc failed building libfitsne_b200.so (see build.log)")
     if verbose:

@@ -608,7 +608,15 @@ static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void*
   else { if (g.p == 3) CMB(2, 3); else CMB(2, 0); }
 #undef CMB
   FITSNE_CHECK_LAUNCH();
+  if (clear) tiled_consumed(ctx);
   return FITSNE_OK;
+}
+
+int join_on_error(fitsne_ctx* ctx, int rc) {
+  if (rc == FITSNE_OK) return rc;
+  for (cudaStream_t s : {ctx->side, ctx->hp, ctx->out})
+    if (s) cudaStreamSynchronize(s);
+  return rc;
 }
 
 // Attractive SpMV feeding the combine kernel: the tiled kernel when it applies
@@ -646,8 +654,16 @@ static int out_stream(fitsne_ctx* ctx) {
   return FITSNE_OK;
 }
 
+static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha, void* grad,
+                                    cudaStream_t st, void* grad_host);
+
 int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad, cudaStream_t st,
                         void* grad_host) {
+  return join_on_error(ctx, gradient_overlapped_impl(ctx, Y, alpha, grad, st, grad_host));
+}
+
+static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha, void* grad,
+                                    cudaStream_t st, void* grad_host) {
   const int64_t n = ctx->n_total;
   void* attr = nullptr;
   bool clear = false;
@@ -714,7 +730,15 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
 // copy-out stream the combine of piece k (F_rep gather + 4 (alpha F_attr -
 // F_rep)) and its device-to-host copy start as soon as SpMV piece k is done,
 // so the gradient leaves the device while the later pieces still run.
+static int gradient_host_impl(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host,
+                              cudaStream_t st);
+
 int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host, cudaStream_t st) {
+  return join_on_error(ctx, gradient_host_impl(ctx, Y_host, alpha, grad_host, st));
+}
+
+static int gradient_host_impl(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host,
+                              cudaStream_t st) {
   const int64_t n = ctx->n_total;
   const size_t row_bytes = dsize(ctx->dtype) * (size_t)ctx->dims;
   const size_t bytes = row_bytes * (size_t)n;
@@ -794,8 +818,19 @@ int combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int64_t n,
   return FITSNE_OK;
 }
 
+static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains,
+                              double alpha, double momentum, double lr, double* kl_dev,
+                              int32_t* status_dev, cudaStream_t st);
+
 int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains, double alpha,
                   double momentum, double lr, double* kl_dev, int32_t* status_dev, cudaStream_t st) {
+  return join_on_error(ctx, iterate_fused_impl(ctx, Yin, Yout, vel, gains, alpha, momentum, lr, kl_dev,
+                                               status_dev, st));
+}
+
+static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains,
+                              double alpha, double momentum, double lr, double* kl_dev,
+                              int32_t* status_dev, cudaStream_t st) {
   const int64_t n = ctx->n_total;
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
   void* attr = nullptr;

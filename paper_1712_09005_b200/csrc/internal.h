@@ -77,6 +77,11 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 // out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
 int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st);
 void free_tiled(fitsne_ctx* ctx);
+// the tiled F_attr buffer's consumer (which clears it) has been queued
+void tiled_consumed(fitsne_ctx* ctx);
+// error exit of a multi-stream schedule: wait for the internal streams so no
+// queued work outlives the call (the next call reuses their buffers)
+int join_on_error(fitsne_ctx* ctx, int rc);
 // band spread (bandspread.cu): fp32, 2-D, p = 3, n_int <= 1024
 bool band_spread_applies(const fitsne_ctx* ctx, int64_t n);
 int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);

@@ -173,7 +173,7 @@ int bbox_wait(fitsne_ctx* ctx, double* bbox_host) {
   FITSNE_CUDA(cudaEventSynchronize(ctx->ev_bbox));
   if (ctx->h_scal[8 + 2 * S] != 0.0) {
     set_error("points must be finite");
-    return FITSNE_ENONFINITE;
+    return FITSNE_EPOINTS;
   }
   for (int d = 0; d < 2 * S; ++d) bbox_host[d] = ctx->h_scal[8 + d];
   return FITSNE_OK;
@@ -205,7 +205,7 @@ int grid_from_bbox(fitsne_ctx* ctx, const double* bbox, fitsne_grid* out) {
     hi[d] = bbox[S + d];
     if (!std::isfinite(lo[d]) || !std::isfinite(hi[d])) {
       set_error("points must be finite");
-      return FITSNE_ENONFINITE;
+      return FITSNE_EPOINTS;
     }
     span[d] = hi[d] - lo[d];
     widest = std::max(widest, span[d]);
@@ -510,6 +510,20 @@ __global__ void k_point_interp(const T* __restrict__ Y, int64_t n, GridArgs g,
   PointInterp<T, S> pi;
   double y[S];
   interp_point<T, S>(Y, i, g, pi, y);
+  if constexpr (sizeof(T) == 4) {
+    // fp32, p = 3: the node indices come from the guarded fp32 box estimate
+    // that the production spread / gather / combine kernels use
+    // (box_weights3_f32), so the bit-exactness checks of this entry point
+    // cover the production cells; the weights stay the exact fp64 ones
+    if (g.p == 3) {
+#pragma unroll
+      for (int d = 0; d < S; ++d) {
+        float wf[3];
+        pi.cell[d] = box_weights3_f32((float)Y[i * S + d], g.lo[d], g.h[d], g.lo_f[d], g.invh_f[d],
+                                      g.guard[d], g.n_int, wf);
+      }
+    }
+  }
   const int p = g.p;
   const int64_t nn = g.n;
   const int cnt = (S == 1) ? p : p * p;

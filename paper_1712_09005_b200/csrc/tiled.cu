@@ -26,6 +26,8 @@
 
 #include <algorithm>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -89,6 +91,11 @@ struct TiledP {
   const void* val = nullptr;
   int64_t n_rows = 0, row_begin = 0, n_total = 0, nnz = 0;
   bool failed = false;  // build impossible for this CSR (size limits / memory)
+  // fattr holds forces of a pass whose consumer (combine / finish kernel, which
+  // clears it) was never queued -- an error between the SpMV and its consumer.
+  // The next pass clears it first (after the stream that ran the stale pass).
+  bool dirty = false;
+  cudaStream_t dirty_stream = nullptr;
 };
 
 static void release_buf(DevBuf& b) {
@@ -1009,15 +1016,20 @@ static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* 
   TiledP* T = ctx->tiled;
   const size_t smem = tiled_smem(T->R, T->C, T->hdr_max);
   const int stage_sz = (int)stage_bytes(T->C, T->hdr_max);
-  static thread_local int configured_dev = -1;
-  static thread_local size_t configured_smem = 0;
-  if (configured_dev != ctx->device || configured_smem < smem) {
-    FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)smem));
-    configured_dev = ctx->device;
-    configured_smem = smem;
+  {
+    // the attribute is per device and process-wide: cache what was set per
+    // device under a lock (raise only; a smaller request fits a larger limit)
+    static std::mutex mu;
+    static std::map<int, size_t> configured;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = configured[ctx->device];
+    if (have < smem) {
+      FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+      FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       (int)smem));
+      have = smem;
+    }
   }
   double* part = (double*)T->part.ptr;
 #define TILED_ARGS                                                                                  \
@@ -1033,10 +1045,29 @@ static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* 
   return FITSNE_OK;
 }
 
+// Start of an SpMV pass over fattr: clear a stale accumulation first (see
+// TiledP::dirty), then mark the buffer as owned by this pass until
+// tiled_consumed().
+static int tiled_begin(fitsne_ctx* ctx, cudaStream_t st) {
+  TiledP* T = ctx->tiled;
+  if (T->dirty) {
+    if (T->dirty_stream != st) cudaStreamSynchronize(T->dirty_stream);
+    FITSNE_CUDA(cudaMemsetAsync(T->fattr.ptr, 0, sizeof(float) * 2 * (size_t)ctx->n_rows, st));
+  }
+  T->dirty = true;
+  T->dirty_stream = st;
+  return FITSNE_OK;
+}
+
+void tiled_consumed(fitsne_ctx* ctx) {
+  if (ctx->tiled) ctx->tiled->dirty = false;
+}
+
 int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** fattr_out,
                   double** part_out, int* nparts) {
   TiledP* T = ctx->tiled;
   double* part = (double*)T->part.ptr;
+  FITSNE_TRY(tiled_begin(ctx, st));
   FITSNE_TRY(launch_tiled(ctx, Y, kl, (const int32_t*)T->sched.ptr, st));
   *fattr_out = T->fattr.ptr;
   if (part_out) *part_out = part;
@@ -1046,6 +1077,7 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 
 int attract_tiled_piece(fitsne_ctx* ctx, const void* Y, int piece, cudaStream_t st, void** fattr_out) {
   TiledP* T = ctx->tiled;
+  if (piece == 0) FITSNE_TRY(tiled_begin(ctx, st));
   FITSNE_TRY(launch_tiled(ctx, Y, false, (const int32_t*)T->psched.ptr + (size_t)piece * (T->grid + 1),
                           st));
   *fattr_out = T->fattr.ptr;
@@ -1074,6 +1106,7 @@ int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void
   k_tiled_finish<<<nb(n, 256), 256, 0, st>>>((float2*)T->fattr.ptr, n, (const float2*)frep, (float)alpha,
                                              mode, (float2*)out);
   FITSNE_CHECK_LAUNCH();
+  tiled_consumed(ctx);
   return FITSNE_OK;
 }
 

@@ -162,7 +162,7 @@ def make_grid(points, min_intervals: int = 20, points_per_interval: int = 3, *,
                        intervals_per_integer)
     g = _lib.Grid()
     rc = ctx.lib.fitsne_make_grid(ctx.h, _lib.ptr(y), y.shape[0], C.byref(g), ctx.stream)
-    if rc == _lib.ENONFINITE:
+    if rc in (_lib.ENONFINITE, _lib.EPOINTS):
         raise ValueError("points must be finite")
     _lib.check(rc, "fitsne_make_grid")
     return _grid_from_c(g)
@@ -284,7 +284,7 @@ def evaluate_nbody(points, charges, kernel, min_intervals: int = 20, points_per_
     out = torch.empty_like(q)
     rc = ctx.lib.fitsne_evaluate_nbody(ctx.h, _lib.ptr(y), n, _lib.ptr(q), q.shape[1], code,
                                        1 if include_self else 0, _lib.ptr(out), ctx.stream)
-    if rc == _lib.ENONFINITE:
+    if rc in (_lib.ENONFINITE, _lib.EPOINTS):
         raise ValueError("points must be finite")
     _lib.check(rc, "fitsne_evaluate_nbody")
     out = out[:, 0] if single else out

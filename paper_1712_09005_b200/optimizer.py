@@ -200,7 +200,8 @@ def _resolve_method(method, n, limit=EXACT_REPULSION_MAX_N):
     return method
 
 
-def _repulsion_device(y, dev, dt, min_intervals, points_per_interval, method, ipi=1.0):
+def _repulsion_device(y, dev, dt, min_intervals, points_per_interval, method, ipi=1.0,
+                      check_z=True):
     n, s = y.shape
     ctx = _lib.context(dev, s, dt, points_per_interval, min_intervals, ipi)
     forces = torch.empty_like(y)
@@ -208,8 +209,10 @@ def _repulsion_device(y, dev, dt, min_intervals, points_per_interval, method, ip
     k2 = torch.empty((n, s + 1), dtype=dt, device=dev)
     z = C.c_double()
     fn = ctx.lib.fitsne_repulsive if method == "fft" else ctx.lib.fitsne_repulsive_exact
-    _lib.check(fn(ctx.h, _lib.ptr(y), n, _lib.ptr(forces), C.byref(z), _lib.ptr(k1), _lib.ptr(k2),
-                  ctx.stream), "fitsne_repulsive")
+    rc = fn(ctx.h, _lib.ptr(y), n, _lib.ptr(forces), C.byref(z), _lib.ptr(k1), _lib.ptr(k2),
+            ctx.stream)
+    if not (rc == _lib.EZ and not check_z):
+        _lib.check(rc, "fitsne_repulsive")
     return forces, float(z.value), k1, k2
 
 
@@ -317,7 +320,10 @@ def kl_divergence(P, Y, method: str = "auto", *, dtype=None) -> float:
         y = y.reshape(-1, 1)
     # Z: exact O(N^2) sum, or the grid's unit-charge Cauchy sum with the
     # reference's evaluate_nbody defaults (min_intervals 20, p 3)
-    _, z, _, _ = _repulsion_device(y, dev, dt, 20, 3, "exact" if method == "exact" else "fft")
+    # (the reference checks neither Z's sign nor its finiteness here: a
+    # non-finite exact Z gives a NaN KL, optimizer.py:289-296)
+    _, z, _, _ = _repulsion_device(y, dev, dt, 20, 3, "exact" if method == "exact" else "fft",
+                                   check_z=False)
     ctx, _ = _ctx_with_P(P, dev, y.shape[1], dt)
     return _kl_device(ctx, y, z)
 
@@ -453,7 +459,7 @@ def _run_fused(P, y0, cfg, dev, dt) -> TsneResult:
                 ctx.h, _lib.ptr(ya), _lib.ptr(yb), _lib.ptr(vel), _lib.ptr(gains), float(alpha),
                 float(mom), float(cfg.learning_rate), C.c_void_p(kl.data_ptr() + 8 * it),
                 C.c_void_p(status.data_ptr() + 4 * it), st)
-            if rc == _lib.ENONFINITE:
+            if rc in (_lib.ENONFINITE, _lib.EPOINTS):
                 _raise_status(status, it)
             _lib.check(rc, "fitsne_iterate")
             ya, yb = yb, ya

@@ -50,6 +50,22 @@ def test_c1_affinities_match_reference_structure(c1):
     assert abs(P.values.sum() - float(ref["p_sum"][0])) <= 1e-12
 
 
+def test_c1_affinities_identical_to_reference(c1):
+    """The GPU-built P is the reference's P: the same (row, col) pattern
+    (SHA-256 of the sorted pairs) and the same per-point mass to 1e-9
+    (fingerprint of the reference's affinities_from_data,
+    tests/golden/make_c1_pcheck.py), so both full runs start from one input."""
+    import hashlib
+    P, _ = c1
+    with np.load(Path(__file__).resolve().parent / "golden" / "c1_pcheck.npz") as z:
+        sha, rs_ref = str(z["pattern_sha256"][0]), z["row_sums"]
+    key = np.sort(P.rows.astype(np.int64) * P.n + P.cols.astype(np.int64))
+    assert hashlib.sha256(key.tobytes()).hexdigest() == sha
+    rs = np.bincount(P.rows, weights=P.values, minlength=P.n) + np.bincount(P.cols, weights=P.values,
+                                                                           minlength=P.n)
+    assert np.max(np.abs(rs - rs_ref) / rs_ref) <= 1e-9
+
+
 @pytest.mark.parametrize("dtype,early_tol", [("float64", 1e-6), ("float32", 1e-3)])
 def test_c1_full_run_final_kl_within_1pct(c1, dtype, early_tol):
     P, ref = c1
