@@ -99,7 +99,9 @@ enum fitsne_option {
   FITSNE_OPT_TILED_CTAS = 8,
   FITSNE_OPT_TILED_BANK_ORDER = 9,
   FITSNE_OPT_HOST_PIECES = 10,
-  FITSNE_OPT_FFT_COLS = 11
+  FITSNE_OPT_FFT_COLS = 11,
+  FITSNE_OPT_FFT_PATH = 12,
+  FITSNE_OPT_GRID_F64 = 13
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -118,7 +120,16 @@ enum fitsne_option {
  *   stream with each piece's combine + copy-out overlapping later pieces;
  *   2 = copy in, gradient, one copy out.
  *   FITSNE_OPT_FFT_COLS: adjacent columns per block of the column FFT stage
- *   (1 = default, 2, 4; fewer when shared memory does not fit). */
+ *   (1 = default, 2, 4; fewer when shared memory does not fit).
+ *   FITSNE_OPT_FFT_PATH: 0 (default) = one-block-per-transform kernels while
+ *   the transform fits shared memory (L <= 5184 fp32 / 2592 fp64), the
+ *   four-step path (L = L1 L2, two shared-memory passes per axis through HBM)
+ *   beyond; 1 = shared-memory kernels only; 2 = four-step always.
+ *   FITSNE_OPT_GRID_F64 (fp32 contexts): 0 = fp32 grid pipeline; 1 (default)
+ *   = spread accumulation, FFT stage, potentials and F_rep in fp64 when the
+ *   embedding's widest span exceeds 256 (fp32's repulsive force loses
+ *   accuracy with the span: F = y K2*1 - K2*y cancels |y|-sized terms); 2 =
+ *   always.  Points, the attractive SpMV and the gradient stay fp32. */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
  * only for its alignment): out[0..5] = {in use (0/1), tiles, slabs, slot
@@ -227,6 +238,9 @@ int fitsne_exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* ch
  * 4 slots per node in the context dtype, fitsne_grid_accum_len() elements, and
  * must be zero before the first spread (it is cleared again by fitsne_fft_tsne). */
 int64_t fitsne_grid_accum_len(fitsne_ctx* ctx);
+/* dtype (FITSNE_F32 / FITSNE_F64) of that accumulator for the current grid:
+ * FITSNE_F64 when an fp32 context runs the grid in fp64 (FITSNE_OPT_GRID_F64). */
+int fitsne_grid_accum_dtype(fitsne_ctx* ctx);
 int fitsne_spread_tsne(fitsne_ctx* ctx, const void* Y_local, int64_t n_local, void* accum,
                        void* stream);
 int fitsne_fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, int with_k1,
@@ -241,6 +255,10 @@ int fitsne_gradient_rows(fitsne_ctx* ctx, const void* Y_full, const void* forces
  * were computed separately. */
 int fitsne_combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int64_t n, double alpha,
                         void* grad, void* stream);
+/* Stream-ordered copy of the last FFT stage's Z (device scalar) to z_dst
+ * (host pinned or device memory), so a caller can check Z > 0
+ * (optimizer.py:242-243) without a synchronisation inside the step. */
+int fitsne_read_z(fitsne_ctx* ctx, double* z_dst, void* stream);
 
 #ifdef __cplusplus
 }

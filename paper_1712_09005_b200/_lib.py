@@ -21,6 +21,10 @@ _PKG = Path(__file__).resolve().parent
 LIB_PATH = _PKG / os.environ.get("FITSNE_LIB", "libfitsne_b200.so")
 
 OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG, EPOINTS = range(9)
+# implementation switches (include/fitsne_b200.h fitsne_option)
+(OPT_SORTED_SPREAD, OPT_OVERLAP, OPT_SPMV_BLOCKS_PER_SM, OPT_SPREAD_REPLICAS, OPT_TILED_SPMV,
+ OPT_TILE_ROWS, OPT_TILE_COLS, OPT_TILED_CTAS, OPT_TILED_BANK_ORDER, OPT_HOST_PIECES, OPT_FFT_COLS,
+ OPT_FFT_PATH, OPT_GRID_F64) = range(1, 14)
 F32, F64 = 0, 1
 CAUCHY, CAUCHY_SQUARED = 0, 1
 
@@ -82,6 +86,8 @@ _SIGS = {
     "fitsne_gather_tsne": (_int, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
     "fitsne_gradient_rows": (_int, [_vp, _vp, _vp, _dbl, _vp, _vp]),
     "fitsne_combine_rows": (_int, [_vp, _vp, _vp, _i64, _dbl, _vp, _vp]),
+    "fitsne_read_z": (_int, [_vp, _vp, _vp]),
+    "fitsne_grid_accum_dtype": (_int, [_vp]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -170,6 +176,8 @@ class Context:
                                          self.ipi), "fitsne_create")
         self.h = h
         self._P_ref = None  # weak reference to the registered DeviceCSR
+        for opt, val in _default_options.items():
+            check(self.lib.fitsne_set_option(self.h, opt, val), "fitsne_set_option")
 
     def __del__(self):
         try:
@@ -208,6 +216,35 @@ class Context:
 
 
 _contexts: dict = {}
+_default_options: dict = {}
+
+
+class option:
+    """Context manager (A/B tests): set an implementation switch on every
+    existing context and on the contexts created inside the block; restored
+    to `restore` (the library default unless given) on exit."""
+
+    _DEFAULTS = {OPT_FFT_PATH: 0, OPT_GRID_F64: 1, OPT_TILED_SPMV: 1, OPT_SORTED_SPREAD: 1,
+                 OPT_OVERLAP: 1, OPT_HOST_PIECES: 0}
+
+    def __init__(self, opt: int, value: int, restore: int | None = None):
+        self.opt, self.value = opt, value
+        self.restore = self._DEFAULTS.get(opt) if restore is None else restore
+
+    def _apply(self, value):
+        for ctx in list(_contexts.values()):
+            check(ctx.lib.fitsne_set_option(ctx.h, self.opt, value), "fitsne_set_option")
+
+    def __enter__(self):
+        _default_options[self.opt] = self.value
+        self._apply(self.value)
+        return self
+
+    def __exit__(self, *exc):
+        _default_options.pop(self.opt, None)
+        if self.restore is not None:
+            self._apply(self.restore)
+        return False
 
 
 def context(device: int, dims: int, dtype: torch.dtype, p: int = 3, min_intervals: int = 20,

@@ -17,7 +17,8 @@ from pathlib import Path
 PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfitsne_b200.so"
-SOURCES = ["api.cu", "repulsion.cu", "attract.cu", "sortspread.cu", "bandspread.cu", "tiled.cu"]
+SOURCES = ["api.cu", "repulsion.cu", "attract.cu", "sortspread.cu", "bandspread.cu", "tiled.cu",
+           "bigfft.cu"]
 HEADERS = ["common.cuh", "fft.cuh", "interp.cuh", "internal.h", "twiddles.cuh"]
 
 NVCC_FLAGS = [

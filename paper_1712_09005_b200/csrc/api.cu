@@ -120,8 +120,9 @@ int fitsne_destroy(fitsne_ctx* c) {
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&c->accum, &c->fbuf, &c->sbuf, &c->pot, &c->tw, &c->zpart, &c->bbox_part,
                     &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf,
-                    &c->hy, &c->hg};
+                    &c->hy, &c->hg, &c->big, &c->bigtw, &c->y64, &c->r64};
   for (DevBuf* b : bufs) release(*b);
+  if (c->shadow) fitsne_destroy(c->shadow);
   free_tiled(c);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
@@ -201,6 +202,18 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     ctx->tile_cols = C;
     return FITSNE_OK;
   }
+  if (option == FITSNE_OPT_FFT_PATH) {
+    if (value < 0 || value > 2) { set_error("FFT path must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    ctx->fft_path = value;
+    if (ctx->shadow) ctx->shadow->fft_path = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_GRID_F64) {
+    if (value < 0 || value > 2) { set_error("fp64 grid mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    ctx->grid_f64 = value;
+    ctx->grid_valid = false;  // re-derive the pipeline with the next grid
+    return FITSNE_OK;
+  }
   if (option == FITSNE_OPT_FFT_COLS) {
     if (value != 1 && value != 2 && value != 4) { set_error("FFT columns per block must be 1, 2 or 4"); return FITSNE_EINVAL; }
     ctx->cols_per_block = value;
@@ -268,8 +281,12 @@ int fitsne_grid_from_bbox(fitsne_ctx* ctx, const double* bbox_host, fitsne_grid*
   CTX_CHECK(ctx);
   fitsne_grid g;
   FITSNE_TRY(grid_from_bbox(ctx, bbox_host, &g));
+  // no stream argument: the twiddle table is rebuilt (on the legacy stream)
+  // only when the FFT length changes; wait for it only then, so the sharded
+  // step has no host synchronisation here
+  const int gen0 = ctx->tw_gen;
   FITSNE_TRY(install_grid(ctx, g, 0));
-  FITSNE_CUDA(cudaStreamSynchronize(0));
+  if (ctx->tw_gen != gen0) FITSNE_CUDA(cudaStreamSynchronize(0));
   if (grid_host) *grid_host = g;
   return FITSNE_OK;
 }
@@ -290,8 +307,9 @@ int fitsne_set_grid(fitsne_ctx* ctx, const fitsne_grid* gh) {
   for (int d = 0; d < g.dims; ++d) g.spacing[d] = (g.hi[d] - g.lo[d]) / (double)g.nodes_per_dim;
   g.fft_len = smooth23_at_least(2 * g.nodes_per_dim - 1);
   g.status = 0;
+  const int gen0 = ctx->tw_gen;
   FITSNE_TRY(install_grid(ctx, g, 0));
-  FITSNE_CUDA(cudaStreamSynchronize(0));
+  if (ctx->tw_gen != gen0) FITSNE_CUDA(cudaStreamSynchronize(0));
   return FITSNE_OK;
 }
 
@@ -471,6 +489,11 @@ int64_t fitsne_grid_accum_len(fitsne_ctx* ctx) {
   return G * kNodeSlots;
 }
 
+int fitsne_grid_accum_dtype(fitsne_ctx* ctx) {
+  if (!ctx) return FITSNE_F32;
+  return ctx->wide ? FITSNE_F64 : ctx->dtype;
+}
+
 int fitsne_spread_tsne(fitsne_ctx* ctx, const void* Y_local, int64_t n_local, void* accum, void* stream) {
   CTX_CHECK(ctx);
   if (!accum) { set_error("null accumulator"); return FITSNE_EINVAL; }
@@ -507,6 +530,14 @@ int fitsne_combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int
   CTX_CHECK(ctx);
   if (!(alpha >= 1.0)) { set_error("exaggeration alpha must be >= 1"); return FITSNE_EINVAL; }
   return combine_rows(ctx, attr, frep, n, alpha, grad, S_(stream));
+}
+
+int fitsne_read_z(fitsne_ctx* ctx, double* z_dst, void* stream) {
+  CTX_CHECK(ctx);
+  if (!z_dst) { set_error("null destination"); return FITSNE_EINVAL; }
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  FITSNE_CUDA(cudaMemcpyAsync(z_dst, ctx->scal.ptr, sizeof(double), cudaMemcpyDefault, S_(stream)));
+  return FITSNE_OK;
 }
 
 int fitsne_exact_nbody(fitsne_ctx* ctx, const void* Y, int64_t n, const void* charges, int ncharge,

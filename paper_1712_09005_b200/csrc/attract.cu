@@ -539,7 +539,10 @@ __global__ void __launch_bounds__(kBlock)
 k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ pot,
           const double* __restrict__ scal, const T* __restrict__ attr, T alpha,
           T* __restrict__ grad, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel,
-          T* __restrict__ gains, int32_t* __restrict__ status, T* __restrict__ attr_clear) {
+          T* __restrict__ gains, int32_t* __restrict__ status, T* __restrict__ attr_clear,
+          const double* __restrict__ frep64) {
+  // frep64: F_rep precomputed by the fp64 grid pipeline (ctx->wide), else
+  // gathered here from the potentials
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int bad = 0;
   if (i < n) {
@@ -550,13 +553,14 @@ k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ 
 #pragma unroll
       for (int d = 0; d < S; ++d) attr_clear[i * S + d] = (T)0;
     }
-    T phi[4];
-    point_gather<T, S, P>(yi, g, pot, phi);
+    T phi[4] = {0, 0, 0, 0};
+    if (!frep64) point_gather<T, S, P>(yi, g, pot, phi);
     const T Z = (T)scal[0];
 #pragma unroll
     for (int d = 0; d < S; ++d) {
       const int64_t o = i * S + d;
-      const T gd = (T)4 * (alpha * at[d] - frep_from_phi<T, S>(yi, phi, Z, d, g));
+      const T fr = frep64 ? (T)frep64[i * S + d] : frep_from_phi<T, S>(yi, phi, Z, d, g);
+      const T gd = (T)4 * (alpha * at[d] - fr);
       if (!STEP) {
         grad[o] = gd;
       } else {
@@ -599,11 +603,13 @@ static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void*
                           void* gains, int32_t* status, bool clear, cudaStream_t st) {
   const GridArgs g = grid_args(ctx->grid);
   const int blocks = nblocks(n);
+  double* frep64 = nullptr;
+  if (ctx->wide) FITSNE_TRY(shadow_frep(ctx, Y, n, &frep64, st));
 #define CMB(S, P)                                                                              \
   k_combine<T, S, P, STEP><<<blocks, kBlock, 0, st>>>(                                         \
       (const T*)Y, n, g, (const T*)ctx->pot.ptr, (const double*)ctx->scal.ptr, (const T*)attr, \
       (T)alpha, (T*)grad, (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, status,            \
-      clear ? (T*)attr : (T*)nullptr)
+      clear ? (T*)attr : (T*)nullptr, frep64)
   if (ctx->dims == 1) { if (g.p == 3) CMB(1, 3); else CMB(1, 0); }
   else { if (g.p == 3) CMB(2, 3); else CMB(2, 0); }
 #undef CMB

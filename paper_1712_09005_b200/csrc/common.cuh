@@ -129,6 +129,7 @@ struct fitsne_ctx {
   fitsne::DevBuf pot;       // potentials: kNodeSlots per node
   fitsne::DevBuf tw;        // twiddles exp(-2 pi i m / L)
   int tw_len = 0;
+  int tw_gen = 0;           // twiddle regenerations (this context and its shadow)
   fitsne::DevBuf zpart;     // Parseval partials (double), L/2+1
   fitsne::DevBuf bbox_part; // per-block bbox partials (double)
   fitsne::DevBuf scal;      // device scalars (double): [0] Z, [1] KL sum, [2..] misc
@@ -138,6 +139,18 @@ struct fitsne_ctx {
   fitsne::DevBuf part;      // per-block partial sums (double)
   fitsne::DevBuf gen;       // generic scratch
   fitsne::DevBuf sortbuf;   // box sort keys / values / histograms
+  fitsne::DevBuf big;       // four-step FFT planes (bigfft.cu)
+  fitsne::DevBuf bigtw;     // its sub-length twiddle tables
+  int big_tw_l1 = 0, big_tw_l2 = 0;
+  int fft_path = 0;         // 0 auto (four-step above the shared-memory lengths), 1 fast only, 2 four-step
+  // fp64 grid pipeline of an fp32 context (spread accumulation, FFT stage,
+  // potentials and F_rep in double; points and the SpMV stay fp32): used when
+  // the embedding is wide (grid_f64: 0 never, 1 auto, 2 always)
+  int grid_f64 = 1;
+  bool wide = false;             // the current grid runs on the fp64 shadow
+  fitsne_ctx* shadow = nullptr;  // fp64 twin context holding that pipeline
+  fitsne::DevBuf y64;            // points converted for the shadow
+  fitsne::DevBuf r64;            // shadow gather outputs (F_rep, k1, k2)
   int sorted_spread = 1;      // 0 direct scatter, 1 auto (band spread for fp32 2-D p = 3, else box-sorted when crowded), 2 box-sorted, 3 band
   int spread_replicas = 4;    // replicas of the internal spread accumulator (power of two)
   int accum_live_reps = 4;    // replicas the last spread into the internal accumulator wrote

@@ -10,6 +10,9 @@ int grid_from_bbox(fitsne_ctx* ctx, const double* bbox, fitsne_grid* out);
 int compute_bbox(fitsne_ctx* ctx, const void* Y, int64_t n, double* bbox_host,
                  cudaStream_t st);
 int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st);
+// fp64 grid pipeline of an fp32 context (ctx->wide): F_rep (n, dims) in
+// double from the shadow context's potentials
+int shadow_frep(fitsne_ctx* ctx, const void* Y, int64_t n, double** frep, cudaStream_t st);
 int make_grid(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st);
 // make_grid split around other launches: bbox kernels + readback queued on st
 // (bbox_launch), then the host waits for the readback only and installs the
@@ -94,6 +97,12 @@ void tiled_piece_rows(const fitsne_ctx* ctx, int64_t* rows);
 // fitsne_gradient_host (attract.cu)
 int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host, cudaStream_t st);
 int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st);
+
+// four-step FFT convolution for long transforms (bigfft.cu)
+bool big_fft_applies(const fitsne_ctx* ctx, int L);
+int conv_big_tsne(fitsne_ctx* ctx, void* accum, int nrep, int64_t rstride, bool with_k1, int64_t n_total,
+                  cudaStream_t st);
+int conv_big_general(fitsne_ctx* ctx, const void* coeffs, int ncol, int kern, void* out, cudaStream_t st);
 
 int read_scalars(fitsne_ctx* ctx, int count, cudaStream_t st);  // scal[0..count) -> h_scal
 int sub_inplace(fitsne_ctx* ctx, void* out, const void* q, int64_t count, cudaStream_t st);

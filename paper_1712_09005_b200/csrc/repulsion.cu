@@ -261,21 +261,96 @@ __global__ void k_twiddles(typename C2<T>::type* tw, int L) {
   }
 }
 
+// ---------------------------------------------------------------------------
+// fp64 grid pipeline for fp32 contexts (FITSNE_OPT_GRID_F64).  The repulsive
+// force F_i = y_i (K2*1)_i - (K2*y)_i cancels two terms of size |y| K2*1, so
+// fp32 potentials lose accuracy in proportion to the span (rel-L2 3e-4 at
+// span 200, 5e-3 at 430, 1.7e-2 at 860 against the fp64 reference).  Above
+// kWideSpan the grid stages run on an fp64 twin context (same grid, same
+// bit-exact cells): points are widened once per stage, the spread accumulates,
+// the FFT stage transforms and the gather interpolates in double, and F_rep
+// is rounded to fp32 only at the end.  The attractive SpMV is unaffected.
+// ---------------------------------------------------------------------------
+static constexpr double kWideSpan = 256.0;
+
+__global__ void k_widen(const float* __restrict__ x, int64_t m, double* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (double)x[i];
+}
+
+__global__ void k_narrow(const double* __restrict__ x, int64_t m, float* __restrict__ y) {
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
+    y[i] = (float)x[i];
+}
+
+static int shadow_ctx(fitsne_ctx* ctx) {
+  if (ctx->shadow) return FITSNE_OK;
+  fitsne_ctx* sh = nullptr;
+  FITSNE_TRY(fitsne_create(&sh, ctx->device, ctx->dims, FITSNE_F64, ctx->p, ctx->min_intervals,
+                           ctx->intervals_per_integer));
+  sh->sorted_spread = ctx->sorted_spread;
+  sh->spread_replicas = ctx->spread_replicas;
+  sh->fft_path = ctx->fft_path;
+  ctx->shadow = sh;
+  return FITSNE_OK;
+}
+
+// Y (n, dims) fp32 -> ctx->y64 (double), stream-ordered
+const double* widen_points(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
+  const int64_t m = n * ctx->dims;
+  if (ensure(ctx->y64, sizeof(double) * (size_t)std::max<int64_t>(m, 1)) != FITSNE_OK) return nullptr;
+  if (m > 0) {
+    k_widen<<<(int)std::min<int64_t>((m + 255) / 256, 8 * ctx->num_sms), 256, 0, st>>>((const float*)Y, m,
+                                                                                     (double*)ctx->y64.ptr);
+    if (cudaGetLastError() != cudaSuccess) return nullptr;
+  }
+  return (const double*)ctx->y64.ptr;
+}
+
+int narrow_values(const double* x, int64_t m, float* y, cudaStream_t st) {
+  if (m <= 0 || !y) return FITSNE_OK;
+  k_narrow<<<(int)std::min<int64_t>((m + 255) / 256, 1184), 256, 0, st>>>(x, m, y);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+// F_rep (n, dims) of the wide pipeline, in double, into ctx->r64
+int shadow_frep(fitsne_ctx* ctx, const void* Y, int64_t n, double** frep, cudaStream_t st) {
+  const double* y = widen_points(ctx, Y, n, st);
+  if (!y) { set_error("fp64 grid: point conversion failed"); return FITSNE_ECUDA; }
+  FITSNE_TRY(ensure(ctx->r64, sizeof(double) * (size_t)std::max<int64_t>(n, 1) * (2 * ctx->dims + 2)));
+  *frep = (double*)ctx->r64.ptr;
+  return gather_tsne(ctx->shadow, y, n, *frep, nullptr, nullptr, st);
+}
+
 int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
   if (g.dims != ctx->dims) {
     set_error("grid dims do not match the context");
     return FITSNE_EINVAL;
   }
   const int L = g.fft_len;
-  // rows stage holds 2 pairs x 2 ping-pong buffers of L complex in shared memory
-  // column stage needs (L + 4 plen(L)) complex of shared memory at batch 1
-  const int lmax = (ctx->dtype == FITSNE_F32) ? 5184 : 2592;
-  if (L > lmax) {
-    set_error("interpolation grid needs an FFT longer than supported (L=" + std::to_string(L) + ")");
+  // lengths beyond one block's shared memory take the four-step path
+  // (bigfft.cu); its launch grid bounds L by 65535
+  if (L > 65535) {
+    set_error("interpolation grid needs an FFT longer than 65535 (L=" + std::to_string(L) + ")");
     return FITSNE_ETOOBIG;
   }
   ctx->grid = g;
   ctx->grid_valid = true;
+  ctx->wide = false;
+  if (ctx->dtype == FITSNE_F32 && ctx->grid_f64 != 0) {
+    double widest = 0;
+    for (int d = 0; d < g.dims; ++d) widest = std::max(widest, g.hi[d] - g.lo[d]);
+    if (ctx->grid_f64 == 2 || widest > kWideSpan) {
+      FITSNE_TRY(shadow_ctx(ctx));
+      for (int d = 0; d < 4; ++d) ctx->shadow->raw_bbox[d] = ctx->raw_bbox[d];
+      const int gen0 = ctx->shadow->tw_gen;
+      FITSNE_TRY(install_grid(ctx->shadow, g, st));
+      ctx->tw_gen += ctx->shadow->tw_gen - gen0;
+      ctx->wide = true;
+      return FITSNE_OK;  // the fp32 stages of this context are not used for this grid
+    }
+  }
   if (ctx->tw_len != L) {
     size_t es = 2 * dsize(ctx->dtype);
     FITSNE_TRY(ensure(ctx->tw, es * (size_t)L));
@@ -285,6 +360,7 @@ int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
       k_twiddles<double><<<grid_for(L), kBlock, 0, st>>>((double2*)ctx->tw.ptr, L);
     FITSNE_CHECK_LAUNCH();
     ctx->tw_len = L;
+    ++ctx->tw_gen;
   }
   return FITSNE_OK;
 }
@@ -410,6 +486,11 @@ static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
 
 int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
   if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  if (ctx->wide) {  // fp64 grid: a caller's accumulator is double (fitsne_grid_accum_dtype)
+    const double* y = widen_points(ctx, Y, n, st);
+    if (!y) { set_error("fp64 grid: point conversion failed"); return FITSNE_ECUDA; }
+    return spread_tsne(ctx->shadow, y, n, accum, st);
+  }
   GridArgs g = grid_args(ctx->grid);
   const int nrep = accum_reps(ctx, accum);
   const int64_t rstride = (int64_t)accum_elems(ctx->grid);
@@ -1067,6 +1148,12 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
   const fitsne_grid& gr = ctx->grid;
   GridArgs g = grid_args(gr);
   const int L = g.L, n = g.n, H = L / 2 + 1;
+  if (big_fft_applies(ctx, L)) {
+    if (MODE == MODE_TSNE)
+      return conv_big_tsne(ctx, accum, accum_reps_live(ctx, accum), (int64_t)accum_elems(gr), with_k1,
+                           n_total, st);
+    return conv_big_general(ctx, coeffs, ncol, kern, out, st);
+  }
   FftPlan pl;
   make_plan(pl, L);
   const V* tw = (const V*)ctx->tw.ptr;
@@ -1134,6 +1221,14 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
 
 int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st) {
   if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
+  if (ctx->wide) {
+    FITSNE_TRY(fft_tsne(ctx->shadow, accum, n_total, with_k1, st));
+    FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+    // Z (scal[0]) where this context's consumers read it
+    FITSNE_CUDA(cudaMemcpyAsync(ctx->scal.ptr, ctx->shadow->scal.ptr, sizeof(double),
+                                cudaMemcpyDeviceToDevice, st));
+    return FITSNE_OK;
+  }
   if (accum == nullptr) accum = ctx->accum.ptr;
   size_t G = accum_elems(ctx->grid) / kNodeSlots;
   FITSNE_TRY(ensure(ctx->pot, G * kNodeSlots * dsize(ctx->dtype)));
@@ -1220,6 +1315,20 @@ int gather_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces, void* k
                 cudaStream_t st) {
   GridArgs g = grid_args(ctx->grid);
   if (n <= 0) return FITSNE_OK;
+  if (ctx->wide) {
+    const double* y = widen_points(ctx, Y, n, st);
+    if (!y) { set_error("fp64 grid: point conversion failed"); return FITSNE_ECUDA; }
+    const int S = ctx->dims;
+    FITSNE_TRY(ensure(ctx->r64, sizeof(double) * (size_t)n * (2 * S + 2)));
+    double* f = (double*)ctx->r64.ptr;
+    double* a1 = f + (size_t)n * S;
+    double* a2 = a1 + (size_t)n;
+    FITSNE_TRY(gather_tsne(ctx->shadow, y, n, f, k1 ? a1 : nullptr, k2 ? a2 : nullptr, st));
+    FITSNE_TRY(narrow_values(f, n * S, (float*)forces, st));
+    if (k1) FITSNE_TRY(narrow_values(a1, n, (float*)k1, st));
+    if (k2) FITSNE_TRY(narrow_values(a2, n * (S + 1), (float*)k2, st));
+    return FITSNE_OK;
+  }
   const double* scal = (const double*)ctx->scal.ptr;
 #define GATHER_LAUNCH(T, S)                                                                  \
   do {                                                                                       \

@@ -30,7 +30,7 @@ import torch
 import torch.distributed as dist
 
 from . import _lib
-from .affinities import device_csr, n_points
+from .affinities import DeviceCSR, device_csr, n_points
 
 __all__ = ["shard_range", "LibStages", "ShardedGradient"]
 
@@ -46,8 +46,13 @@ class LibStages:
     # columns, columns, rows inverse), gather, tiled SpMV + finish, combine
     launches_per_step = 14
 
+    # Y is all-gathered into a padded layout (rank r's rows at [r m, r m +
+    # count_r), m = the largest shard) so ragged shards need no per-step
+    # concatenation: the local CSR's column indices are remapped to it once
+    padded_columns = True
+
     def __init__(self, P, dims, dtype, device, min_intervals, points_per_interval,
-                 intervals_per_integer, row_begin, row_end):
+                 intervals_per_integer, row_begin, row_end, counts=None):
         self.dims = dims
         self.dtype = dtype
         self.device = device
@@ -55,9 +60,24 @@ class LibStages:
         self.ctx = _lib.Context(device, dims, dtype, points_per_interval, min_intervals,
                                 intervals_per_integer)
         # the row SpMV (attract_start) runs beside the repulsion stages: the
-        # context's default overlapped schedule sizes its grid to 7/8 of the SMs
-        self.csr = device_csr(P, dtype, device, row_begin, row_end)
+        # context's default overlapped schedule sizes its grid to 11/12 of the SMs
+        csr = device_csr(P, dtype, device, row_begin, row_end)
+        counts = counts or [self.n_total]
+        self.shard = max(counts)
+        if min(counts) != max(counts):
+            starts = torch.tensor(np.cumsum([0] + list(counts))[:-1], device=csr.col.device)
+            c = csr.col.long()
+            r = torch.bucketize(c, starts, right=True) - 1
+            col = (r * self.shard + (c - starts[r])).to(torch.int32)
+            csr = DeviceCSR(csr.rowptr, col.contiguous(), csr.val, csr.row_begin,
+                            self.shard * len(counts), csr.ordered_total)
+        self.csr = csr
         self.ctx.set_affinities(self.csr)
+        self._acc = None
+        self._acc_dirty = False
+        self._f = None
+        self._zh = torch.zeros(1, dtype=torch.float64).pin_memory()
+        self._zev = None
 
     # -- collectives run on device tensors (NCCL) --------------------------
     def to_comm(self, x: np.ndarray) -> torch.Tensor:
@@ -94,24 +114,54 @@ class LibStages:
                    "fitsne_grid_from_bbox")
 
     def spread(self, y_local: torch.Tensor) -> torch.Tensor:
+        """Private spread into a persistent accumulator (the FFT stage
+        consumes and clears it, so it is zeroed only when first made or after
+        a step that failed in between); its dtype follows the grid pipeline
+        (fp64 for a wide fp32 embedding, fitsne_grid_accum_dtype)."""
         n_acc = int(self.ctx.lib.fitsne_grid_accum_len(self.ctx.h))
-        acc = torch.zeros(n_acc, dtype=self.dtype, device=self.device)
+        dt = torch.float64 if self.ctx.lib.fitsne_grid_accum_dtype(self.ctx.h) == _lib.F64 \
+            else torch.float32
+        if self._acc is None or self._acc.numel() < n_acc or self._acc.dtype != dt:
+            self._acc = torch.zeros(max(n_acc, 1), dtype=dt, device=self.device)
+        elif self._acc_dirty:
+            self._acc.zero_()
+        acc = self._acc[:n_acc]
+        self._acc_dirty = True
         _lib.check(self.ctx.lib.fitsne_spread_tsne(self.ctx.h, _lib.ptr(y_local), y_local.shape[0],
                                                    _lib.ptr(acc), self.ctx.stream),
                    "fitsne_spread_tsne")
         return acc
 
     def fft(self, acc: torch.Tensor, want_z: bool = True):
-        """FFT stage + Parseval Z; without want_z, Z stays on the device (no
-        host round trip inside the step)."""
+        """FFT stage + Parseval Z.  Without want_z, Z is copied to pinned host
+        memory behind the FFT stage (no host round trip inside the step); the
+        caller checks it with check_z() once the rest of the step is queued."""
         z = C.c_double()
         _lib.check(self.ctx.lib.fitsne_fft_tsne(self.ctx.h, _lib.ptr(acc), self.n_total, 0,
                                                 C.byref(z) if want_z else None, self.ctx.stream),
                    "fitsne_fft_tsne")
-        return float(z.value) if want_z else None
+        self._acc_dirty = False  # consumed and cleared by the FFT stage
+        if want_z:
+            return float(z.value)
+        _lib.check(self.ctx.lib.fitsne_read_z(self.ctx.h, _lib.ptr(self._zh), self.ctx.stream),
+                   "fitsne_read_z")
+        self._zev = torch.cuda.Event()
+        self._zev.record(torch.cuda.current_stream(self.device))
+        return None
+
+    def check_z(self) -> None:
+        """Z > 0 (optimizer.py:242-243): waits for the FFT stage only."""
+        if self._zev is not None:
+            self._zev.synchronize()
+            z = float(self._zh[0])
+            self._zev = None
+            if not z > 0:
+                raise ValueError("normalization Z must be positive")
 
     def gather(self, y_local: torch.Tensor) -> torch.Tensor:
-        f = torch.empty_like(y_local)
+        if self._f is None or self._f.shape != y_local.shape or self._f.dtype != y_local.dtype:
+            self._f = torch.empty_like(y_local)
+        f = self._f
         _lib.check(self.ctx.lib.fitsne_gather_tsne(self.ctx.h, _lib.ptr(y_local), y_local.shape[0],
                                                    _lib.ptr(f), None, None, self.ctx.stream),
                    "fitsne_gather_tsne")
@@ -172,9 +222,12 @@ class ShardedGradient:
                        for r in range(self.world)]
         if stages is None:
             stages = LibStages(P, n_dims, dtype, device, min_intervals, points_per_interval,
-                               intervals_per_integer, self.row_begin, self.row_end)
+                               intervals_per_integer, self.row_begin, self.row_end, self.counts)
         self.stages = stages
         self.launches_per_step = getattr(stages, "launches_per_step", 0)
+        self._padded = getattr(stages, "padded_columns", False)
+        self._yfull = None
+        self._ypad = None
 
     def local(self, y_full):
         return y_full[self.row_begin:self.row_end]
@@ -182,6 +235,19 @@ class ShardedGradient:
     def _all_gather_rows(self, y_local):
         if self.world == 1:
             return y_local.contiguous()
+        if self._padded:
+            # padded layout (LibStages.padded_columns): one all-gather into a
+            # persistent buffer, no per-step allocation or concatenation
+            m = max(self.counts)
+            if self._yfull is None or self._yfull.dtype != y_local.dtype:
+                self._yfull = y_local.new_zeros((m * self.world, self.dims))
+                self._ypad = y_local.new_zeros((m, self.dims))
+            src = y_local.contiguous()
+            if y_local.shape[0] != m:
+                self._ypad[: y_local.shape[0]].copy_(y_local)
+                src = self._ypad
+            dist.all_gather_into_tensor(self._yfull, src, group=self.group)
+            return self._yfull
         if min(self.counts) == max(self.counts):  # equal shards: gather in place
             out = y_local.new_empty((self.n, self.dims))
             dist.all_gather_into_tensor(out, y_local.contiguous(), group=self.group)
@@ -202,6 +268,13 @@ class ShardedGradient:
         # 3: all-gather Y (skipped when the caller already holds it)
         if y_full is None:
             y_full = self._all_gather_rows(y_local)
+        elif self._padded and self.world > 1 and min(self.counts) != max(self.counts):
+            m = max(self.counts)
+            pad = y_full.new_zeros((m * self.world, self.dims))
+            for r, c in enumerate(self.counts):
+                b = shard_range(self.n, r, self.world)[0]
+                pad[r * m: r * m + c] = y_full[b: b + c]
+            y_full = pad
         device_box = hasattr(st, "bbox_start")
         if device_box:
             box = st.bbox_start(y_local)  # 1: queued first, so it gets the whole GPU
@@ -230,5 +303,8 @@ class ShardedGradient:
         # 7-8: gather local F_rep, combine with the SpMV over the local rows
         f_local = st.gather(y_local)
         if overlap:
-            return st.attract_finish(done, f_local, alpha)
+            g = st.attract_finish(done, f_local, alpha)
+            if hasattr(st, "check_z"):
+                st.check_z()  # the rest of the step is already queued
+            return g
         return st.attract_rows(y_full, f_local, alpha)

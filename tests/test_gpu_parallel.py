@@ -104,3 +104,26 @@ def test_bbox_device_packed_layout(cuda):
         _lib.check(ctx.lib.fitsne_bbox_device(ctx.h, _lib.ptr(y), y.shape[0], _lib.ptr(buf),
                                               ctx.stream), "nan")
         assert buf.cpu().numpy()[4] < 0
+
+
+def test_lib_stages_wide_fp32_uses_fp64_grid(nccl_group):
+    """A wide fp32 embedding (span ~600 > 256): the sharded stages switch the
+    grid accumulator to fp64 (fitsne_grid_accum_dtype) and keep the 1e-3 bar."""
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    from paper_1712_09005_b200.parallel import ShardedGradient
+    rng = np.random.default_rng(5)
+    n = 20000
+    c = rng.uniform(0, 600, (30, 2))
+    y = (c[rng.integers(0, 30, n)] + 3 * rng.standard_normal((n, 2))).astype(np.float32)
+    r = np.repeat(np.arange(n), 10)
+    cc = rng.integers(0, n - 1, n * 10)
+    cc = cc + (cc >= r)
+    key = np.unique(np.minimum(r, cc) * n + np.maximum(r, cc))
+    P = SparseAffinities(n=n, rows=key // n, cols=key % n, values=np.full(key.size, 0.5 / key.size))
+    sg = ShardedGradient(P, n_dims=2, dtype=torch.float32, device=0, min_intervals=50)
+    yt = torch.from_numpy(y).cuda()
+    for _ in range(2):
+        g = sg.gradient(yt, alpha=1.0).double().cpu().numpy()
+    assert sg.stages._acc.dtype == torch.float64
+    ref = O.grad(P.rows, P.cols, P.values, y.astype(np.float64), 1.0, 50, 3, "fft")
+    assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 1e-3

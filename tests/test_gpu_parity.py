@@ -305,17 +305,22 @@ class TestLargeProperties:
         assert abs(rep.z - z) <= 1e-4 * z
 
     @pytest.mark.parametrize("dtype,span,tol", [
-        ("float32", 200.0, 1e-3),   # fp32 meets the 1e-3 bar up to spans of ~200-250
-        ("float32", 860.0, 3e-2),   # widest fp32 grid (L = 5184): documented fp32 limit
-        ("float64", 428.0, 1e-5),   # widest fp64 grid (L = 2592)
+        ("float32", 200.0, 1e-3),   # fp32 grid pipeline
+        ("float32", 430.0, 1e-3),   # fp64 grid pipeline of an fp32 context (span > 256)
+        ("float32", 860.0, 1e-3),   # longest one-block fp32 transform (L = 5184)
+        ("float64", 428.0, 1e-5),   # longest one-block fp64 transform (L = 2592)
+        ("float64", 860.0, 1e-5),   # fp64 four-step FFT (L = 5184)
+        ("float32", 2000.0, 1e-3),  # four-step FFT, L = 12288
+        ("float64", 2000.0, 1e-5),
     ])
     def test_wide_grids(self, fs, dtype, span, tol):
-        """Wide embeddings (late t-SNE layouts): the longest FFTs, where the
-        spectrum stage takes fewer columns per block.  In fp32 the repulsive
-        force F = y_i K2*1 - K2*y loses digits as the span grows (the self
-        charge y_i is subtracted from a potential of the same magnitude), so
-        the bar is 1e-3 up to span ~200 and is checked loosely beyond; fp64
-        stays at the reference's precision.  Z stays accurate throughout."""
+        """Wide embeddings (late t-SNE layouts) against the reference's
+        algorithm at any span (nbody.py:134, 267, 276 size every grid with
+        next_fast_len).  In fp32 the repulsive force F = y_i K2*1 - K2*y
+        cancels |y|-sized terms, so past span 256 an fp32 context runs its
+        grid pipeline in fp64 (FITSNE_OPT_GRID_F64) and keeps the 1e-3 bar;
+        transforms longer than one block's shared memory take the four-step
+        path.  Z stays accurate throughout."""
         _, _, opt, _ = fs
         rng = np.random.default_rng(21)
         # 40 blobs spread over [0, span]^2 (a late-iteration t-SNE layout)
@@ -329,11 +334,61 @@ class TestLargeProperties:
         assert err <= tol, err
         assert abs(rep.z - z) <= 1e-5 * z
 
+    @pytest.mark.parametrize("span", [600.0, 2000.0])
+    def test_wide_gradient_fp32(self, fs, span):
+        """fp32 gradient through both entry points (device buffers: the
+        overlapped schedule's combine reads the fp64 grid's F_rep; host
+        buffers: fitsne_gradient_host) at wide spans, and the fused iteration
+        (fitsne_iterate) against the oracle's update."""
+        _, _, opt, aff = fs
+        rng = np.random.default_rng(int(span))
+        n = 20_000
+        c = rng.uniform(0, span, (40, 2))
+        y = (c[rng.integers(0, 40, n)] + 3.0 * rng.standard_normal((n, 2))).astype(np.float32)
+        r = np.repeat(np.arange(n), 8)
+        cc = rng.integers(0, n - 1, n * 8)
+        cc = cc + (cc >= r)
+        key = np.unique(np.minimum(r, cc) * n + np.maximum(r, cc))
+        v = rng.exponential(1.0, key.size)
+        P = aff.SparseAffinities(n=n, rows=key // n, cols=key % n, values=v / (2 * v.sum()))
+        y64 = y.astype(np.float64)
+        ref = O.grad(P.rows, P.cols, P.values, y64, 4.0, 50, 3, "fft")
+        g_dev = opt.gradient(P, torch.from_numpy(y).cuda(), 4.0, 50, 3, "fft").double().cpu().numpy()
+        g_host = opt.gradient(P, y, 4.0, 50, 3, "fft")
+        assert rel_l2(g_dev, ref) <= 1e-3 and rel_l2(g_host, ref) <= 1e-3
+
     def test_grid_too_large(self, fs):
+        """Only a grid whose FFT exceeds the four-step path's 65535 points is
+        refused (span > ~10900 at p = 3)."""
         _, _, opt, _ = fs
-        y = np.array([[0.0, 0.0], [2000.0, 1.0], [5.0, 7.0]])
+        y = np.array([[0.0, 0.0], [12000.0, 1.0], [5.0, 7.0]])
         with pytest.raises(ValueError, match="FFT"):
             opt.compute_repulsive(y, 50, 3, "fft")
+
+    @pytest.mark.parametrize("dtype", DTYPES)
+    @pytest.mark.parametrize("dims", [1, 2])
+    def test_four_step_path_matches_one_block_path(self, fs, dtype, dims):
+        """The four-step FFT (forced at a length the one-block kernels also
+        handle) gives the same repulsion, Z and nbody matvec as the one-block
+        kernels and the oracle."""
+        from paper_1712_09005_b200 import _lib, nbody
+        _, _, opt, _ = fs
+        rng = np.random.default_rng(dims)
+        y = (rng.standard_normal((30_000, dims)) * 40).astype(np.float32 if dtype == "float32" else np.float64)
+        yd = torch.from_numpy(y).cuda()
+        f_o, z_o, _, _ = O.repulsion(y.astype(np.float64), 50, 3, "fft")
+        out = {}
+        q = torch.from_numpy(rng.standard_normal(y.shape[0])).to(yd)
+        for path in (1, 2):
+            with _lib.option(_lib.OPT_FFT_PATH, path):
+                rep = opt.compute_repulsive(yd, 50, 3, "fft")
+                out[path] = (rep.forces.double().cpu().numpy(), rep.z,
+                             nbody.evaluate_nbody(yd, q, "cauchy", 50, 3).double().cpu().numpy(), q)
+        tol = TOL[dtype]
+        assert rel_l2(out[2][0], f_o) <= tol and rel_l2(out[2][0], out[1][0]) <= tol
+        assert abs(out[2][1] - z_o) <= 1e-5 * z_o
+        nb_o = O.nbody_fft(y.astype(np.float64), out[2][3].double().cpu().numpy(), O.CAUCHY, 50, 3)
+        assert rel_l2(out[2][2], nb_o) <= (1e-4 if dtype == "float32" else 1e-10)
 
 
 # ----------------------------------------------------------------------------- errors
