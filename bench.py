@@ -68,10 +68,20 @@ def parse():
                     help="also time the complete 1000-iteration C3 t-SNE run (run_tsne, fused "
                          "device iterations, late exaggeration 4 from 750) and report it")
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--shuffle", action="store_true",
+                    help="randomly permute the C3 point order (real data arrive in no cluster "
+                         "order; the library relabels P internally, FITSNE_OPT_RELABEL)")
+    ap.add_argument("--bank-order", type=int, default=1, choices=[0, 1, 2],
+                    help="FITSNE_OPT_TILED_BANK_ORDER (A/B)")
+    ap.add_argument("--relabel", type=int, default=1, choices=[0, 1, 2],
+                    help="FITSNE_OPT_RELABEL: 0 caller's order, 1 auto (default), 2 always")
     ap.add_argument("--host-schedule", type=int, default=0, choices=[0, 1, 2],
                     help="FITSNE_OPT_HOST_PIECES for the e2e call (A/B)")
     ap.add_argument("--sharded", action="store_true",
                     help="run the multi-GPU (sharded, NCCL) code path even with one rank (testing)")
+    ap.add_argument("--torch-comm", action="store_true",
+                    help="multi-GPU: orchestrate the collectives from Python (torch.distributed, "
+                         "parallel.ShardedGradient) instead of the library's NCCL communicator")
     ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2, 3],
                     help="0 direct atomics, 1 auto (default), 2 box-sorted")
     ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2],
@@ -184,6 +194,8 @@ def make_inputs(args, device):
     n = args.n or WORKLOADS["c3"]["n"]
     t0 = time.time()
     P, Y = synth.c3(device=device, n=n, seed=args.seed)
+    if getattr(args, "shuffle", False):
+        P, Y = synth.shuffle(P, Y, seed=args.seed + 1000)
     torch.cuda.synchronize() if str(device).startswith("cuda") else None
     return P, Y, time.time() - t0
 
@@ -369,11 +381,21 @@ def run_ours(args):
 
     if sharded:
         from paper_1712_09005_b200 import parallel
-        ev = parallel.ShardedGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
-                                      points_per_interval=3)
+        if args.torch_comm:
+            # Python orchestration over torch.distributed (parallel.ShardedGradient)
+            ev = parallel.ShardedGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
+                                          points_per_interval=3)
+        else:
+            # the library's own NCCL communicator: one C-ABI call per step
+            ev = parallel.NcclGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
+                                       points_per_interval=3)
         y_full = torch.from_numpy(Y).to(device=dev, dtype=dt)
         y_local = ev.local(y_full).contiguous()
-        step = lambda: ev.gradient(y_local, 1.0)  # noqa: E731  (all-gathers Y inside)
+        g_buf = torch.empty_like(y_local)
+        if args.torch_comm:
+            step = lambda: ev.gradient(y_local, 1.0)  # noqa: E731  (all-gathers Y inside)
+        else:
+            step = lambda: ev.gradient(y_local, 1.0, out=g_buf)  # noqa: E731
         for _ in range(args.warmup):
             step()
         launches = count_launches(step)
@@ -383,7 +405,7 @@ def run_ours(args):
             ms = timed(step, args.steps, stream)
         # e2e per rank: this rank's Y rows from pinned host memory in, its
         # gradient rows out, every step (max over ranks of the same timing)
-        st_ = ev.stages
+        st_ = ev.stages if args.torch_comm else None
         yh = y_local.cpu().pin_memory()
         gh = torch.empty_like(yh).pin_memory()
         yd = torch.empty_like(y_local)
@@ -400,14 +422,23 @@ def run_ours(args):
         ms_e2e = max(ms_e2e, (time.perf_counter() - t0w) / args.steps * 1e3)
         # roofline: this rank's attractive SpMV alone (same kernel and grid as
         # in the step), bytes of its rows
-        def spmv_only():
-            done = st_.attract_start(y_full)
-            stream.wait_event(done)
+        if args.torch_comm:
+            def spmv_only():
+                done = st_.attract_start(y_full)
+                stream.wait_event(done)
+        else:
+            # equal shards at the bench sizes: the padded all-gather layout is
+            # the natural one, so the full Y feeds the rank's SpMV directly
+            attr_buf = torch.empty_like(y_local)
+
+            def spmv_only():
+                _lib.check(ev.ctx.lib.fitsne_attractive(ev.ctx.h, _lib.ptr(y_full), _lib.ptr(attr_buf),
+                                                        ev.ctx.stream), "fitsne_attractive")
         for _ in range(3):
             spmv_only()
         ms_spmv = timed(spmv_only, args.steps, stream)
         es = 4 if dt == torch.float32 else 8
-        nnz_l = int(st_.csr.col.numel())
+        nnz_l = int((st_ if args.torch_comm else ev).csr.col.numel())
         n_l = int(y_local.shape[0])
         b_spmv = nnz_l * (4 + es) + 8 * (n_l + 1) + 3 * 2 * es * n_l
         t = torch.tensor([ms, ms_e2e, ms_spmv], device=dev, dtype=torch.float64)
@@ -431,7 +462,9 @@ def run_ours(args):
                              "launch_ms": ms_spmv, "traffic": None},
                 "cpu_baseline": None,
                 "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
-                        "api": "parallel.ShardedGradient.gradient with this rank's rows copied in "
+                        "api": ("parallel.ShardedGradient.gradient" if args.torch_comm else
+                                "parallel.NcclGradient.gradient -> fitsne_gradient_sharded") +
+                               " with this rank's rows copied in "
                                "from pinned host memory and its gradient rows copied out",
                         "h2d_bytes_per_step": int(yh.numel() * yh.element_size()) * world,
                         "d2h_bytes_per_step": int(gh.numel() * gh.element_size()) * world},
@@ -440,6 +473,8 @@ def run_ours(args):
                 "clocks": clk.summary(),
             }
             print(json.dumps(line), flush=True)
+        if not args.torch_comm:
+            ev.close()
         dist.destroy_process_group()
         return
 
@@ -452,6 +487,8 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, args.overlap_mode), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 3, args.spmv_blocks), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, args.spread_replicas), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, args.relabel), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_BANK_ORDER, args.bank_order), "set_option")
     g = torch.empty_like(y)
     zc = __import__("ctypes").c_double()
 
@@ -492,8 +529,11 @@ def run_ours(args):
 
     # which SpMV ran (tiled copy of P or the CSR kernel), and its layout
     import ctypes as _C
-    tst = (_C.c_int64 * 6)()
+    tst = (_C.c_int64 * 8)()
     _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), tst, ctx.stream), "tiled_stats")
+    layout = {"tiled": bool(tst[0]), "tiles": int(tst[1]), "segments": int(tst[4]),
+              "relabelled": bool(tst[6]), "segments_caller_order": int(tst[7]),
+              "entries_per_segment": round(nnz / max(int(tst[4]), 1), 2)}
     if tst[0]:
         spmv_kernel = "k_attract_tiled (tiled attractive SpMV) + k_tiled_finish"
         traffic_key = "spmv_tiled"
@@ -586,6 +626,8 @@ def run_ours(args):
         "config": workload_config(
             P, n_intervals=int(gr.n_intervals), nodes_per_dim=int(gr.nodes_per_dim),
             fft_len=int(gr.fft_len), parallelism="single",
+            point_order="shuffled (random permutation)" if args.shuffle else "generator (cluster by cluster)",
+            spmv_layout=layout,
             l2="inputs larger than L2 (CSR %.2f GB > 126 MB L2), no flush" % (nnz * (4 + es) / 1e9),
             input_gen_s=round(t_gen, 1)),
         "roofline": {"kernel": spmv_kernel, "bound": "hbm",
@@ -685,7 +727,8 @@ def stage_breakdown(ctx, y, n, dt, steps, stream):
     out = {}
     out["bbox+grid"] = timed(lambda: ctx.lib.fitsne_make_grid(ctx.h, _lib.ptr(y), n, C.byref(gr),
                                                               ctx.stream), steps, stream)
-    acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=dt, device=y.device)
+    adt = torch.float64 if ctx.lib.fitsne_grid_accum_dtype(ctx.h) == _lib.F64 else torch.float32
+    acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=adt, device=y.device)
     out["spread"] = timed(lambda: ctx.lib.fitsne_spread_tsne(ctx.h, _lib.ptr(y), n, _lib.ptr(acc),
                                                              ctx.stream), steps, stream)
     # fft stage clears the accumulator it consumes, so re-spread is not needed for timing

@@ -45,9 +45,10 @@ enum fitsne_status {
   FITSNE_ENOMEM = 5,      /* device allocation failed */
   FITSNE_EOUTSIDE = 6,    /* point outside grid bounds -> ValueError (nbody.py:210) */
   FITSNE_ETOOBIG = 7,     /* grid larger than the FFT kernels support */
-  FITSNE_EPOINTS = 8      /* non-finite point met while building the grid -> ValueError
+  FITSNE_EPOINTS = 8,     /* non-finite point met while building the grid -> ValueError
                              ("points must be finite", nbody.py:127-128); the fused
                              iteration reports it for a diverged embedding */
+  FITSNE_ENCCL = 9        /* NCCL missing or failed (fitsne_comm_init / sharded gradient) */
 };
 
 enum fitsne_dtype { FITSNE_F32 = 0, FITSNE_F64 = 1 };
@@ -101,7 +102,8 @@ enum fitsne_option {
   FITSNE_OPT_HOST_PIECES = 10,
   FITSNE_OPT_FFT_COLS = 11,
   FITSNE_OPT_FFT_PATH = 12,
-  FITSNE_OPT_GRID_F64 = 13
+  FITSNE_OPT_GRID_F64 = 13,
+  FITSNE_OPT_RELABEL = 14
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -119,6 +121,9 @@ enum fitsne_option {
  *   overlaps the next range; 1 = tiled SpMV in row pieces on a high-priority
  *   stream with each piece's combine + copy-out overlapping later pieces;
  *   2 = copy in, gradient, one copy out.
+ *   FITSNE_OPT_TILED_BANK_ORDER: slot order inside the tiles' slabs chosen
+ *   to spread each step's y_j gathers over shared-memory bank pairs; 0 = off,
+ *   1 (default) = every slab up to 256 slots per lane, 2 = slabs up to 32 only.
  *   FITSNE_OPT_FFT_COLS: adjacent columns per block of the column FFT stage
  *   (1 = default, 2, 4; fewer when shared memory does not fit).
  *   FITSNE_OPT_FFT_PATH: 0 (default) = one-block-per-transform kernels while
@@ -129,11 +134,17 @@ enum fitsne_option {
  *   = spread accumulation, FFT stage, potentials and F_rep in fp64 when the
  *   embedding's widest span exceeds 256 (fp32's repulsive force loses
  *   accuracy with the span: F = y K2*1 - K2*y cancels |y|-sized terms); 2 =
- *   always.  Points, the attractive SpMV and the gradient stay fp32. */
+ *   always.  Points, the attractive SpMV and the gradient stay fp32.
+ *   FITSNE_OPT_RELABEL: the tiled copy of P over a Cuthill-McKee relabelling
+ *   of the points computed from P's pattern on the device (components and
+ *   neighbourhoods get contiguous labels; results stay in the caller's
+ *   order).  0 = caller's order; 1 (default) = relabel when that cuts the
+ *   (row, column chunk) segments of the tiles by >= 10%; 2 = always. */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
- * only for its alignment): out[0..5] = {in use (0/1), tiles, slabs, slot
- * groups, (row, chunk) segments, stored entries}. */
+ * only for its alignment): out[0..7] = {in use (0/1), tiles, slabs, slot
+ * groups, (row, chunk) segments, stored entries, relabelled (0/1), segments
+ * in the caller's order}. */
 int fitsne_tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, void* stream);
 
 /* --- a1: make_grid (nbody.py:118-150).  Device bbox reduction + fp64 grid
@@ -259,6 +270,21 @@ int fitsne_combine_rows(fitsne_ctx* ctx, const void* attr, const void* frep, int
  * (host pinned or device memory), so a caller can check Z > 0
  * (optimizer.py:242-243) without a synchronisation inside the step. */
 int fitsne_read_z(fitsne_ctx* ctx, double* z_dst, void* stream);
+
+/* --- Multi-GPU over NCCL inside the library: one context
+ * and one process per GPU.  Rank 0 makes the id (128 bytes) and sends it to
+ * the others by any means; every rank then calls fitsne_comm_init, registers
+ * the CSR rows of its shard [N r / R, N (r+1) / R) with fitsne_set_affinities
+ * (global column indices, n_total = N) and calls fitsne_gradient_sharded each
+ * evaluation: device bbox + MIN all-reduce (one 40-byte readback), all-gather
+ * of Y, the shard's attractive SpMV on a side stream, private spread + SUM
+ * all-reduce of the grid, replicated FFT stage, gather, combine.  NCCL is
+ * loaded at run time (libnccl.so.2; the copy already in the process first). */
+int fitsne_nccl_unique_id(void* unique_id_out);
+int fitsne_comm_init(fitsne_ctx* ctx, const void* unique_id, int rank, int nranks, int64_t n_total);
+int fitsne_comm_destroy(fitsne_ctx* ctx);
+int fitsne_gradient_sharded(fitsne_ctx* ctx, const void* Y_local, double alpha, void* grad_local,
+                            double* z_host, void* stream);
 
 #ifdef __cplusplus
 }

@@ -20,11 +20,11 @@ _PKG = Path(__file__).resolve().parent
 # FITSNE_LIB selects another in-tree build of the library (A/B experiments)
 LIB_PATH = _PKG / os.environ.get("FITSNE_LIB", "libfitsne_b200.so")
 
-OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG, EPOINTS = range(9)
+OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG, EPOINTS, ENCCL = range(10)
 # implementation switches (include/fitsne_b200.h fitsne_option)
 (OPT_SORTED_SPREAD, OPT_OVERLAP, OPT_SPMV_BLOCKS_PER_SM, OPT_SPREAD_REPLICAS, OPT_TILED_SPMV,
  OPT_TILE_ROWS, OPT_TILE_COLS, OPT_TILED_CTAS, OPT_TILED_BANK_ORDER, OPT_HOST_PIECES, OPT_FFT_COLS,
- OPT_FFT_PATH, OPT_GRID_F64) = range(1, 14)
+ OPT_FFT_PATH, OPT_GRID_F64, OPT_RELABEL) = range(1, 15)
 F32, F64 = 0, 1
 CAUCHY, CAUCHY_SQUARED = 0, 1
 
@@ -88,6 +88,10 @@ _SIGS = {
     "fitsne_combine_rows": (_int, [_vp, _vp, _vp, _i64, _dbl, _vp, _vp]),
     "fitsne_read_z": (_int, [_vp, _vp, _vp]),
     "fitsne_grid_accum_dtype": (_int, [_vp]),
+    "fitsne_nccl_unique_id": (_int, [_vp]),
+    "fitsne_comm_init": (_int, [_vp, _vp, _int, _int, _i64]),
+    "fitsne_comm_destroy": (_int, [_vp]),
+    "fitsne_gradient_sharded": (_int, [_vp, _vp, _dbl, _vp, C.POINTER(_dbl), _vp]),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -175,7 +179,7 @@ class Context:
             check(self.lib.fitsne_create(C.byref(h), device, dims, self.code, p, min_intervals,
                                          self.ipi), "fitsne_create")
         self.h = h
-        self._P_ref = None  # weak reference to the registered DeviceCSR
+        self._P_ref = None  # the registered DeviceCSR
         for opt, val in _default_options.items():
             check(self.lib.fitsne_set_option(self.h, opt, val), "fitsne_set_option")
 
@@ -191,28 +195,35 @@ class Context:
     def stream(self):
         return stream_handle(self.device)
 
-    def set_affinities(self, csr):
+    def set_affinities(self, csr, owner=None):
         """Register a DeviceCSR with this context (no-op if it is already the
-        registered one).  The context holds the CSR weakly: when the caller's
-        P (which owns the cached CSR) goes away, the library is told to forget
-        the device pointers and frees its tiled copy of P."""
-        cur = self._P_ref() if self._P_ref is not None else None
-        if csr is cur:
+        registered one).  The context keeps the CSR alive while it is
+        registered; with `owner` (the caller's P, which caches the CSR), the
+        registration is dropped -- and the library frees its tiled copy of P
+        -- once that P is garbage-collected."""
+        if csr is self._P_ref:
             return
         check(self.lib.fitsne_set_affinities(self.h, ptr(csr.rowptr), ptr(csr.col), ptr(csr.val),
                                              csr.n_rows, csr.row_begin, csr.n_total,
                                              csr.col.numel()),
               "fitsne_set_affinities")
-        self._P_ref = weakref.ref(csr, self._released)
-
-    def _released(self, wr):
-        if self._P_ref is wr and getattr(self, "h", None) and _lib is not None:
-            self._P_ref = None
+        self._P_ref = csr
+        if owner is not None:
             try:
-                with torch.cuda.device(self.device):
-                    _lib.fitsne_set_affinities(self.h, None, None, None, 0, 0, 0, 0)
-            except Exception:  # noqa: BLE001 - interpreter shutdown
+                weakref.finalize(owner, self._released, weakref.ref(csr))
+            except TypeError:  # owner not weak-referenceable: keep the CSR
                 pass
+
+    def _released(self, csr_ref):
+        csr = csr_ref()
+        if csr is None or self._P_ref is not csr or not getattr(self, "h", None) or _lib is None:
+            return
+        self._P_ref = None
+        try:
+            with torch.cuda.device(self.device):
+                _lib.fitsne_set_affinities(self.h, None, None, None, 0, 0, 0, 0)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
 
 
 _contexts: dict = {}
@@ -224,7 +235,7 @@ class option:
     existing context and on the contexts created inside the block; restored
     to `restore` (the library default unless given) on exit."""
 
-    _DEFAULTS = {OPT_FFT_PATH: 0, OPT_GRID_F64: 1, OPT_TILED_SPMV: 1, OPT_SORTED_SPREAD: 1,
+    _DEFAULTS = {OPT_FFT_PATH: 0, OPT_GRID_F64: 1, OPT_TILED_SPMV: 1, OPT_SORTED_SPREAD: 1, OPT_RELABEL: 1,
                  OPT_OVERLAP: 1, OPT_HOST_PIECES: 0}
 
     def __init__(self, opt: int, value: int, restore: int | None = None):

@@ -18,7 +18,7 @@ PKG = Path(__file__).resolve().parent
 CSRC = PKG / "csrc"
 LIB = PKG / "libfitsne_b200.so"
 SOURCES = ["api.cu", "repulsion.cu", "attract.cu", "sortspread.cu", "bandspread.cu", "tiled.cu",
-           "bigfft.cu"]
+           "bigfft.cu", "reorder.cu", "comm.cu"]
 HEADERS = ["common.cuh", "fft.cuh", "interp.cuh", "internal.h", "twiddles.cuh"]
 
 NVCC_FLAGS = [
@@ -46,24 +46,28 @@ def stale() -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def _compile(src: str, obj: Path) -> tuple[int, str]:
-    flags = [f for f in NVCC_FLAGS if f not in ("-shared",)]
+def _compile(src: str, obj: Path, defines=()) -> tuple[int, str]:
+    flags = [f for f in NVCC_FLAGS if f not in ("-shared",)] + [f"-D{d}" for d in defines]
     cmd = [nvcc(), *flags, "-c", "-o", str(obj), str(CSRC / src)]
     res = subprocess.run(cmd, capture_output=True, text=True)
     return res.returncode, f"== {src}\n" + (res.stdout or "") + (res.stderr or "")
 
 
-def build(force: bool = False, verbose: bool = False) -> Path:
-    if not force and not stale():
+def build(force: bool = False, verbose: bool = False, variant: str | None = None,
+          defines=()) -> Path:
+    """Build the library.  `variant` + `defines` build an A/B copy
+    (libfitsne_b200_<variant>.so, selected at run time with FITSNE_LIB)."""
+    lib = LIB if variant is None else PKG / f"libfitsne_b200_{variant}.so"
+    if variant is None and not force and not stale():
         return LIB
     # one nvcc per translation unit, in parallel, then one link
     import tempfile
     from concurrent.futures import ThreadPoolExecutor
-    tmp = LIB.with_suffix(".so.tmp")
+    tmp = lib.with_suffix(".so.tmp")
     with tempfile.TemporaryDirectory(prefix="fitsne_build_") as td:
         objs = [Path(td) / (Path(s).stem + ".o") for s in SOURCES]
         with ThreadPoolExecutor(max_workers=min(len(SOURCES), os.cpu_count() or 1)) as ex:
-            results = list(ex.map(_compile, SOURCES, objs))
+            results = list(ex.map(lambda a: _compile(a[0], a[1], defines), zip(SOURCES, objs)))
         log = "".join(r[1] for r in results)
         rc = max(r[0] for r in results)
         if rc == 0:
@@ -78,9 +82,12 @@ def build(force: bool = False, verbose: bool = False) -> Path:
         raise RuntimeError("nvcc failed building libfitsne_b200.so (see build.log)")
     if verbose:
         sys.stdout.write(log)
-    os.replace(tmp, LIB)
-    return LIB
+    os.replace(tmp, lib)
+    return lib
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv))
+    args = sys.argv[1:]
+    var = next((a.split("=", 1)[1] for a in args if a.startswith("--variant=")), None)
+    defs = [a[2:] for a in args if a.startswith("-D")]
+    print(build(force="--force" in args, verbose="-v" in args, variant=var, defines=defs))

@@ -51,6 +51,7 @@ static void release(DevBuf& b) {
 using namespace fitsne;
 
 #define CTX_CHECK(ctx)                                    \
+  FITSNE_RANGE(__func__);                                 \
   do {                                                    \
     if (!(ctx)) {                                         \
       set_error("null context");                          \
@@ -123,6 +124,7 @@ int fitsne_destroy(fitsne_ctx* c) {
                     &c->hy, &c->hg, &c->big, &c->bigtw, &c->y64, &c->r64};
   for (DevBuf* b : bufs) release(*b);
   if (c->shadow) fitsne_destroy(c->shadow);
+  comm_free(c);
   free_tiled(c);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
@@ -208,6 +210,11 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     if (ctx->shadow) ctx->shadow->fft_path = value;
     return FITSNE_OK;
   }
+  if (option == FITSNE_OPT_RELABEL) {
+    if (value < 0 || value > 2) { set_error("relabel mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    ctx->relabel = value;
+    return FITSNE_OK;
+  }
   if (option == FITSNE_OPT_GRID_F64) {
     if (value < 0 || value > 2) { set_error("fp64 grid mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
     ctx->grid_f64 = value;
@@ -225,7 +232,7 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_TILED_BANK_ORDER) {
-    if (value < 0 || value > 1) { set_error("bank order must be 0 or 1"); return FITSNE_EINVAL; }
+    if (value < 0 || value > 2) { set_error("bank order must be 0, 1 or 2"); return FITSNE_EINVAL; }
     ctx->tiled_bank_order = value;
     return FITSNE_OK;
   }

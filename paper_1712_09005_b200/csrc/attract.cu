@@ -670,6 +670,7 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
 
 static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha, void* grad,
                                     cudaStream_t st, void* grad_host) {
+  FITSNE_RANGE("gradient_schedule");
   const int64_t n = ctx->n_total;
   void* attr = nullptr;
   bool clear = false;
@@ -759,7 +760,8 @@ static int gradient_host_impl(fitsne_ctx* ctx, const void* Y_host, double alpha,
     FITSNE_CUDA(cudaStreamSynchronize(st));
     return FITSNE_OK;
   }
-  if (ctx->host_pieces == 0 || ctx->overlap == 0 || !tiled_usable(ctx, y, st)) {
+  if (ctx->host_pieces == 0 || ctx->overlap == 0 || !tiled_usable(ctx, y, st) ||
+      tiled_relabeled(ctx)) {  // row pieces are ranges of the caller's order
     // the combine runs in point ranges whose copy-out overlaps the next range
     FITSNE_TRY(gradient_overlapped(ctx, y, alpha, g, st, grad_host));
     FITSNE_CUDA(cudaStreamSynchronize(st));
@@ -837,6 +839,7 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
 static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void* gains,
                               double alpha, double momentum, double lr, double* kl_dev,
                               int32_t* status_dev, cudaStream_t st) {
+  FITSNE_RANGE("iterate_schedule");
   const int64_t n = ctx->n_total;
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
   void* attr = nullptr;

@@ -338,6 +338,7 @@ bool big_fft_applies(const fitsne_ctx* ctx, int L) {
 template <typename T, int MODE>
 static int conv_big_t(fitsne_ctx* ctx, T* accum, int nrep, int64_t rstride, const T* coeffs, int ncol,
                       int kern, bool with_k1, T* out, int64_t n_total, cudaStream_t st) {
+  FITSNE_RANGE("four_step_fft");
   using V = typename C2<T>::type;
   const GridArgs g = grid_args(ctx->grid);
   const int L = g.L, n = g.n, dims = ctx->grid.dims;

@@ -3,6 +3,7 @@
 #pragma once
 
 #include <cuda_runtime.h>
+#include <nvtx3/nvToolsExt.h>
 #include <stdint.h>
 #include <cstddef>
 #include <string>
@@ -33,6 +34,17 @@ struct Status {
   } while (0)
 
 #define FITSNE_CHECK_LAUNCH() FITSNE_CUDA(cudaGetLastError())
+
+// NVTX range for the lifetime of a scope (C-ABI entry points and pipeline
+// stages show up by name in Nsight timelines; a push/pop pair when no tool
+// is attached)
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define FITSNE_RANGE(name) ::fitsne::NvtxRange _fitsne_nvtx_range(name)
 
 #define FITSNE_TRY(expr)              \
   do {                                \
@@ -107,6 +119,7 @@ struct DevBuf {
 };
 
 struct TiledP;  // tiled copy of P (tiled.cu)
+struct Comm;    // NCCL communicator state (comm.cu)
 
 }  // namespace fitsne
 
@@ -159,9 +172,11 @@ struct fitsne_ctx {
   int tiled_spmv = 1;              // 0 CSR kernel, 1 auto, 2 tiled when applicable
   int tile_rows = 3072, tile_cols = 8192, tiled_ctas = 0;
   int tiled_bank_order = 1;        // bank-aware slot order inside slabs (tiled build)
+  int relabel = 1;                 // tiled build over a Cuthill-McKee relabelling of P: 0 off, 1 auto, 2 on
   int cols_per_block = 1;          // adjacent FFT columns per k_cols block (1, 2 or 4)
   int host_pieces = 0;             // fitsne_gradient_host: SpMV row pieces + overlapped copy-out
   fitsne::TiledP* tiled = nullptr; // built lazily from the registered CSR
+  fitsne::Comm* comm = nullptr;    // fitsne_comm_init
   double* kl_part = nullptr;       // where the last SpMV left its KL partials
   int kl_nparts = 0;
   cudaStream_t side = nullptr;     // repulsion stream (overlaps the attractive SpMV)

@@ -80,8 +80,10 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 // out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
 int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st);
 void free_tiled(fitsne_ctx* ctx);
+int comm_free(fitsne_ctx* ctx);  // comm.cu
 // the tiled F_attr buffer's consumer (which clears it) has been queued
 void tiled_consumed(fitsne_ctx* ctx);
+bool tiled_relabeled(const fitsne_ctx* ctx);  // the tiled copy runs over relabelled points
 // error exit of a multi-stream schedule: wait for the internal streams so no
 // queued work outlives the call (the next call reuses their buffers)
 int join_on_error(fitsne_ctx* ctx, int rc);
@@ -94,6 +96,10 @@ int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
 constexpr int kTiledPieces = 4;
 int attract_tiled_piece(fitsne_ctx* ctx, const void* Y, int piece, cudaStream_t st, void** fattr);
 void tiled_piece_rows(const fitsne_ctx* ctx, int64_t* rows);
+// Cuthill-McKee ordering of a symmetric CSR pattern (reorder.cu):
+// order[new] = old, pos_of[old] = new
+int cuthill_mckee(const int64_t* rowptr, const int32_t* col, int n, int* order, int* pos_of, int num_sms,
+                  cudaStream_t st);
 // fitsne_gradient_host (attract.cu)
 int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host, cudaStream_t st);
 int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st);

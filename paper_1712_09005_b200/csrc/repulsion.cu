@@ -169,6 +169,7 @@ int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
 }
 
 int bbox_wait(fitsne_ctx* ctx, double* bbox_host) {
+  FITSNE_RANGE("bbox_wait");
   const int S = ctx->dims;
   FITSNE_CUDA(cudaEventSynchronize(ctx->ev_bbox));
   if (ctx->h_scal[8 + 2 * S] != 0.0) {
@@ -324,6 +325,7 @@ int shadow_frep(fitsne_ctx* ctx, const void* Y, int64_t n, double** frep, cudaSt
 }
 
 int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
+  FITSNE_RANGE("install_grid");
   if (g.dims != ctx->dims) {
     set_error("grid dims do not match the context");
     return FITSNE_EINVAL;
@@ -348,7 +350,8 @@ int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
       FITSNE_TRY(install_grid(ctx->shadow, g, st));
       ctx->tw_gen += ctx->shadow->tw_gen - gen0;
       ctx->wide = true;
-      return FITSNE_OK;  // the fp32 stages of this context are not used for this grid
+      // the t-SNE stages run on the shadow; this context's own (fp32) FFT
+      // still serves the general n-body calls on the same grid
     }
   }
   if (ctx->tw_len != L) {
@@ -485,6 +488,7 @@ static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
 }
 
 int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
+  FITSNE_RANGE("spread");
   if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
   if (ctx->wide) {  // fp64 grid: a caller's accumulator is double (fitsne_grid_accum_dtype)
     const double* y = widen_points(ctx, Y, n, st);
@@ -1220,6 +1224,7 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
 }
 
 int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st) {
+  FITSNE_RANGE("fft_stage");
   if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
   if (ctx->wide) {
     FITSNE_TRY(fft_tsne(ctx->shadow, accum, n_total, with_k1, st));
@@ -1313,6 +1318,7 @@ __global__ void k_gather_tsne(const T* __restrict__ Y, int64_t n, GridArgs g,
 
 int gather_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces, void* k1, void* k2,
                 cudaStream_t st) {
+  FITSNE_RANGE("gather");
   GridArgs g = grid_args(ctx->grid);
   if (n <= 0) return FITSNE_OK;
   if (ctx->wide) {

@@ -166,7 +166,7 @@ def _embedding(Y, dtype):
 def _ctx_with_P(P, dev, dims, dt, p=3, min_int=20, ipi=1.0):
     csr = device_csr(P, dt, dev)
     ctx = _lib.context(dev, dims, dt, p, min_int, ipi)
-    ctx.set_affinities(csr)
+    ctx.set_affinities(csr, owner=P)
     return ctx, csr
 
 

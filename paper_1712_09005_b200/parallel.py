@@ -32,7 +32,7 @@ import torch.distributed as dist
 from . import _lib
 from .affinities import DeviceCSR, device_csr, n_points
 
-__all__ = ["shard_range", "LibStages", "ShardedGradient"]
+__all__ = ["shard_range", "LibStages", "ShardedGradient", "NcclGradient"]
 
 
 def shard_range(n: int, rank: int, world: int) -> tuple[int, int]:
@@ -308,3 +308,54 @@ class ShardedGradient:
                 st.check_z()  # the rest of the step is already queued
             return g
         return st.attract_rows(y_full, f_local, alpha)
+
+
+class NcclGradient:
+    """The sharded gradient run entirely inside the library over its own NCCL
+    communicator (fitsne_comm_init / fitsne_gradient_sharded): one C-ABI call
+    per evaluation, the same partition and collectives as ShardedGradient.
+    torch.distributed only carries the 128-byte NCCL id from rank 0."""
+
+    def __init__(self, P, n_dims=2, dtype=torch.float32, device=None, min_intervals=20,
+                 points_per_interval=3, intervals_per_integer=1.0, group=None):
+        self.group = group
+        self.rank = dist.get_rank(group)
+        self.world = dist.get_world_size(group)
+        self.n = n_points(P)
+        self.dims = n_dims
+        self.dtype = dtype
+        self.device = device
+        self.row_begin, self.row_end = shard_range(self.n, self.rank, self.world)
+        self.ctx = _lib.Context(device, n_dims, dtype, points_per_interval, min_intervals,
+                                intervals_per_integer)
+        self.csr = device_csr(P, dtype, device, self.row_begin, self.row_end)
+        self.ctx.set_affinities(self.csr)
+        uid = (C.c_char * 128)()
+        if self.rank == 0:
+            _lib.check(self.ctx.lib.fitsne_nccl_unique_id(uid), "fitsne_nccl_unique_id")
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (C.c_char * 128).from_buffer_copy(box[0])
+        _lib.check(self.ctx.lib.fitsne_comm_init(self.ctx.h, uid, self.rank, self.world, self.n),
+                   "fitsne_comm_init")
+
+    def local(self, y_full):
+        return y_full[self.row_begin:self.row_end]
+
+    def gradient(self, y_local, alpha: float = 1.0, out=None, z=None):
+        """Gradient rows of this rank (n_local, s); y_local are its own points."""
+        if alpha < 1.0:
+            raise ValueError("exaggeration alpha must be >= 1")
+        y_local = y_local.contiguous()
+        g = out if out is not None else torch.empty_like(y_local)
+        zc = C.c_double()
+        _lib.check(self.ctx.lib.fitsne_gradient_sharded(self.ctx.h, _lib.ptr(y_local), float(alpha),
+                                                        _lib.ptr(g), C.byref(zc), self.ctx.stream),
+                   "fitsne_gradient_sharded")
+        if z is not None:
+            z.append(float(zc.value))
+        return g
+
+    def close(self):
+        if getattr(self, "ctx", None) is not None:
+            self.ctx.lib.fitsne_comm_destroy(self.ctx.h)

@@ -127,3 +127,36 @@ def test_lib_stages_wide_fp32_uses_fp64_grid(nccl_group):
     assert sg.stages._acc.dtype == torch.float64
     ref = O.grad(P.rows, P.cols, P.values, y.astype(np.float64), 1.0, 50, 3, "fft")
     assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= 1e-3
+
+
+@pytest.mark.parametrize("dtype,tol", [(torch.float64, 1e-9), (torch.float32, 1e-4)])
+def test_native_nccl_sharded_gradient(nccl_group, dtype, tol):
+    """The library's own NCCL path (fitsne_comm_init + fitsne_gradient_sharded,
+    a single-rank communicator) equals the fused single-GPU gradient and the
+    oracle, with the tiled SpMV on its side stream."""
+    from paper_1712_09005_b200 import optimizer
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    from paper_1712_09005_b200.parallel import NcclGradient
+    rng = np.random.default_rng(12)
+    n, k = 40_000, 60
+    c = rng.uniform(-40, 40, (12, 2))
+    y = c[rng.integers(0, 12, n)] + 2 * rng.standard_normal((n, 2))
+    r = np.repeat(np.arange(n), k)
+    cc = rng.integers(0, n - 1, n * k)
+    cc = cc + (cc >= r)
+    key = np.unique(np.minimum(r, cc) * n + np.maximum(r, cc))
+    v = rng.exponential(1.0, key.size)
+    P = SparseAffinities(n=n, rows=key // n, cols=key % n, values=v / (2 * v.sum()))
+    sg = NcclGradient(P, n_dims=2, dtype=dtype, device=0, min_intervals=50)
+    yt = torch.from_numpy(y).to(device=0, dtype=dtype)
+    zs = []
+    for _ in range(3):  # repeated: accumulators consumed and cleared
+        g = sg.gradient(yt, alpha=4.0, z=zs).double().cpu().numpy()
+    ref = optimizer.gradient(P, yt, 4.0, 50, 3, "fft").double().cpu().numpy()
+    assert np.linalg.norm(g - ref) / np.linalg.norm(ref) <= tol
+    yo = y.astype(np.float32).astype(np.float64) if dtype == torch.float32 else y
+    o = O.grad(P.rows, P.cols, P.values, yo, 4.0, 50, 3, "fft")
+    assert np.linalg.norm(g - o) / np.linalg.norm(o) <= (1e-3 if dtype == torch.float32 else 1e-9)
+    _, z_o, _, _ = O.repulsion(yo, 50, 3, "fft")
+    assert abs(zs[-1] - z_o) <= 1e-5 * z_o
+    sg.close()

@@ -16,7 +16,11 @@ from oracle import fitsne_oracle as O
 pytestmark = pytest.mark.gpu
 
 
-def _spread(y, dtype, sorted_on, dims, mode=None):
+def _spread(y, dtype, sorted_on, dims, mode=None, grid_f64=0):
+    """Spread through fitsne_spread_tsne into a caller's accumulator.  The
+    fp32 spread kernels are tested with the fp32 grid pipeline (grid_f64=0);
+    grid_f64=2 routes an fp32 context through its fp64 twin (double
+    accumulator, fitsne_grid_accum_dtype)."""
     from paper_1712_09005_b200 import _lib
     dt = torch.float32 if dtype == "float32" else torch.float64
     yt = torch.from_numpy(np.ascontiguousarray(y)).to(device=0, dtype=dt)
@@ -24,9 +28,12 @@ def _spread(y, dtype, sorted_on, dims, mode=None):
     if mode is None:
         mode = 2 if sorted_on else 0
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, mode))
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_GRID_F64, grid_f64))
     g = _lib.Grid()
     _lib.check(ctx.lib.fitsne_make_grid(ctx.h, _lib.ptr(yt), yt.shape[0], C.byref(g), ctx.stream))
-    acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=dt, device=0)
+    adt = torch.float64 if ctx.lib.fitsne_grid_accum_dtype(ctx.h) == _lib.F64 else torch.float32
+    wide = adt != dt
+    acc = torch.zeros(int(ctx.lib.fitsne_grid_accum_len(ctx.h)), dtype=adt, device=0)
     _lib.check(ctx.lib.fitsne_spread_tsne(ctx.h, _lib.ptr(yt), yt.shape[0], _lib.ptr(acc), ctx.stream))
     torch.cuda.synchronize()
     a = acc.reshape(-1, 4).cpu().numpy().astype(np.float64)
@@ -35,7 +42,7 @@ def _spread(y, dtype, sorted_on, dims, mode=None):
     # reference's bincount layout
     for d in range(dims):
         c = 0.5 * (g.lo[d] + g.hi[d])
-        c = float(np.float32(c)) if dtype == "float32" else c
+        c = float(np.float32(c)) if dtype == "float32" and not wide else c
         a[:, 1 + d] += c * a[:, 0]
     return a, g
 
@@ -87,6 +94,17 @@ def test_sorted_spread_large_grid_radix_path(cuda, dtype):
     tol = 1e-12 if dtype == "float64" else 5e-4
     for c in range(3):
         assert rel_inf(a[:, c], ref[:, c]) <= tol, c
+
+
+def test_wide_fp32_spread_into_double_accumulator(cuda):
+    """An fp32 context with the fp64 grid pipeline (FITSNE_OPT_GRID_F64 = 2)
+    reports a double accumulator and fills it with the fp64 spread."""
+    rng = np.random.default_rng(10)
+    y = rng.uniform(-200, 200, (60_000, 2)).astype(np.float32).astype(np.float64)
+    a, g = _spread(y, "float32", True, 2, mode=1, grid_f64=2)
+    ref = _oracle(y, g, 2)
+    for c in range(3):
+        assert rel_inf(a[:, c], ref[:, c]) <= 1e-12, c
 
 
 BAND_CASES = dict(CASES)

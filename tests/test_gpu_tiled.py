@@ -255,7 +255,7 @@ def test_random_graph_keeps_csr_kernel(cuda):
     assert 2 * rr.size >= (1 << 22)
     csr = _csr(n, rr, cc, v)
     y = torch.from_numpy(Y.astype(np.float32)).cuda()
-    st = (C.c_int64 * 6)()
+    st = (C.c_int64 * 8)()
     ctx = _ctx(1, 3072, 8192)
     ctx.set_affinities(csr)
     _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), st, ctx.stream), "stats")
@@ -289,3 +289,65 @@ def test_one_dim_gradient_at_scale(cuda, dtype, tol):
                            50, 3, "fft").double().cpu().numpy()
     want = O.grad(P.rows, P.cols, P.values, yd, 12.0, 50, 3, "fft")
     assert rel_l2(g, want) <= tol
+
+
+def _shuffled(n, rr, cc, v, Y, seed):
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n)
+    inv = np.empty(n, dtype=np.int64)
+    inv[perm] = np.arange(n)
+    r, c = inv[rr], inv[cc]
+    return np.minimum(r, c), np.maximum(r, c), v, Y[perm]
+
+
+@pytest.mark.parametrize("relabel", [1, 2])
+@pytest.mark.parametrize("shape", [(64, 128, 0), (256, 1024, 7), (2, 2, 3)])
+def test_relabelled_tiles_on_shuffled_graph(cuda, relabel, shape):
+    """A clustered graph in random point order: the tiled copy built over the
+    device Cuthill-McKee relabelling (FITSNE_OPT_RELABEL) gives the oracle's
+    F_attr in the caller's order; auto mode takes the relabelling because it
+    cuts the (row, chunk) segments."""
+    from paper_1712_09005_b200 import _lib
+    n = 5003
+    rr, cc, v, Y = _shuffled(n, *_graph(n, 24, 11), seed=5)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    ctx = _ctx(2, *shape)
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, relabel), "set_option")
+    got = _attr(ctx, _csr(n, rr, cc, v), y)
+    st = (C.c_int64 * 8)()
+    _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), st, ctx.stream), "stats")
+    assert st[0] == 1 and st[6] == 1
+    assert st[4] <= 0.9 * st[7] or relabel == 2
+    ref = O.attraction(rr, cc, v, Y.astype(np.float32).astype(np.float64))
+    assert rel_l2(got, ref) <= 1e-5
+
+
+def test_relabel_off_keeps_caller_order(cuda):
+    from paper_1712_09005_b200 import _lib
+    n = 3001
+    rr, cc, v, Y = _shuffled(n, *_graph(n, 16, 12), seed=6)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    ctx = _ctx(2, 64, 128)
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, 0), "set_option")
+    got = _attr(ctx, _csr(n, rr, cc, v), y)
+    st = (C.c_int64 * 8)()
+    _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), st, ctx.stream), "stats")
+    assert st[0] == 1 and st[6] == 0
+    assert rel_l2(got, O.attraction(rr, cc, v, Y.astype(np.float32).astype(np.float64))) <= 1e-5
+
+
+def test_relabelled_gradient_and_iterate(cuda):
+    """The overlapped gradient (tiled SpMV on relabelled points, combine in
+    the caller's order) and the fused run_tsne iteration on a shuffled graph."""
+    from paper_1712_09005_b200 import _lib, optimizer
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    n = 20_000
+    rr, cc, v, Y = _shuffled(n, *_graph(n, 30, 13), seed=7)
+    P = SparseAffinities(n=n, rows=rr, cols=cc, values=v)
+    y32 = Y.astype(np.float32)
+    with _lib.option(OPT_TILED, 2), _lib.option(_lib.OPT_RELABEL, 2):
+        g = optimizer.gradient(P, torch.from_numpy(y32).cuda(), 12.0, 50, 3, "fft")
+        g_host = optimizer.gradient(P, y32, 12.0, 50, 3, "fft")
+    ref = O.grad(rr, cc, v, y32.astype(np.float64), 12.0, 50, 3, "fft")
+    assert rel_l2(g.double().cpu().numpy(), ref) <= 1e-3
+    assert rel_l2(g_host, ref) <= 1e-3

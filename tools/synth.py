@@ -177,6 +177,19 @@ class Upper:
         return 2.0 * float(self.values.sum())
 
 
+def shuffle(P, Y, seed=0):
+    """The same (P, Y) with the points in a random order (upper COO kept
+    rows < cols): real data arrive in no cluster order."""
+    n = int(P.n)
+    rng = np.random.default_rng(seed)
+    perm = rng.permutation(n)            # new i <- old perm[i]
+    inv = np.empty(n, dtype=np.int64)
+    inv[perm] = np.arange(n)
+    r, c = inv[P.rows], inv[P.cols]
+    lo, hi = np.minimum(r, c), np.maximum(r, c)
+    return Upper(n, lo, hi, P.values), np.ascontiguousarray(Y[perm])
+
+
 def c3(device="cuda", n=1_300_000, seed=3):
     """Config 3 inputs: (P upper COO numpy holder, Y (n, 2) float64 numpy)."""
     X, _ = mixture(n, 50, 40, seed, anisotropic=True, power=1.5, device=device)

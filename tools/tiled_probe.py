@@ -71,7 +71,7 @@ def main():
         build = time.time() - tb
         if mode:
             import ctypes
-            st = (ctypes.c_int64 * 6)()
+            st = (ctypes.c_int64 * 8)()
             _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), st, ctx.stream), "stats")
             print(f"  tiles {st[1]} slabs {st[2]} groups {st[3]} segments {st[4]} nnz {st[5]}: "
                   f"entries/segment {st[5] / max(st[4], 1):.2f} groups/slab {st[3] / max(st[2], 1):.2f} "
