@@ -138,8 +138,8 @@ enum fitsne_option {
  *   FITSNE_OPT_RELABEL: the tiled copy of P over a Cuthill-McKee relabelling
  *   of the points computed from P's pattern on the device (components and
  *   neighbourhoods get contiguous labels; results stay in the caller's
- *   order).  0 = caller's order; 1 (default) = relabel when that cuts the
- *   (row, column chunk) segments of the tiles by >= 10%; 2 = always. */
+ *   order).  0 = caller's order; 1 (default) = relabel when that at least
+ *   halves the (row, column chunk) segments of the tiles; 2 = always. */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
  * only for its alignment): out[0..7] = {in use (0/1), tiles, slabs, slot
