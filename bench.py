@@ -51,6 +51,13 @@ WORKLOADS = {
     "c3": dict(n=1_300_000, desc="C3: N=1.3M, d=50 40-cluster anisotropic power-law mixture, "
                                  "exact kNN k=90, perplexity 30, symmetric CSR P; 2-D Y = "
                                  "top-2 PCA of X scaled to |y|<=100; min_intervals 50, p 3"),
+    "c4": dict(n=10_000_000, desc="C4: N=10M 2-D, Y = 100 blobs (centres U[-100,100]^2, std 2, "
+                                  "Dirichlet sizes); P = random kNN graph, 45 partners per row "
+                                  "union-symmetrised (~90/row, 900M stored entries), Exp(1) "
+                                  "weights; min_intervals 50, p 3"),
+    "c5": dict(n=1_000_000, desc="C5: N=1M, d=50 30-cluster mixture, exact kNN k=90, perplexity "
+                                 "30; 1-D Y = top PCA direction scaled to |y|<=150; "
+                                 "min_intervals 50, p 3"),
 }
 
 
@@ -68,6 +75,10 @@ def parse():
                     help="also time the complete 1000-iteration C3 t-SNE run (run_tsne, fused "
                          "device iterations, late exaggeration 4 from 750) and report it")
     ap.add_argument("--seed", type=int, default=3)
+    ap.add_argument("--inputs-cache", default=None,
+                    help="A/B runs: load the seeded inputs from this .npz (written on first use)")
+    ap.add_argument("--workload", default="c3", choices=sorted(WORKLOADS),
+                    help="BASELINE config (c3 = the headline metric's; c4 / c5 for the record)")
     ap.add_argument("--shuffle", action="store_true",
                     help="randomly permute the C3 point order (real data arrive in no cluster "
                          "order; the library relabels P internally, FITSNE_OPT_RELABEL)")
@@ -191,9 +202,25 @@ def make_inputs(args, device):
     """Seeded C3 inputs (P upper COO holder, Y float64 (N, 2))."""
     import torch
     from tools import synth
-    n = args.n or WORKLOADS["c3"]["n"]
+    wl = getattr(args, "workload", "c3")
+    n = args.n or WORKLOADS[wl]["n"]
     t0 = time.time()
-    P, Y = synth.c3(device=device, n=n, seed=args.seed)
+    cache = getattr(args, "inputs_cache", None)
+    if cache and wl != "c4" and Path(cache).exists():
+        with np.load(cache) as z:
+            P = synth.Upper(int(z["n"]), z["rows"], z["cols"], z["values"])
+            Y = z["Y"]
+        if getattr(args, "shuffle", False):
+            P, Y = synth.shuffle(P, Y, seed=args.seed + 1000)
+        return P, Y, time.time() - t0
+    if wl == "c4":
+        P, Y = synth.c4(device=device, n=n, seed=4)
+    elif wl == "c5":
+        P, Y = synth.c5(device=device, n=n, seed=5)
+    else:
+        P, Y = synth.c3(device=device, n=n, seed=args.seed)
+    if cache and wl != "c4":
+        np.savez(cache, n=P.n, rows=P.rows, cols=P.cols, values=P.values, Y=Y)
     if getattr(args, "shuffle", False):
         P, Y = synth.shuffle(P, Y, seed=args.seed + 1000)
     torch.cuda.synchronize() if str(device).startswith("cuda") else None
@@ -285,7 +312,7 @@ def run_reference(args):
     val = 1.0 / sec
     line = {
         "impl": "reference",
-        "metric": "t-SNE gradient evals/sec at N=1.3M 2-D",
+        "metric": metric_name(int(P.n), int(Y.shape[1])),
         "value": val, "unit": "grad_evals/s", "n_gpus": args.gpus, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": sec * 1e3, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -299,6 +326,12 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def metric_name(n, dims):
+    if n == 1_300_000 and dims == 2:
+        return "t-SNE gradient evals/sec at N=1.3M 2-D"
+    return f"t-SNE gradient evals/sec at N={n / 1e6:g}M {dims}-D"
+
+
 def cpu_model():
     try:
         for ln in Path("/proc/cpuinfo").read_text().splitlines():
@@ -309,8 +342,11 @@ def cpu_model():
     return None
 
 
+_WL = ["c3"]
+
+
 def workload_config(P, **extra):
-    cfg = {"workload": WORKLOADS["c3"]["desc"], "N": int(P.n), "nnz_full": int(2 * P.rows.size),
+    cfg = {"workload": WORKLOADS[_WL[0]]["desc"], "N": int(P.n), "nnz_full": int(2 * len(P.rows)),
            "min_intervals": 50, "points_per_interval": 3, "alpha": 1.0}
     cfg.update(extra)
     return cfg
@@ -383,12 +419,12 @@ def run_ours(args):
         from paper_1712_09005_b200 import parallel
         if args.torch_comm:
             # Python orchestration over torch.distributed (parallel.ShardedGradient)
-            ev = parallel.ShardedGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
-                                          points_per_interval=3)
+            ev = parallel.ShardedGradient(P, n_dims=int(Y.shape[1]), dtype=dt, device=dev,
+                                          min_intervals=50, points_per_interval=3)
         else:
             # the library's own NCCL communicator: one C-ABI call per step
-            ev = parallel.NcclGradient(P, n_dims=2, dtype=dt, device=dev, min_intervals=50,
-                                       points_per_interval=3)
+            ev = parallel.NcclGradient(P, n_dims=int(Y.shape[1]), dtype=dt, device=dev,
+                                       min_intervals=50, points_per_interval=3)
         y_full = torch.from_numpy(Y).to(device=dev, dtype=dt)
         y_local = ev.local(y_full).contiguous()
         g_buf = torch.empty_like(y_local)
@@ -447,7 +483,7 @@ def run_ours(args):
         peak, peak_src = peaks()
         if rank == 0:
             line = {
-                "metric": "t-SNE gradient evals/sec at N=1.3M 2-D", "value": 1e3 / ms,
+                "metric": metric_name(n, int(Y.shape[1])), "value": 1e3 / ms,
                 "unit": "grad_evals/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "f32" if dt == torch.float32 else "f64",
@@ -481,7 +517,8 @@ def run_ours(args):
     # ---- single GPU -----------------------------------------------------------
     y = torch.from_numpy(Y).to(device=dev, dtype=dt)
     csr = device_csr(P, dt, dev)
-    ctx = _lib.context(dev, 2, dt, 3, 50, 1.0)
+    dims = int(Y.shape[1])
+    ctx = _lib.context(dev, dims, dt, 3, 50, 1.0)
     ctx.set_affinities(csr)
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 1, args.spread_mode), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 2, args.overlap_mode), "set_option")
@@ -520,7 +557,7 @@ def run_ours(args):
         spmv()
     ms_spmv = timed(spmv, args.steps, stream)
     es = 4 if dt == torch.float32 else 8
-    s = 2
+    s = dims
     # algorithmic bytes: col (4) + val per nnz, int64 rowptr, Y read once (L2-resident
     # neighbour reads counted once), F_rep in, gradient out
     b_spmv = nnz * (4 + es) + 8 * (n + 1) + 3 * s * es * n
@@ -555,8 +592,8 @@ def run_ours(args):
     g_host = torch.empty_like(y_host).pin_memory()
     api = lambda: optimizer.gradient(P, y_host, 1.0, 50, 3, "fft", out=g_host)  # noqa: E731
     api()
-    _lib.check(_lib.context(dev, 2, dt, 3, 50, 1.0).lib.fitsne_set_option(
-        _lib.context(dev, 2, dt, 3, 50, 1.0).h, 10, args.host_schedule), "set_option")
+    _lib.check(_lib.context(dev, dims, dt, 3, 50, 1.0).lib.fitsne_set_option(
+        _lib.context(dev, dims, dt, 3, 50, 1.0).h, 10, args.host_schedule), "set_option")
     # host-side warm-up (CPU clocks, page tables of the pinned buffers): the
     # e2e call is host-synchronised, so a cold host shows up in the timing
     for _ in range(max(args.warmup, 30)):
@@ -578,10 +615,11 @@ def run_ours(args):
     # the other two kernels the north star names (spread, gather), each timed
     # alone on the whole GPU, against SURVEY 8(d)'s algorithmic bytes
     breakdown = stage_breakdown(ctx, y, n, dt, args.steps, stream)
-    G = int(gr.nodes_per_dim) ** 2
+    G = int(gr.nodes_per_dim) ** dims
     fb = es  # float bytes
-    stage_bytes = {"spread": 2 * fb * n + 3 * fb * G,           # B_spread = 4sN + 4CG
-                   "gather": 2 * fb * n + 3 * fb * G + 2 * fb * n}  # B_gather = 4sN + 4KG + 4sN
+    C_ = dims + 1
+    stage_bytes = {"spread": dims * fb * n + C_ * fb * G,                  # B_spread = 4sN + 4CG
+                   "gather": dims * fb * n + C_ * fb * G + dims * fb * n}  # B_gather = 4sN + 4KG + 4sN
     stages = {}
     for k, b in stage_bytes.items():
         t = breakdown[k]
@@ -597,7 +635,7 @@ def run_ours(args):
     stages["fft_conv"] = {"ms": breakdown["fft_conv"],
                           "kernels": "k_rows_forward + k_spec_cols + k_cols + k_rows_inverse"}
     stages["fft_conv"]["cufft"] = cufft_reference(int(gr.nodes_per_dim), int(gr.fft_len), dt,
-                                                  args.steps, stream)
+                                                  args.steps, stream, dims)
 
     # CPU baseline: one whole evaluation of the reference's CPU gradient on the
     # same (P, Y) -- and the parity check of this run's gradient against it
@@ -619,7 +657,7 @@ def run_ours(args):
                  "path": "the timed step (fitsne_gradient, production schedule)"}
 
     line = {
-        "metric": "t-SNE gradient evals/sec at N=1.3M 2-D",
+        "metric": metric_name(n, dims),
         "value": 1e3 / ms, "unit": "grad_evals/s", "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f32" if dt == torch.float32 else "f64", "data": "synthetic",
@@ -634,7 +672,7 @@ def run_ours(args):
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src, "algorithmic_bytes": b_spmv,
                      "launch_ms": ms_spmv, "share_of_step": ms_spmv / ms,
-                     "traffic": traffic_from_profiles(traffic_key)},
+                     "traffic": traffic_from_profiles(traffic_key) if args.workload == "c3" else None},
         "cpu_baseline": cpu,
         "check": check,
         "e2e": {"value": 1e3 / ms_e2e, "unit": "grad_evals/s",
@@ -678,7 +716,7 @@ def full_run(P, dt, dev, n_iter=1000, reorder=True):
             "note": "wall clock of run_tsne incl. one bbox readback per iteration"}
 
 
-def cufft_reference(n, L, dt, steps, stream):
+def cufft_reference(n, L, dt, steps, stream, dims=2):
     """cuFFT (through torch.fft) doing the FFT work of one evaluation's
     convolution stage at the same L: one spectrum transform of the packed
     kernels (K1 + i K2), two forward transforms of the packed charge pairs,
@@ -689,24 +727,35 @@ def cufft_reference(n, L, dt, steps, stream):
     cd = torch.complex64 if dt == torch.float32 else torch.complex128
     rd = torch.float32 if dt == torch.float32 else torch.float64
     g = torch.Generator(device="cuda").manual_seed(0)
-    kern = torch.randn(L, L, dtype=cd, device="cuda", generator=g)
-    w = torch.zeros(2, L, L, dtype=cd, device="cuda")
-    w[:, :n, :n] = torch.randn(2, n, n, dtype=cd, device="cuda", generator=g)
-    kr = torch.randn(2, L, L, dtype=rd, device="cuda", generator=g)
-    wr = torch.zeros(3, L, L, dtype=rd, device="cuda")
-    wr[:, :n, :n] = torch.randn(3, n, n, dtype=rd, device="cuda", generator=g)
+    shp = (L, L) if dims == 2 else (L,)
+    kern = torch.randn(*shp, dtype=cd, device="cuda", generator=g)
+    w = torch.zeros(2, *shp, dtype=cd, device="cuda")
+    kr = torch.randn(2, *shp, dtype=rd, device="cuda", generator=g)
+    wr = torch.zeros(3, *shp, dtype=rd, device="cuda")
+    if dims == 2:
+        w[:, :n, :n] = torch.randn(2, n, n, dtype=cd, device="cuda", generator=g)
+        wr[:, :n, :n] = torch.randn(3, n, n, dtype=rd, device="cuda", generator=g)
+    else:
+        w[:, :n] = torch.randn(2, n, dtype=cd, device="cuda", generator=g)
+        wr[:, :n] = torch.randn(3, n, dtype=rd, device="cuda", generator=g)
+    fwd = torch.fft.fft2 if dims == 2 else torch.fft.fft
+    inv = torch.fft.ifft2 if dims == 2 else torch.fft.ifft
+    rfwd = torch.fft.rfft2 if dims == 2 else torch.fft.rfft
     out = {}
 
     def c2c():
-        kh = torch.fft.fft2(kern)
-        W = torch.fft.fft2(w)
-        torch.fft.ifft2(W)
+        kh = fwd(kern)
+        W = fwd(w)
+        inv(W)
         return kh
 
     def r2c():
-        kh = torch.fft.rfft2(kr)
-        W = torch.fft.rfft2(wr)
-        torch.fft.irfft2(W, s=(L, L))
+        kh = rfwd(kr)
+        W = rfwd(wr)
+        if dims == 2:
+            torch.fft.irfft2(W, s=(L, L))
+        else:
+            torch.fft.irfft(W, n=L)
         return kh
 
     for name, fn in (("c2c_5_transforms_ms", c2c), ("r2c_c2r_8_transforms_ms", r2c)):
@@ -714,7 +763,8 @@ def cufft_reference(n, L, dt, steps, stream):
             fn()
         out[name] = timed(fn, steps, stream)
     out["L"] = L
-    out["note"] = "torch.fft (cuFFT) on pre-padded L x L inputs; transform time only"
+    out["note"] = ("torch.fft (cuFFT) on pre-padded %s inputs; transform time only" %
+                   ("L x L" if dims == 2 else "length-L"))
     return out
 
 
@@ -742,6 +792,9 @@ def stage_breakdown(ctx, y, n, dt, steps, stream):
 
 def main():
     args = parse()
+    _WL[0] = args.workload
+    if args.workload != "c3":
+        args.no_cpu_baseline = args.no_cpu_baseline or args.workload == "c4"
     if args.impl == "reference":
         run_reference(args)
     else:

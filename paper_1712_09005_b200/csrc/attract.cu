@@ -53,6 +53,39 @@ __device__ __forceinline__ void load_point(const T* __restrict__ Y, int64_t j, T
   }
 }
 
+// Neighbour gathers with an L2 evict-last hint: the CSR stream (8-12 B per
+// entry, read once) is loaded evict-first, so at large N (C4: Y is 80 MB,
+// the stream 7 GB) the embedding stays resident in the 126 MB L2 instead of
+// being pushed out by the stream it is gathered against.
+__device__ __forceinline__ uint64_t l2_evict_last_policy() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <typename T, int S>
+__device__ __forceinline__ void load_point_el(const T* __restrict__ Y, int64_t j, T (&v)[S], uint64_t pol) {
+  if constexpr (S == 2 && sizeof(T) == 4) {
+    float a, b;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;"
+                 : "=f"(a), "=f"(b) : "l"(Y + 2 * j), "l"(pol));
+    v[0] = a; v[1] = b;
+  } else if constexpr (S == 2) {
+    double a, b;
+    asm volatile("ld.global.nc.L2::cache_hint.v2.f64 {%0, %1}, [%2], %3;"
+                 : "=d"(a), "=d"(b) : "l"(Y + 2 * j), "l"(pol));
+    v[0] = a; v[1] = b;
+  } else if constexpr (sizeof(T) == 4) {
+    float a;
+    asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(a) : "l"(Y + j), "l"(pol));
+    v[0] = a;
+  } else {
+    double a;
+    asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(a) : "l"(Y + j), "l"(pol));
+    v[0] = a;
+  }
+}
+
 // p / (1 + d2): fp32 uses the fast reciprocal-based division (<= 2 ulp, well
 // inside the fp32 parity bar); fp64 keeps IEEE division.
 template <typename T>
@@ -69,7 +102,8 @@ __device__ __forceinline__ float cauchy_weight<float>(float p, float d2) {
 template <typename T, int S, bool KL>
 __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, const T* __restrict__ val,
                                            const T* __restrict__ Y, int64_t beg, int64_t end,
-                                           int lane, const T (&yi)[S], T (&acc)[S], T& klr) {
+                                           int lane, const T (&yi)[S], T (&acc)[S], T& klr,
+                                           uint64_t pol) {
   constexpr int kU = 4;
   for (int64_t k0 = beg + lane; k0 < end; k0 += 32 * kU) {
     int32_t j[kU];
@@ -78,13 +112,13 @@ __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, cons
     for (int u = 0; u < kU; ++u) {
       const int64_t k = k0 + 32 * u;
       const bool ok = k < end;
-      j[u] = ok ? __ldg(col + k) : 0;
-      p[u] = ok ? __ldg(val + k) : (T)0;
+      j[u] = ok ? __ldcs(col + k) : 0;
+      p[u] = ok ? __ldcs(val + k) : (T)0;
     }
     T yj[kU][S];
 #pragma unroll
     for (int u = 0; u < kU; ++u) {
-      if (k0 + 32 * u < end) load_point<T, S>(Y, j[u], yj[u]);
+      if (k0 + 32 * u < end) load_point_el<T, S>(Y, j[u], yj[u], pol);
       else {
 #pragma unroll
         for (int d = 0; d < S; ++d) yj[u][d] = yi[d];
@@ -136,6 +170,7 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
   double kl = 0.0;
   T Z = (T)1;
   if (MODE == 2) Z = (T)scal[0];
+  const uint64_t pol = l2_evict_last_policy();
   for (int64_t t = warp; t < ntiles; t += nwarps) {
     const int64_t r_mine = t * 32 + lane;
     const bool valid = r_mine < n_rows;
@@ -166,7 +201,7 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
 #pragma unroll
       for (int d = 0; d < S; ++d) acc[d] = 0;
       T klr = 0;
-      row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr);
+      row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr, pol);
 #pragma unroll
       for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
       if (lane == m) {
@@ -426,88 +461,6 @@ int step_update(fitsne_ctx* ctx, void* Y, const void* grad, void* vel, void* gai
                                                   (double*)gains, m, momentum, lr);
   FITSNE_CHECK_LAUNCH();
   return FITSNE_OK;
-}
-
-// ---------------------------------------------------------------------------
-// fused iteration: gather + SpMV + KL partial + gradient + update + next-Y finiteness
-// ---------------------------------------------------------------------------
-template <typename T, int S, int P>
-__global__ void __launch_bounds__(kBlock)
-k_iterate(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
-          const T* __restrict__ val, const T* __restrict__ Y, int64_t n, GridArgs gr,
-          const T* __restrict__ pot, const double* __restrict__ scal,
-          T alpha, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel, T* __restrict__ gains,
-          double* __restrict__ klpart, int32_t* __restrict__ status) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-  const int64_t ntiles = (n + 31) >> 5;
-  const T Z = (T)scal[0];
-  double kl = 0.0;
-  int bad = 0;
-  for (int64_t t = warp; t < ntiles; t += nwarps) {
-    const int64_t i_mine = t * 32 + lane;
-    const bool valid = i_mine < n;
-    T ym[S], fr[S], res[S];
-#pragma unroll
-    for (int d = 0; d < S; ++d) { ym[d] = 0; fr[d] = 0; res[d] = 0; }
-    int64_t rb = 0, re = 0;
-    if (valid) {
-      load_point<T, S>(Y, i_mine, ym);
-      rb = rowptr[i_mine];
-      re = rowptr[i_mine + 1];
-      T phi[4];
-      point_gather<T, S, P>(ym, gr, pot, phi);
-#pragma unroll
-      for (int d = 0; d < S; ++d) fr[d] = frep_from_phi<T, S>(ym, phi, Z, d, gr);
-    }
-    const int mcount = (n - t * 32 < 32) ? (int)(n - t * 32) : 32;
-    for (int m = 0; m < mcount; ++m) {
-      T yi[S];
-#pragma unroll
-      for (int d = 0; d < S; ++d) yi[d] = __shfl_sync(0xffffffffu, ym[d], m);
-      const int64_t beg = __shfl_sync(0xffffffffu, rb, m);
-      const int64_t end = __shfl_sync(0xffffffffu, re, m);
-      T acc[S];
-#pragma unroll
-      for (int d = 0; d < S; ++d) acc[d] = 0;
-      T klr = 0;
-      row_reduce<T, S, true>(col, val, Y, beg, end, lane, yi, acc, klr);
-#pragma unroll
-      for (int d = 0; d < S; ++d) {
-        acc[d] = warp_sum(acc[d]);
-        if (lane == m) res[d] = acc[d];
-      }
-      kl += (double)klr;
-    }
-    if (valid) {
-#pragma unroll
-      for (int d = 0; d < S; ++d) {
-        const int64_t o = i_mine * S + d;
-        T g = (T)4 * (alpha * res[d] - fr[d]);
-        if (!isfinite(g)) bad |= 1;
-        T v = vel[o], gn = gains[o];
-        bool agree = npsign(g) == npsign(v);
-        T vn = momentum * v - lr * gn * g;
-        T ynew = ym[d] + vn;
-        if (!isfinite(ynew)) bad |= 2;
-        vel[o] = vn;
-        Yout[o] = ynew;
-        T ng = agree ? gn * (T)0.8 : gn + (T)0.2;
-        gains[o] = ng < (T)0.01 ? (T)0.01 : ng;
-      }
-    }
-  }
-  __shared__ double red[kBlock / 32];
-  kl = warp_sum(kl);
-  if (lane == 0) red[threadIdx.x >> 5] = kl;
-  bad = __syncthreads_or(bad);
-  if (threadIdx.x == 0) {
-    double s = 0;
-    for (int w = 0; w < kBlock / 32; ++w) s += red[w];
-    klpart[blockIdx.x] = s;
-    if (bad && status) atomicOr(status, bad);
-  }
 }
 
 // KL = plogp + sum p log1p(d^2) + psum log Z  -> dst

@@ -18,7 +18,8 @@
 //
 // Cells and weights come from box_weights3_f32 exactly as in k_spread_tsne
 // (bit-exact cells); only the summation order differs.
-#include <cub/cub.cuh>
+#include <mutex>
+#include <set>
 
 #include "common.cuh"
 #include "internal.h"
@@ -75,9 +76,15 @@ __device__ __forceinline__ void band_weights(float u, float* w) {
   w[2] = 0.5f * u * d1;
 }
 
-// per-block histogram of box rows -> counts[row * nblk + block]
+// Two-pass binning by box row without a device-wide scan: pass 1 adds each
+// block's row histogram into global row totals; pass 2 recomputes its
+// histogram, takes the exclusive scan of the (<= 1024) row totals in shared
+// memory, reserves a contiguous range inside each of its rows with one atomic
+// per (block, row), and scatters.  (The order of blocks inside a row is
+// arbitrary; the reduce pass sorts each piece by box anyway, and the grid
+// accumulation is an unordered sum of float reductions already.)
 __global__ void __launch_bounds__(kBandBlock)
-k_band_count(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* __restrict__ counts) {
+k_band_rowcount(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* __restrict__ rowtot) {
   __shared__ uint32_t hist[kBandMaxRows];
   for (int r = threadIdx.x; r < g.n_int; r += kBandBlock) hist[r] = 0;
   __syncthreads();
@@ -89,23 +96,70 @@ k_band_count(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* __re
   }
   __syncthreads();
   for (int r = threadIdx.x; r < g.n_int; r += kBandBlock)
-    counts[(size_t)r * gridDim.x + blockIdx.x] = hist[r];
+    if (hist[r]) atomicAdd(rowtot + r, hist[r]);
 }
 
-// scatter the points into box-row order (offsets = exclusive scan of counts)
 __global__ void __launch_bounds__(kBandBlock)
-k_band_scatter(const float2* __restrict__ Y, int64_t n, GridArgs g,
-               const uint32_t* __restrict__ offsets, float2* __restrict__ sorted) {
-  __shared__ uint32_t base[kBandMaxRows];
-  for (int r = threadIdx.x; r < g.n_int; r += kBandBlock)
-    base[r] = offsets[(size_t)r * gridDim.x + blockIdx.x];
+k_band_place(const float2* __restrict__ Y, int64_t n, GridArgs g, const uint32_t* __restrict__ rowtot,
+             uint32_t* __restrict__ rowcur, float2* __restrict__ sorted) {
+  __shared__ uint32_t hist[kBandMaxRows];
+  __shared__ uint32_t start[kBandMaxRows];
+  __shared__ uint32_t part[kBandBlock];
+  const int ni = g.n_int, tid = threadIdx.x;
+  for (int r = tid; r < ni; r += kBandBlock) hist[r] = 0;
   __syncthreads();
   const int64_t p0 = blockIdx.x * (int64_t)kBandPts;
   const int64_t p1 = min(n, p0 + kBandPts);
-  for (int64_t i = p0 + threadIdx.x; i < p1; i += kBandBlock) {
+  for (int64_t i = p0 + tid; i < p1; i += kBandBlock) {
+    float w[3];
+    atomicAdd(&hist[band_cell(Y[i].x, g, 0, w)], 1u);
+  }
+  // exclusive scan of the row totals: kBandMaxRows / kBandBlock per thread
+  constexpr int E = kBandMaxRows / kBandBlock;
+  uint32_t loc[E], run = 0;
+#pragma unroll
+  for (int e = 0; e < E; ++e) {
+    const int r = tid * E + e;
+    loc[e] = run;
+    run += r < ni ? rowtot[r] : 0u;
+  }
+  part[tid] = run;
+  __syncthreads();
+  if (tid < 32) {
+    uint32_t v[kBandBlock / 32], t = 0;
+#pragma unroll
+    for (int j = 0; j < kBandBlock / 32; ++j) {
+      v[j] = part[tid * (kBandBlock / 32) + j];
+      t += v[j];
+    }
+    uint32_t x = t;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+      if ((tid & 31) >= o) x += y;
+    }
+    uint32_t ex = x - t;
+#pragma unroll
+    for (int j = 0; j < kBandBlock / 32; ++j) {
+      const uint32_t vj = v[j];
+      part[tid * (kBandBlock / 32) + j] = ex;
+      ex += vj;
+    }
+  }
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < E; ++e) start[tid * E + e] = loc[e] + part[tid];
+  __syncthreads();
+  // this block's range inside each row it touches
+  for (int r = tid; r < ni; r += kBandBlock)
+    if (hist[r]) hist[r] = start[r] + atomicAdd(rowcur + r, hist[r]);
+  __syncthreads();
+  for (int64_t i = p0 + tid; i < p1; i += kBandBlock) {
     const float2 y = Y[i];
     float w[3];
-    sorted[atomicAdd(&base[band_cell(y.x, g, 0, w)], 1u)] = y;
+    const uint32_t at = atomicAdd(&hist[band_cell(y.x, g, 0, w)], 1u);
+    FITSNE_DCHECK(at < n);
+    sorted[at] = y;
   }
 }
 
@@ -173,6 +227,7 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
     float2 uv;
     const int cx = band_cell_u(y.x, g, 0, &uv.x), cy = band_cell_u(y.y, g, 1, &uv.y);
     const int key = (cx - cx0) * ni + cy;
+    FITSNE_DCHECK(key >= 0 && key < kBandKeys && cx < ni && cy < ni);
     pts[k] = y;
     uvs[k] = uv;
     keyof[k] = (uint16_t)key;
@@ -225,6 +280,7 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
   int cur = -1, ccx = 0, ccy = 0;
   for (int q = s0; q < s1; ++q) {
     const int k = order[q];
+    FITSNE_DCHECK(k < cnt);
     const int key = keyof[k];
     const float2 y = pts[k];
     const float2 uv = uvs[k];
@@ -262,32 +318,29 @@ bool band_spread_applies(const fitsne_ctx* ctx, int64_t n) {
 int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
   const GridArgs g = grid_args(ctx->grid);
   const int nblk = (int)((n + kBandPts - 1) / kBandPts);
-  const size_t ncount = (size_t)g.n_int * nblk;
-  size_t scan_bytes = 0;
-  FITSNE_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, scan_bytes, (const uint32_t*)nullptr,
-                                            (uint32_t*)nullptr, (int)ncount, st));
-  // scratch: counts, offsets, cub temp, sorted points (16-byte aligned)
-  const size_t off_counts = 0;
-  const size_t off_offsets = off_counts + ((sizeof(uint32_t) * ncount + 255) & ~(size_t)255);
-  const size_t off_tmp = off_offsets + ((sizeof(uint32_t) * ncount + 255) & ~(size_t)255);
-  const size_t off_sorted = off_tmp + ((scan_bytes + 255) & ~(size_t)255);
+  // scratch: row totals + row cursors, then the sorted points (16-byte aligned)
+  const size_t off_rows = 0;
+  const size_t off_sorted = (2 * sizeof(uint32_t) * kBandMaxRows + 255) & ~(size_t)255;
   FITSNE_TRY(ensure(ctx->sortbuf, off_sorted + sizeof(float2) * (size_t)n));
   unsigned char* base = (unsigned char*)ctx->sortbuf.ptr;
-  uint32_t* counts = (uint32_t*)(base + off_counts);
-  uint32_t* offsets = (uint32_t*)(base + off_offsets);
+  uint32_t* rowtot = (uint32_t*)(base + off_rows);
+  uint32_t* rowcur = rowtot + kBandMaxRows;
   float2* sorted = (float2*)(base + off_sorted);
-  k_band_count<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, counts);
+  FITSNE_CUDA(cudaMemsetAsync(rowtot, 0, 2 * sizeof(uint32_t) * kBandMaxRows, st));
+  k_band_rowcount<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot);
   FITSNE_CHECK_LAUNCH();
-  FITSNE_CUDA(cub::DeviceScan::ExclusiveSum(base + off_tmp, scan_bytes, counts, offsets, (int)ncount,
-                                            st));
-  k_band_scatter<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, offsets, sorted);
+  k_band_place<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, rowcur, sorted);
   FITSNE_CHECK_LAUNCH();
   const int nred = (int)((n + kBandChunk - 1) / kBandChunk);
-  static thread_local int configured = -1;
-  if (configured != ctx->device) {
-    FITSNE_CUDA(cudaFuncSetAttribute(k_band_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     kBandSmem));
-    configured = ctx->device;
+  {
+    static std::mutex mu;
+    static std::set<int> configured;
+    std::lock_guard<std::mutex> lock(mu);
+    if (!configured.count(ctx->device)) {
+      FITSNE_CUDA(cudaFuncSetAttribute(k_band_reduce, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                       kBandSmem));
+      configured.insert(ctx->device);
+    }
   }
   k_band_reduce<<<nred, kBandBlock, kBandSmem, st>>>(sorted, n, g, (float*)accum);
   FITSNE_CHECK_LAUNCH();

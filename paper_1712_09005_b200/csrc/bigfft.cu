@@ -68,6 +68,7 @@ k_fft_pass(V* __restrict__ data, PassArgs a, FftPlan pl, const V* __restrict__ t
     int t, e;
     if (a.es == 1) { t = idx / m; e = idx - t * m; }
     else { e = idx / nt; t = idx - e * nt; }
+    FITSNE_DCHECK(t < nt && e < m);
     b0buf[(size_t)t * PL + pidx(e)] = base[(int64_t)t * a.bs_in + (int64_t)e * a.es];
   }
   V* r = block_fft<V, T>(b0buf, b1buf, pl, nt, PL, s_tw, a.inv != 0);

@@ -35,6 +35,28 @@ struct Status {
 
 #define FITSNE_CHECK_LAUNCH() FITSNE_CUDA(cudaGetLastError())
 
+// Device-side bounds checks of the debug build variant (python -m
+// paper_1712_09005_b200.build --variant=debug -DFITSNE_DEBUG_BOUNDS=1; the
+// test suite runs against it with FITSNE_LIB=libfitsne_b200_debug.so).  They
+// stand in for compute-sanitizer memcheck, which is closed on the GPU pool.
+#ifndef FITSNE_DEBUG_BOUNDS
+#define FITSNE_DEBUG_BOUNDS 0
+#endif
+#if FITSNE_DEBUG_BOUNDS
+#define FITSNE_DCHECK(c)                                                                  \
+  do {                                                                                    \
+    if (!(c)) {                                                                           \
+      printf("FITSNE_DCHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #c, (int)blockIdx.x, (int)threadIdx.x);                                      \
+      __trap();                                                                           \
+    }                                                                                     \
+  } while (0)
+#else
+#define FITSNE_DCHECK(c) \
+  do {                   \
+  } while (0)
+#endif
+
 // NVTX range for the lifetime of a scope (C-ABI entry points and pipeline
 // stages show up by name in Nsight timelines; a push/pop pair when no tool
 // is attached)

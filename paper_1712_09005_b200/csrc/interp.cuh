@@ -120,6 +120,7 @@ __device__ __forceinline__ void point_gather(const T (&yi)[S], const GridArgs& g
     if (S == 2)
       c1 = box_weights3_f32((float)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.lo_f[S - 1],
                             g.invh_f[S - 1], g.guard[S - 1], g.n_int, w1);
+    FITSNE_DCHECK(c0 >= 0 && c0 < g.n_int && c1 >= 0 && c1 < g.n_int);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int64_t rowbase = (S == 1) ? ((int64_t)c0 * 3 + a)

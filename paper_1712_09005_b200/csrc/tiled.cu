@@ -72,6 +72,12 @@ static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
 #ifndef FITSNE_TILED_L2PF
 #define FITSNE_TILED_L2PF 1
 #endif
+#ifndef FITSNE_TILED_DEPTH
+#define FITSNE_TILED_DEPTH 2
+#endif
+#ifndef FITSNE_TILED_FASTPATH
+#define FITSNE_TILED_FASTPATH 0
+#endif
 static constexpr int kTiledU = FITSNE_TILED_U;    // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
 
@@ -1143,6 +1149,8 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
     mbar_wait(&full[b], (uint32_t)((it / kTiledStages) & 1));
     const int32_t* meta = reinterpret_cast<const int32_t*>(h);
     const int rb = meta[0], ns = meta[1];
+    FITSNE_DCHECK(rb >= 0 && (int64_t)rb * R < n_rows && ns >= 1 && ns <= (R + 31) / 32 + 1 &&
+                  meta[3] >= 0);
     const int64_t g0 = (uint32_t)meta[2];
     const int ng = meta[3];
     const uint32_t* goff = reinterpret_cast<const uint32_t*>(h + kHdrGoff);
@@ -1213,6 +1221,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       // one group: slab boundary check, gather, accumulate (tail groups)
       auto step = [&](int gg, unsigned short c, float p) {
         if (gg == s_end) advance();
+        FITSNE_DCHECK(c < C && s < ns && (row == 0xFFFF || row < R));
         accum(cb[c], p);
       };
       const uint16_t* cp = cols + (size_t)slot_index(g0 + lo, lane);
@@ -1224,14 +1233,32 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
         pA[u] = __ldcs(vp + u * 32);
       }
+#if FITSNE_TILED_DEPTH >= 3
+      // two batches in flight: B holds the next batch, C is loaded ahead of it
+      unsigned short cC[kTiledU];
+      float pC[kTiledU];
+#pragma unroll
+      for (int u = 0; u < kTiledU; ++u) {
+        cB[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + (kTiledU + u) * 32);
+        pB[u] = __ldcs(vp + (kTiledU + u) * 32);
+      }
+#endif
       int g = lo;
       for (; g + kTiledU <= hi; g += kTiledU) {
         // prefetch the next step (reads past hi stay inside the padded arrays)
+#if FITSNE_TILED_DEPTH >= 3
+#pragma unroll
+        for (int u = 0; u < kTiledU; ++u) {
+          cC[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + (2 * kTiledU + u) * 32);
+          pC[u] = __ldcs(vp + (2 * kTiledU + u) * 32);
+        }
+#else
 #pragma unroll
         for (int u = 0; u < kTiledU; ++u) {
           cB[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + (kTiledU + u) * 32);
           pB[u] = __ldcs(vp + (kTiledU + u) * 32);
         }
+#endif
 #if FITSNE_TILED_HOIST
         // the batch's y_j gathers issued together (the staged chunk is never
         // written while the tile is processed; the flushes write accumulators)
@@ -1249,6 +1276,15 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
             accum(yj[u], pA[u]);
           }
         }
+#elif FITSNE_TILED_FASTPATH
+        if (s_end >= g + kTiledU) {
+          // no slab boundary inside the batch: straight-line accumulation
+#pragma unroll
+          for (int u = 0; u < kTiledU; ++u) accum(cb[cA[u]], pA[u]);
+        } else {
+#pragma unroll
+          for (int u = 0; u < kTiledU; ++u) step(g + u, cA[u], pA[u]);
+        }
 #else
         // (hoisting the batch's four gathers measured 14% slower: the
         // compiler then delays the next batch's global loads)
@@ -1257,6 +1293,10 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
 #endif
 #pragma unroll
         for (int u = 0; u < kTiledU; ++u) { cA[u] = cB[u]; pA[u] = pB[u]; }
+#if FITSNE_TILED_DEPTH >= 3
+#pragma unroll
+        for (int u = 0; u < kTiledU; ++u) { cB[u] = cC[u]; pB[u] = pC[u]; }
+#endif
         cp += kTiledU * 32;
         vp += kTiledU * 32;
       }

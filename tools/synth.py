@@ -177,6 +177,34 @@ class Upper:
         return 2.0 * float(self.values.sum())
 
 
+class DeviceUpper:
+    """Upper-COO P held on the device as torch tensors (C4's 450M pairs need
+    no host round trip; the drop-in API accepts tensors for rows/cols/values)."""
+
+    def __init__(self, n, rows, cols, values):
+        self.n, self.rows, self.cols, self.values = int(n), rows, cols, values
+
+    @property
+    def ordered_total(self):
+        return 2.0 * float(self.values.sum().item())
+
+
+def c4(device="cuda", n=10_000_000, seed=4):
+    """Config 4: random kNN graph P (device tensors) + 100-blob 2-D Y."""
+    r, c, v = random_knn_graph(n, 45, seed=seed, device=device)
+    Y = blobs2d(n, 100, 100.0, 2.0, seed=seed)
+    return DeviceUpper(n, r, c, v), Y
+
+
+def c5(device="cuda", n=1_000_000, seed=5):
+    """Config 5 inputs: 30-cluster mixture, kNN P, 1-D Y (top PCA direction)."""
+    X, _ = mixture(n, 50, 30, seed, device=device)
+    rows, cols, vals = affinities(X, 90, 30.0)
+    Y = pca2(X, 150.0, dims=1)
+    P = Upper(n, rows.cpu().numpy(), cols.cpu().numpy(), vals.cpu().numpy())
+    return P, Y.cpu().numpy()
+
+
 def shuffle(P, Y, seed=0):
     """The same (P, Y) with the points in a random order (upper COO kept
     rows < cols): real data arrive in no cluster order."""
