@@ -95,10 +95,14 @@ def parse():
                          "parallel.ShardedGradient) instead of the library's NCCL communicator")
     ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2, 3],
                     help="0 direct atomics, 1 auto (default), 2 box-sorted")
-    ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2],
+    ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2, 3],
                     help="0 serial, 1 (default) SpMV || repulsion, 2 + priority repulsion stream")
     ap.add_argument("--spmv-blocks", type=int, default=0, help="persistent SpMV blocks per SM (0: one tile per warp)")
     ap.add_argument("--spread-replicas", type=int, default=4, help="spread accumulator replicas")
+    ap.add_argument("--fft-cols", type=int, default=0, choices=[0, 1, 2, 4],
+                    help="FITSNE_OPT_FFT_COLS: columns per block of the column FFT stage (0 = default)")
+    ap.add_argument("--tiled-ctas", type=int, default=0,
+                    help="FITSNE_OPT_TILED_CTAS: persistent grid of the tiled SpMV (0 = default)")
     return ap.parse_args()
 
 
@@ -525,6 +529,9 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 3, args.spmv_blocks), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, args.spread_replicas), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, args.relabel), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_CTAS, args.tiled_ctas), "set_option")
+    if args.fft_cols:
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_FFT_COLS, args.fft_cols), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_BANK_ORDER, args.bank_order), "set_option")
     g = torch.empty_like(y)
     zc = __import__("ctypes").c_double()
@@ -689,18 +696,19 @@ def run_ours(args):
     if args.breakdown:
         line["breakdown_ms"] = breakdown
     if args.full_run:
-        line["full_run"] = full_run(P, dt, dev, reorder=False)
+        line["full_run"] = full_run(P, dt, dev, reorder=False, dims=dims)
     print(json.dumps(line), flush=True)
 
 
-def full_run(P, dt, dev, n_iter=1000, reorder=True):
-    """Config 3 as described: a full t-SNE run (Y0 ~ N(0, 1e-4^2), early
-    exaggeration 12 for 250 iterations, late exaggeration 4 from 750)."""
+def full_run(P, dt, dev, n_iter=1000, reorder=True, dims=2):
+    """The config's full t-SNE run (Y0 ~ N(0, 1e-4^2), early exaggeration 12
+    for 250 iterations; C3: late exaggeration 4 from 750; C5: 1-D)."""
     import torch
     from paper_1712_09005_b200 import optimizer
+    late = (4.0, 750) if dims == 2 else (1.0, None)
     cfg = optimizer.TsneConfig(
-        dims=2, n_iter=n_iter, learning_rate=200.0, min_intervals=50, points_per_interval=3,
-        exaggeration=optimizer.ExaggerationSchedule(12.0, 250, 4.0, 750), seed=0, pca_dims=None,
+        dims=dims, n_iter=n_iter, learning_rate=200.0, min_intervals=50, points_per_interval=3,
+        exaggeration=optimizer.ExaggerationSchedule(12.0, 250, *late), seed=0, pca_dims=None,
         repulsion_method="fft", dtype="float32" if dt == torch.float32 else "float64", device=dev,
         reorder_iters=(100, 250, 500, 750) if reorder else None)
     torch.cuda.synchronize()

@@ -160,7 +160,7 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_OVERLAP) {
-    if (value < 0 || value > 2) { set_error("overlap mode must be 0, 1 or 2"); return FITSNE_EINVAL; }
+    if (value < 0 || value > 3) { set_error("overlap mode must be 0, 1, 2 or 3"); return FITSNE_EINVAL; }
     if (ctx->side && value != ctx->overlap) {  // priority is fixed at creation
       cudaStreamSynchronize(ctx->side);
       cudaStreamDestroy(ctx->side);

@@ -632,6 +632,17 @@ static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
     FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
+  } else if (ctx->overlap == 3) {
+    // spread first on the whole GPU, then the SpMV with the FFT stages beside it
+    FITSNE_TRY(side_stream(ctx));
+    FITSNE_TRY(make_grid(ctx, Y, n, st));
+    FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
+    FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
+    FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
   } else {
     // bbox kernels first on the side stream (dispatched ahead of the SpMV, so
     // they get the whole GPU for a few microseconds), then the SpMV on st,
@@ -802,6 +813,16 @@ static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, st));
     FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
+  } else if (ctx->overlap == 3) {
+    FITSNE_TRY(side_stream(ctx));
+    FITSNE_TRY(make_grid(ctx, Yin, n, st));
+    FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
+    FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
+    FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
   } else {
     FITSNE_TRY(side_stream(ctx));
     FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));

@@ -226,7 +226,7 @@ __global__ void k_big_zfold(const double* __restrict__ zpart, int nb, double n_t
 // planes -> potentials (t-SNE: K2*1, K2*y_0, K2*y_1, K1*1 per node) or
 // general outputs (ncol, G); crops the circulant to the n^dims grid
 template <typename V, typename T, int MODE>
-__global__ void k_big_store(const V* __restrict__ W, int64_t ps, int ncol, int n, int L, int dims,
+__global__ void k_big_store(const V* __restrict__ W, int64_t ps, int ncol, int n, int L, int dims, int p,
                             T* __restrict__ pot, T* __restrict__ out) {
   const int64_t G = (dims == 1) ? (int64_t)n : (int64_t)n * n;
   for (int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; q < G;
@@ -234,7 +234,7 @@ __global__ void k_big_store(const V* __restrict__ W, int64_t ps, int ncol, int n
     const int64_t pos = (dims == 1) ? q : (q / n) * L + (q % n);
     if (MODE == 0) {
       const V a = W[pos], b = W[ps + pos];
-      T* rec = pot + q * kNodeSlots;
+      T* rec = pot + ((dims == 1) ? q : pot_node(q / n, q % n, p, n / p)) * kNodeSlots;
       rec[0] = b.x;
       rec[1] = a.x;
       rec[2] = (dims == 1) ? (T)0 : a.y;
@@ -401,7 +401,7 @@ static int conv_big_t(fitsne_ctx* ctx, T* accum, int nrep, int64_t rstride, cons
     FITSNE_TRY((cols_passes<V, T>(W, nw, plane, L, L1, L2, tw1, tw2, twL, true, st)));
     FITSNE_TRY((rows_passes<V, T>(W, nw, plane, n, L, L1, L2, tw1, tw2, twL, true, st)));
   }
-  k_big_store<V, T, MODE><<<nb, 256, 0, st>>>(W, plane, ncol, n, L, dims, (T*)ctx->pot.ptr, out);
+  k_big_store<V, T, MODE><<<nb, 256, 0, st>>>(W, plane, ncol, n, L, dims, g.p, (T*)ctx->pot.ptr, out);
   FITSNE_CHECK_LAUNCH();
   return FITSNE_OK;
 }

@@ -127,6 +127,20 @@ inline GridArgs grid_args(const fitsne_grid& g) {
 // nodes in a box per point: p^dims
 constexpr int kMaxP = 8;
 
+// The t-SNE potentials (ctx->pot) are stored box-major in 2-D: the p x p
+// nodes of box (bx, by) are one contiguous run of p^2 records, so a point's
+// p^2-node gather reads 9 x 16 B = 144 contiguous bytes (p = 3) instead of
+// three 48-byte pieces n records apart.  (Boxes own their nodes: node x
+// belongs to box x / p.)  1-D: the node order is already box-major.
+__host__ __device__ __forceinline__ int64_t pot_box_node(int64_t bx, int64_t by, int a, int b, int p,
+                                                         int n_int) {
+  return ((bx * n_int + by) * p + a) * p + b;
+}
+__host__ __device__ __forceinline__ int64_t pot_node(int64_t x, int64_t y, int p, int n_int) {
+  const int64_t bx = x / p, by = y / p;
+  return pot_box_node(bx, by, (int)(x - bx * p), (int)(y - by * p), p, n_int);
+}
+
 // Channel layout of the t-SNE spread / potentials: one 4-slot record per node.
 //   spread:     [0] unit charge, [1] y_0, [2] y_1, [3] unused
 //   potentials: [0] K2*1, [1] K2*y_0, [2] K2*y_1, [3] K1*1

@@ -70,7 +70,7 @@ __device__ __forceinline__ void warp_gather_partial(const T (&yi)[S], const Grid
     int64_t node = (int64_t)c0 * 3 + a;
     if (S == 2) {
       wt = wa * ((b == 0) ? w1[0] : ((b == 1) ? w1[1] : w1[2]));
-      node = node * g.n + (int64_t)c1 * 3 + b;
+      node = pot_box_node(c0, c1, a, b, 3, g.n_int);
     }
     T v[4];
     load_slots<T>(pot + node * kNodeSlots, v);
@@ -94,7 +94,7 @@ __device__ __forceinline__ void warp_gather_partial(const T (&yi)[S], const Grid
       wt = w[0][m];
     } else {
       const int a = m / p, b = m - (m / p) * p;
-      node = ((int64_t)cell[0] * p + a) * g.n + (int64_t)cell[1] * p + b;
+      node = pot_box_node(cell[0], cell[1], a, b, p, g.n_int);
       wt = w[0][a] * w[S - 1][b];
     }
     T v[4];
@@ -121,10 +121,11 @@ __device__ __forceinline__ void point_gather(const T (&yi)[S], const GridArgs& g
       c1 = box_weights3_f32((float)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.lo_f[S - 1],
                             g.invh_f[S - 1], g.guard[S - 1], g.n_int, w1);
     FITSNE_DCHECK(c0 >= 0 && c0 < g.n_int && c1 >= 0 && c1 < g.n_int);
+    // box-major potentials: the 9 records of box (c0, c1) are contiguous
+    const int64_t box0 = (S == 1) ? (int64_t)c0 * 3 : pot_box_node(c0, c1, 0, 0, 3, g.n_int);
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
-      const int64_t rowbase = (S == 1) ? ((int64_t)c0 * 3 + a)
-                                       : (((int64_t)c0 * 3 + a) * g.n + (int64_t)c1 * 3);
+      const int64_t rowbase = box0 + a * ((S == 1) ? 1 : 3);
 #pragma unroll
       for (int b = 0; b < ((S == 1) ? 1 : 3); ++b) {
         T v[4];
@@ -144,7 +145,7 @@ __device__ __forceinline__ void point_gather(const T (&yi)[S], const GridArgs& g
     for (int m = 0; m < cnt; ++m) {
       const int a = (S == 1) ? m : m / p, b = (S == 1) ? 0 : m - (m / p) * p;
       const int64_t node = (S == 1) ? ((int64_t)cell[0] * p + a)
-                                    : (((int64_t)cell[0] * p + a) * g.n + (int64_t)cell[1] * p + b);
+                                    : pot_box_node(cell[0], cell[1], a, b, p, g.n_int);
       const double wt = (S == 1) ? w[0][a] : w[0][a] * w[S - 1][b];
       T v[4];
       load_slots<T>(pot + node * kNodeSlots, v);

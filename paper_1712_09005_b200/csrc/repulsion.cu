@@ -980,7 +980,7 @@ k_rows_inverse(const typename C2<T>::type* __restrict__ F, GridArgs g,
   if (MODE == MODE_TSNE) {
     for (int y = threadIdx.x; y < n; y += blockDim.x) {
       V A = r[pidx(y)], B = r[PL + pidx(y)];
-      T* rec = pot + ((size_t)x * n + y) * kNodeSlots;
+      T* rec = pot + pot_node(x, y, g.p, g.n_int) * kNodeSlots;
       // slots: K2*1, K2*y_0, K2*y_1, K1*1 (the last only with_k1)
       if constexpr (sizeof(T) == 4) {
         *reinterpret_cast<float4*>(rec) = make_float4(B.x, A.x, A.y, B.y);
@@ -1289,12 +1289,10 @@ __global__ void k_gather_tsne(const T* __restrict__ Y, int64_t n, GridArgs g,
       for (int c = 0; c < 4; ++c) phi[c] += v[c] * w;
     }
   } else {
-    const int64_t nn = g.n;
     for (int a = 0; a < p; ++a) {
-      int64_t rowbase = ((int64_t)pi.cell[0] * p + a) * nn + (int64_t)pi.cell[1] * p;
       for (int b = 0; b < p; ++b) {
         T v[4];
-        load_slots<T>(pot + (rowbase + b) * kNodeSlots, v);
+        load_slots<T>(pot + pot_box_node(pi.cell[0], pi.cell[1], a, b, p, g.n_int) * kNodeSlots, v);
         T w = (T)(pi.w[0][a] * pi.w[1][b]);
 #pragma unroll
         for (int c = 0; c < 4; ++c) phi[c] += v[c] * w;

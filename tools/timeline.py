@@ -31,6 +31,9 @@ def main():
     g = torch.empty_like(y)
     csr = device_csr(P, torch.float32, 0)
     ctx = _lib.Context(0, 2, torch.float32, 3, 50, 1.0)
+    for name, opt in (("--overlap", _lib.OPT_OVERLAP), ("--tiled-ctas", _lib.OPT_TILED_CTAS)):
+        if name in sys.argv:
+            _lib.check(ctx.lib.fitsne_set_option(ctx.h, opt, int(sys.argv[sys.argv.index(name) + 1])), name)
     ctx.set_affinities(csr)
 
     def step():
@@ -47,7 +50,7 @@ def main():
     evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
     evs.sort(key=lambda e: e.time_range.start)
     # split into the three steps at the bbox kernel (first kernel of a step)
-    starts = [i for i, e in enumerate(evs) if e.name.startswith("void fitsne::k_bbox") or "k_bbox" in e.name]
+    starts = [i for i, e in enumerate(evs) if "k_bbox" in e.name]
     last = evs[starts[-1]:] if starts else evs
     t0 = last[0].time_range.start
     rows = [{"kernel": e.name.split("(")[0][:80], "start_us": round(e.time_range.start - t0, 1),
