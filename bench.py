@@ -101,6 +101,7 @@ def parse():
     ap.add_argument("--spread-replicas", type=int, default=4, help="spread accumulator replicas")
     ap.add_argument("--fft-cols", type=int, default=0, choices=[0, 1, 2, 4],
                     help="FITSNE_OPT_FFT_COLS: columns per block of the column FFT stage (0 = default)")
+    ap.add_argument("--tile", default=None, help="ROWSxCOLS tile shape of the tiled SpMV (A/B)")
     ap.add_argument("--tiled-ctas", type=int, default=0,
                     help="FITSNE_OPT_TILED_CTAS: persistent grid of the tiled SpMV (0 = default)")
     return ap.parse_args()
@@ -530,6 +531,10 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, args.spread_replicas), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, args.relabel), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_CTAS, args.tiled_ctas), "set_option")
+    if args.tile:
+        tr, tc = (int(v) for v in args.tile.lower().split("x"))
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILE_ROWS, tr), "set_option")
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILE_COLS, tc), "set_option")
     if args.fft_cols:
         _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_FFT_COLS, args.fft_cols), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_BANK_ORDER, args.bank_order), "set_option")

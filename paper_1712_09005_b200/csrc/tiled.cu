@@ -84,7 +84,10 @@ static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot 
 // Slot layout: group-major, lane-minor (a warp reads one group's columns and
 // values with one coalesced 64-byte and one 128-byte load).
 __host__ __device__ inline int64_t slot_index(int64_t g, int lane) { return g * 32 + lane; }
-static constexpr int kTiledStages = 2;            // chunk + header ring depth
+#ifndef FITSNE_TILED_STAGES
+#define FITSNE_TILED_STAGES 2
+#endif
+static constexpr int kTiledStages = FITSNE_TILED_STAGES;  // chunk + header ring depth
 
 // First group of consumer warp w's run in a tile of ng groups: equal shares
 // (group granularity: all consumers meet at every tile, so the longest run
@@ -120,6 +123,12 @@ struct TiledP {
   bool dirty = false;
   cudaStream_t dirty_stream = nullptr;
 };
+
+// points per column chunk: the option's value for 2-D, twice that for 1-D
+// (same bytes per staged chunk); column indices are 16-bit
+static int tile_cols_eff(const fitsne_ctx* ctx) {
+  return std::min(ctx->dims == 1 ? 2 * ctx->tile_cols : ctx->tile_cols, 65536);
+}
 
 static void release_buf(DevBuf& b) {
   if (b.ptr) cudaFree(b.ptr);
@@ -615,7 +624,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     // 28M segments) runs 7% slower relabelled, a randomly ordered one (117M
     // segments, no tiled layout at all) gets the tiled SpMV back.
     int64_t seg_new = 0, seg_old = 0;
-    FITSNE_TRY(count_segments(nrowptr, scol, n, ctx->tile_cols, tmp, &seg_new, st));
+    FITSNE_TRY(count_segments(nrowptr, scol, n, tile_cols_eff(ctx), tmp, &seg_new, st));
     const int32_t* c0 = ctx->col;
     {
       // the caller's rows may be unsorted: count on a sorted copy
@@ -641,7 +650,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
         c0 = oc;
       }
     }
-    FITSNE_TRY(count_segments(ctx->rowptr, c0, n, ctx->tile_cols, tmp, &seg_old, st));
+    FITSNE_TRY(count_segments(ctx->rowptr, c0, n, tile_cols_eff(ctx), tmp, &seg_old, st));
     T->nseg_natural = seg_old;
     use = (double)seg_new <= 0.5 * (double)seg_old;
   }
@@ -657,7 +666,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
 static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, const int32_t* col_in,
                            const float* val_in, cudaStream_t st) {
   const int64_t n_rows = ctx->n_rows, n_total = ctx->n_total, nnz = ctx->nnz;
-  const int R = ctx->tile_rows, C = ctx->tile_cols;
+  const int R = ctx->tile_rows, C = tile_cols_eff(ctx);
   const int64_t nrb = (n_rows + R - 1) / R, nch = (n_total + C - 1) / C;
   const int64_t ntd = nrb * nch;  // dense tile count
   if (ntd >= (1LL << 31) || nnz >= (1LL << 31) || nrb >= (1LL << 31)) {
@@ -923,24 +932,28 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   return FITSNE_OK;
 }
 
-static size_t stage_bytes(int C, int hdr_max) { return (size_t)C * 8 + (size_t)((hdr_max + 15) & ~15); }
-static size_t tiled_smem(int R, int C, int hdr_max) {
-  return sizeof(float2) * 3 * (size_t)R + kTiledStages * stage_bytes(C, hdr_max);
+// es: bytes per point (8 for 2-D float2, 4 for 1-D float)
+static size_t stage_bytes(int C, int hdr_max, size_t es) {
+  return (size_t)C * es + (size_t)((hdr_max + 15) & ~15);
+}
+static size_t tiled_smem(int R, int C, int hdr_max, size_t es) {
+  return ((es * 3 * (size_t)R + 15) & ~(size_t)15) + kTiledStages * stage_bytes(C, hdr_max, es);
 }
 
 // Use the tiled kernel for this call?  Builds the tiled copy on first use.
 bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
-  if (ctx->tiled_spmv == 0 || ctx->dtype != FITSNE_F32 || ctx->dims != 2 || !ctx->rowptr) return false;
+  if (ctx->tiled_spmv == 0 || ctx->dtype != FITSNE_F32 || !ctx->rowptr) return false;
   if (((uintptr_t)Y & 15) != 0) return false;
   if (ctx->tiled_spmv == 1 && ctx->nnz < (1LL << 22)) return false;
-  if (tiled_smem(ctx->tile_rows, ctx->tile_cols, hdr_bytes_for((ctx->tile_rows + 31) / 32)) >
+  if (tiled_smem(ctx->tile_rows, tile_cols_eff(ctx), hdr_bytes_for((ctx->tile_rows + 31) / 32),
+                 ctx->dims == 1 ? sizeof(float) : sizeof(float2)) >
       227 * 1024 - 1024)
     return false;  // tile shape does not fit in shared memory
   TiledP* T = ctx->tiled;
   const bool same = T && T->rowptr == ctx->rowptr && T->col == ctx->col && T->val == ctx->val &&
                     T->n_rows == ctx->n_rows && T->row_begin == ctx->row_begin &&
                     T->n_total == ctx->n_total && T->nnz == ctx->nnz && T->R == ctx->tile_rows &&
-                    T->C == ctx->tile_cols && T->relabel_mode == ctx->relabel &&
+                    T->C == tile_cols_eff(ctx) && T->relabel_mode == ctx->relabel &&
                     T->bank_mode == ctx->tiled_bank_order &&
                     T->grid == (tiled_grid(ctx));
   if (same) return !T->failed;
@@ -958,7 +971,7 @@ bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
   T->n_total = ctx->n_total;
   T->nnz = ctx->nnz;
   T->R = ctx->tile_rows;
-  T->C = ctx->tile_cols;
+  T->C = tile_cols_eff(ctx);
   T->relabel_mode = ctx->relabel;
   T->bank_mode = ctx->tiled_bank_order;
   T->grid = tiled_grid(ctx);
@@ -1037,6 +1050,43 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 
+// Point type of the tiles: float2 (2-D) or float (1-D embeddings; a chunk of
+// C points is then 4C bytes, so 1-D uses twice the points per chunk).
+template <int S> struct TPt;
+template <> struct TPt<2> {
+  using T = float2;
+  static __device__ __forceinline__ T zero() { return make_float2(0.f, 0.f); }
+  static __device__ __forceinline__ T make(float a, float b) { return make_float2(a, b); }
+  static __device__ __forceinline__ T add(T a, T b) { return make_float2(a.x + b.x, a.y + b.y); }
+  static __device__ __forceinline__ bool nonzero(T a) { return a.x != 0.f || a.y != 0.f; }
+  // accumulate w (y_i - y_j), w = p / (1 + |y_i - y_j|^2); returns 1 + d^2
+  static __device__ __forceinline__ float accum(T yi, T yj, float p, float& ax, float& ay) {
+    const float dx = yi.x - yj.x, dy = yi.y - yj.y;
+    const float q = 1.0f + (dx * dx + dy * dy);
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+    const float w = p * r;
+    ax += w * dx;
+    ay += w * dy;
+    return q;
+  }
+};
+template <> struct TPt<1> {
+  using T = float;
+  static __device__ __forceinline__ T zero() { return 0.f; }
+  static __device__ __forceinline__ T make(float a, float) { return a; }
+  static __device__ __forceinline__ T add(T a, T b) { return a + b; }
+  static __device__ __forceinline__ bool nonzero(T a) { return a != 0.f; }
+  static __device__ __forceinline__ float accum(T yi, T yj, float p, float& ax, float&) {
+    const float dx = yi - yj;
+    const float q = 1.0f + dx * dx;
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(q));
+    ax += p * r * dx;
+    return q;
+  }
+};
+
 // consumer-only barrier (the producer warp never joins it)
 __device__ __forceinline__ void consumer_sync() {
   asm volatile("bar.sync 1, %0;" ::"n"(kTiledConsumers * 32) : "memory");
@@ -1058,18 +1108,22 @@ __device__ __forceinline__ float rcp_approx(float x) {
 // the row block's shared accumulator at every slab boundary.  Row-block
 // changes (rare: a CTA's tiles are a contiguous run of the row-block-major
 // order) flush the accumulator to global memory with vector reductions.
-template <bool KL>
+template <int S, bool KL>
 __global__ void __launch_bounds__(kTiledThreads, 1)
 k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ sched,
                 const unsigned char* __restrict__ hdr, const uint16_t* __restrict__ cols,
-                const float* __restrict__ vals, const float2* __restrict__ Y, int64_t row_begin,
+                const float* __restrict__ vals, const typename TPt<S>::T* __restrict__ Y, int64_t row_begin,
                 int64_t n_rows, int64_t n_total, int R, int C, int stage_sz,
-                float2* __restrict__ fattr, double* __restrict__ klpart, const int* __restrict__ rowmap) {
+                typename TPt<S>::T* __restrict__ fattr, double* __restrict__ klpart,
+                const int* __restrict__ rowmap) {
+  using PT = typename TPt<S>::T;
+  using Tr = TPt<S>;
   // rowmap (relabelled P): the output index of tile row r is rowmap[r]
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  float2* ys = reinterpret_cast<float2*>(smem_raw);
-  float2* acc = ys + R;  // two accumulators: [0, R) even tiles, [R, 2R) odd tiles
-  unsigned char* ring = reinterpret_cast<unsigned char*>(acc + 2 * R);
+  PT* ys = reinterpret_cast<PT*>(smem_raw);
+  PT* acc = ys + R;  // two accumulators: [0, R) even tiles, [R, 2R) odd tiles
+  // the bulk-copy ring starts 16-byte aligned (1-D rows are 12 bytes each)
+  unsigned char* ring = smem_raw + ((3 * (size_t)R * sizeof(PT) + 15) & ~(size_t)15);
   __shared__ __align__(8) uint64_t full[kTiledStages], empty[kTiledStages];
   __shared__ double red[kTiledConsumers];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -1092,14 +1146,16 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         if (it >= kTiledStages) mbar_wait(&empty[b], (uint32_t)(((it / kTiledStages) - 1) & 1));
         const TileLoad d = tiles[t];
         unsigned char* st = ring + (size_t)b * stage_sz;
-        float2* cdst = reinterpret_cast<float2*>(st);
-        unsigned char* hdst = st + (size_t)C * 8;
+        PT* cdst = reinterpret_cast<PT*>(st);
+        unsigned char* hdst = st + (size_t)C * sizeof(PT);
         const int64_t c0 = (int64_t)d.chunk * C;
         const int64_t cnt = (n_total - c0 < C) ? (n_total - c0) : C;
-        const uint32_t cbytes = (uint32_t)(cnt & ~1LL) * 8u;
-        // odd tail point (bulk copies move multiples of 16 bytes): a plain
-        // store, published to the consumers by the release of the arrive below
-        if (cnt & 1) cdst[cnt - 1] = Y[c0 + cnt - 1];
+        constexpr int64_t kAl = 16 / (int64_t)sizeof(PT);  // points per 16 bytes
+        const int64_t cbulk = cnt / kAl * kAl;
+        const uint32_t cbytes = (uint32_t)cbulk * (uint32_t)sizeof(PT);
+        // tail points (bulk copies move multiples of 16 bytes): plain stores,
+        // published to the consumers by the release of the arrive below
+        for (int64_t k = cbulk; k < cnt; ++k) cdst[k] = Y[c0 + k];
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(&full[b], cbytes + (uint32_t)d.hdr_bytes);
         if (cbytes) bulk_g2s_hint(cdst, Y + c0, cbytes, &full[b], pol_y);
@@ -1136,16 +1192,15 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   int nr = 0;
   auto flush_block = [&]() {
     for (int i = tid; i < nr; i += kTiledConsumers * 32) {
-      const float2 a = acc[i], c = acc[R + i];
-      const float2 v = make_float2(a.x + c.x, a.y + c.y);
-      if (v.x != 0.f || v.y != 0.f) atomicAdd(fattr + (rowmap ? (int64_t)rowmap[r0 + i] : r0 + i), v);
+      const PT v = Tr::add(acc[i], acc[R + i]);
+      if (Tr::nonzero(v)) atomicAdd(fattr + (rowmap ? (int64_t)rowmap[r0 + i] : r0 + i), v);
     }
   };
   for (int t = t0; t < t1; ++t) {
     const int it = t - t0, b = it % kTiledStages;
     const unsigned char* st = ring + (size_t)b * stage_sz;
-    const float2* cb = reinterpret_cast<const float2*>(st);
-    const unsigned char* h = st + (size_t)C * 8;
+    const PT* cb = reinterpret_cast<const PT*>(st);
+    const unsigned char* h = st + (size_t)C * sizeof(PT);
     mbar_wait(&full[b], (uint32_t)((it / kTiledStages) & 1));
     const int32_t* meta = reinterpret_cast<const int32_t*>(h);
     const int rb = meta[0], ns = meta[1];
@@ -1162,13 +1217,13 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       r0 = (int64_t)rb * R;
       nr = (n_rows - r0 < R) ? (int)(n_rows - r0) : R;
       for (int i = tid; i < R; i += kTiledConsumers * 32) {
-        ys[i] = i < nr ? Y[row_begin + r0 + i] : make_float2(0.f, 0.f);
-        acc[i] = make_float2(0.f, 0.f);
-        acc[R + i] = make_float2(0.f, 0.f);
+        ys[i] = i < nr ? Y[row_begin + r0 + i] : Tr::zero();
+        acc[i] = Tr::zero();
+        acc[R + i] = Tr::zero();
       }
       consumer_sync();
     }
-    float2* accp = acc + (size_t)(it & 1) * R;
+    PT* accp = acc + (size_t)(it & 1) * R;
     const int lo = tiled_run_lo(ng, warp);
     const int hi = tiled_run_lo(ng, warp + 1);
     if (lo < hi) {
@@ -1176,7 +1231,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       int s_end = (int)goff[s + 1];
       bool shared_slab = (int)goff[s] < lo || s_end > hi;
       int row = hrows[s * 32 + lane];
-      float2 yi = row != 0xFFFF ? ys[row] : make_float2(0.f, 0.f);
+      PT yi = row != 0xFFFF ? ys[row] : Tr::zero();
       float ax = 0.f, ay = 0.f;
       // output index of a shared slab's row, loaded when the slab starts so
       // the (relabelled) row map's L2 latency is hidden behind the slab
@@ -1191,12 +1246,9 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
           // rows of a slab cut by a warp-range boundary are updated by two or
           // more warps of this tile: add straight to the output with a vector
           // reduction in L2 instead of a shared-memory compare-and-swap loop
-          atomicAdd(fattr + orow, make_float2(ax, ay));
+          atomicAdd(fattr + orow, Tr::make(ax, ay));
         } else {
-          float2 v = accp[row];
-          v.x += ax;
-          v.y += ay;
-          accp[row] = v;
+          accp[row] = Tr::add(accp[row], Tr::make(ax, ay));
         }
       };
       // slab boundary (warp-uniform): flush the finished row, load the next
@@ -1207,15 +1259,11 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         s_end = (int)goff[s + 1];
         shared_slab = s_end > hi;
         row = hrows[s * 32 + lane];
-        yi = row != 0xFFFF ? ys[row] : make_float2(0.f, 0.f);
+        yi = row != 0xFFFF ? ys[row] : Tr::zero();
         out_row();
       };
-      auto accum = [&](float2 yj, float p) {
-        const float dx = yi.x - yj.x, dy = yi.y - yj.y;
-        const float q = 1.0f + (dx * dx + dy * dy);
-        const float w = p * rcp_approx(q);
-        ax += w * dx;
-        ay += w * dy;
+      auto accum = [&](PT yj, float p) {
+        const float q = Tr::accum(yi, yj, p, ax, ay);
         if (KL) kl += p * __logf(q);
       };
       // one group: slab boundary check, gather, accumulate (tail groups)
@@ -1262,7 +1310,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
 #if FITSNE_TILED_HOIST
         // the batch's y_j gathers issued together (the staged chunk is never
         // written while the tile is processed; the flushes write accumulators)
-        float2 yj[kTiledU];
+        PT yj[kTiledU];
 #pragma unroll
         for (int u = 0; u < kTiledU; ++u) yj[u] = cb[cA[u]];
         if (s_end >= g + kTiledU) {
@@ -1324,47 +1372,43 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
 }
 
 // out = F_attr (mode 0) or 4 (alpha F_attr - F_rep) (mode 1); clears F_attr
-__global__ void k_tiled_finish(float2* __restrict__ fattr, int64_t n, const float2* __restrict__ frep,
-                               float alpha, int mode, float2* __restrict__ out) {
+__global__ void k_tiled_finish(float* __restrict__ fattr, int64_t m, const float* __restrict__ frep,
+                               float alpha, int mode, float* __restrict__ out) {
+  // m = n rows x dims values
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const float2 a = fattr[i];
-  float2 r = a;
-  if (mode == 1) {
-    const float2 f = frep[i];
-    r.x = 4.f * (alpha * a.x - f.x);
-    r.y = 4.f * (alpha * a.y - f.y);
-  }
-  fattr[i] = make_float2(0.f, 0.f);
-  out[i] = r;
+  if (i >= m) return;
+  const float a = fattr[i];
+  out[i] = (mode == 1) ? 4.f * (alpha * a - frep[i]) : a;
+  fattr[i] = 0.f;
 }
 
 // yp[r] = Y[order[r]]
-__global__ void k_permute_points(const float2* __restrict__ Y, const int* __restrict__ order, int64_t n,
-                                 float2* __restrict__ yp) {
+template <typename PT>
+__global__ void k_permute_points(const PT* __restrict__ Y, const int* __restrict__ order, int64_t n,
+                                 PT* __restrict__ yp) {
   const int64_t r = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (r < n) yp[r] = Y[order[r]];
 }
 
 // Runs the tiled SpMV: F_attr accumulates into the tiled copy's zeroed buffer
 // (*fattr_out; the consumer must clear it), KL partials -> T->part[0, grid).
-static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched,
-                        cudaStream_t st) {
-  FITSNE_RANGE("tiled_spmv");
+template <int S>
+static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched, cudaStream_t st) {
+  using PT = typename TPt<S>::T;
   TiledP* T = ctx->tiled;
-  const size_t smem = tiled_smem(T->R, T->C, T->hdr_max);
-  const int stage_sz = (int)stage_bytes(T->C, T->hdr_max);
+  const size_t smem = tiled_smem(T->R, T->C, T->hdr_max, sizeof(PT));
+  const int stage_sz = (int)stage_bytes(T->C, T->hdr_max, sizeof(PT));
   {
     // the attribute is per device and process-wide: cache what was set per
-    // device under a lock (raise only; a smaller request fits a larger limit)
+    // (device, dims) under a lock (raise only; a smaller request fits)
     static std::mutex mu;
     static std::map<int, size_t> configured;
     std::lock_guard<std::mutex> lock(mu);
-    size_t& have = configured[ctx->device];
+    size_t& have = configured[ctx->device * 4 + S];
     if (have < smem) {
-      FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<S, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
-      FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      FITSNE_CUDA(cudaFuncSetAttribute(k_attract_tiled<S, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                        (int)smem));
       have = smem;
     }
@@ -1373,23 +1417,29 @@ static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* 
   const int* rowmap = nullptr;
   if (T->relabeled) {
     // the tiles index the relabelled points: stage Y in that order
-    k_permute_points<<<nb(ctx->n_total, 256), 256, 0, st>>>((const float2*)Y, (const int*)T->order.ptr,
-                                                            ctx->n_total, (float2*)T->yp.ptr);
+    k_permute_points<PT><<<nb(ctx->n_total, 256), 256, 0, st>>>((const PT*)Y, (const int*)T->order.ptr,
+                                                                ctx->n_total, (PT*)T->yp.ptr);
     FITSNE_CHECK_LAUNCH();
     Y = T->yp.ptr;
     rowmap = (const int*)T->order.ptr;
   }
 #define TILED_ARGS                                                                                  \
-  (const TileLoad*)T->tiles.ptr, sched, (const unsigned char*)T->hdr.ptr,    \
-      (const uint16_t*)T->cols.ptr, (const float*)T->vals.ptr, (const float2*)Y, ctx->row_begin,    \
-      ctx->n_rows, ctx->n_total, T->R, T->C, stage_sz, (float2*)T->fattr.ptr, part, rowmap
+  (const TileLoad*)T->tiles.ptr, sched, (const unsigned char*)T->hdr.ptr,                          \
+      (const uint16_t*)T->cols.ptr, (const float*)T->vals.ptr, (const PT*)Y, ctx->row_begin,        \
+      ctx->n_rows, ctx->n_total, T->R, T->C, stage_sz, (PT*)T->fattr.ptr, part, rowmap
   if (kl)
-    k_attract_tiled<true><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
+    k_attract_tiled<S, true><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
   else
-    k_attract_tiled<false><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
+    k_attract_tiled<S, false><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
 #undef TILED_ARGS
   FITSNE_CHECK_LAUNCH();
   return FITSNE_OK;
+}
+
+static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched,
+                        cudaStream_t st) {
+  FITSNE_RANGE("tiled_spmv");
+  return ctx->dims == 1 ? launch_tiled_s<1>(ctx, Y, kl, sched, st) : launch_tiled_s<2>(ctx, Y, kl, sched, st);
 }
 
 // Start of an SpMV pass over fattr: clear a stale accumulation first (see
@@ -1454,8 +1504,9 @@ int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st) {
 int tiled_finish(fitsne_ctx* ctx, const void* frep, double alpha, int mode, void* out, cudaStream_t st) {
   TiledP* T = ctx->tiled;
   const int64_t n = ctx->n_rows;
-  k_tiled_finish<<<nb(n, 256), 256, 0, st>>>((float2*)T->fattr.ptr, n, (const float2*)frep, (float)alpha,
-                                             mode, (float2*)out);
+  const int64_t m = n * ctx->dims;
+  k_tiled_finish<<<nb(m, 256), 256, 0, st>>>((float*)T->fattr.ptr, m, (const float*)frep, (float)alpha,
+                                             mode, (float*)out);
   FITSNE_CHECK_LAUNCH();
   tiled_consumed(ctx);
   return FITSNE_OK;

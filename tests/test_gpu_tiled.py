@@ -354,3 +354,54 @@ def test_relabelled_gradient_and_iterate(cuda):
     ref = O.grad(rr, cc, v, y32.astype(np.float64), 12.0, 50, 3, "fft")
     assert rel_l2(g.double().cpu().numpy(), ref) <= 1e-3
     assert rel_l2(g_host, ref) <= 1e-3
+
+
+@pytest.mark.parametrize("relabel", [0, 2])
+@pytest.mark.parametrize("shape", [(64, 128, 0), (256, 1024, 7), (2, 2, 3), (4096, 6144, 0)])
+def test_tiled_1d(cuda, shape, relabel):
+    """1-D embeddings on the tiled SpMV (float chunks of twice the points):
+    F_attr and the KL sum against the oracle, with and without relabelling."""
+    from paper_1712_09005_b200 import _lib
+    n = 5003
+    rr, cc, v, Y = _graph(n, 24, 21)
+    if relabel:
+        rr, cc, v, Y = _shuffled(n, rr, cc, v, Y, seed=9)
+    y1 = Y[:, :1].astype(np.float32)
+    y = torch.from_numpy(np.ascontiguousarray(y1)).cuda()
+    ctx = _lib.Context(0, 1, torch.float32, 3, 20, 1.0)
+    for opt, val in ((OPT_TILED, 2), (OPT_ROWS, shape[0]), (OPT_COLS, shape[1]), (OPT_CTAS, shape[2]),
+                     (_lib.OPT_RELABEL, relabel)):
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, opt, val), "set_option")
+    csr = _csr(n, rr, cc, v)
+    ctx.set_affinities(csr)
+    out = torch.empty((n, 1), dtype=torch.float32, device=y.device)
+    _lib.check(ctx.lib.fitsne_attractive(ctx.h, _lib.ptr(y), _lib.ptr(out), ctx.stream), "attractive")
+    st = (C.c_int64 * 8)()
+    _lib.check(ctx.lib.fitsne_tiled_stats(ctx.h, _lib.ptr(y), st, ctx.stream), "stats")
+    assert st[0] == 1 and st[6] == (1 if relabel else 0)
+    ref = O.attraction(rr, cc, v, y1.astype(np.float64))
+    assert rel_l2(out.cpu().numpy().astype(np.float64), ref) <= 1e-5
+    kl = C.c_double()
+    _lib.check(ctx.lib.fitsne_kl(ctx.h, _lib.ptr(y), 2.5, C.byref(kl), ctx.stream), "kl")
+    assert abs(kl.value - O.kl_given_z(rr, cc, v, y1.astype(np.float64), 2.5)) <= 1e-5 * abs(kl.value)
+
+
+def test_tiled_1d_gradient_and_run(cuda):
+    """The 1-D production path (tiled SpMV in the overlapped schedule, the
+    fused iteration) against the oracle."""
+    from paper_1712_09005_b200 import _lib, optimizer
+    from paper_1712_09005_b200.affinities import SparseAffinities
+    n = 20_000
+    rr, cc, v, Y = _graph(n, 30, 22)
+    P = SparseAffinities(n=n, rows=rr, cols=cc, values=v)
+    y1 = np.ascontiguousarray(Y[:, :1].astype(np.float32))
+    with _lib.option(OPT_TILED, 2):
+        g = optimizer.gradient(P, torch.from_numpy(y1).cuda(), 4.0, 50, 3, "fft").double().cpu().numpy()
+        cfg = optimizer.TsneConfig(dims=1, n_iter=5, learning_rate=200.0, min_intervals=50,
+                                   exaggeration=optimizer.ExaggerationSchedule(12.0, 5), seed=0,
+                                   pca_dims=None, repulsion_method="fft", dtype="float32")
+        res = optimizer.run_tsne(affinities=P, config=cfg)
+    assert rel_l2(g, O.grad(rr, cc, v, y1.astype(np.float64), 4.0, 50, 3, "fft")) <= 1e-3
+    _, kl_o = O.tsne(rr, cc, v, n, dims=1, n_iter=5, lr=200.0, early_coeff=12.0, early_until=5,
+                     min_intervals=50, p=3, method="fft", seed=0)
+    assert np.max(np.abs(res.kl_log - kl_o) / np.abs(kl_o)) <= 1e-4
