@@ -84,6 +84,8 @@ def parse():
                          "order; the library relabels P internally, FITSNE_OPT_RELABEL)")
     ap.add_argument("--bank-order", type=int, default=1, choices=[0, 1, 2],
                     help="FITSNE_OPT_TILED_BANK_ORDER (A/B)")
+    ap.add_argument("--device-grid", type=int, default=0, choices=[0, 1],
+                    help="FITSNE_OPT_DEVICE_GRID (A/B)")
     ap.add_argument("--relabel", type=int, default=1, choices=[0, 1, 2],
                     help="FITSNE_OPT_RELABEL: 0 caller's order, 1 auto (default), 2 always")
     ap.add_argument("--host-schedule", type=int, default=0, choices=[0, 1, 2],
@@ -531,6 +533,7 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, 4, args.spread_replicas), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, args.relabel), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_CTAS, args.tiled_ctas), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_DEVICE_GRID, args.device_grid), "set_option")
     if args.tile:
         tr, tc = (int(v) for v in args.tile.lower().split("x"))
         _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILE_ROWS, tr), "set_option")

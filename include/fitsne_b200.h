@@ -103,7 +103,8 @@ enum fitsne_option {
   FITSNE_OPT_FFT_COLS = 11,
   FITSNE_OPT_FFT_PATH = 12,
   FITSNE_OPT_GRID_F64 = 13,
-  FITSNE_OPT_RELABEL = 14
+  FITSNE_OPT_RELABEL = 14,
+  FITSNE_OPT_DEVICE_GRID = 15
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -139,7 +140,14 @@ enum fitsne_option {
  *   of the points computed from P's pattern on the device (components and
  *   neighbourhoods get contiguous labels; results stay in the caller's
  *   order).  0 = caller's order; 1 (default) = relabel when that at least
- *   halves the (row, column chunk) segments of the tiles; 2 = always. */
+ *   halves the (row, column chunk) segments of the tiles; 2 = always.
+ *   FITSNE_OPT_DEVICE_GRID: 1 = fitsne_gradient / _host / _iterate compute
+ *   the grid on the device and queue the spread and FFT stages without
+ *   waiting for the bbox readback (the host checks the grid after queueing
+ *   and re-runs the chain in the rare case the stages' launch capacity was
+ *   exceeded); 0 (default) = wait for the readback first.  At C3 the chain
+ *   then starts ~20 us earlier but its stages run no faster on the SMs the
+ *   SpMV leaves, so the step measured 1.5% slower; kept as an option. */
 int fitsne_set_option(fitsne_ctx* ctx, int option, int value);
 /* Layout of the tiled copy of P (diagnostics; builds it if needed, using Y
  * only for its alignment): out[0..7] = {in use (0/1), tiles, slabs, slot

@@ -121,9 +121,11 @@ int fitsne_destroy(fitsne_ctx* c) {
   cudaDeviceSynchronize();
   DevBuf* bufs[] = {&c->accum, &c->fbuf, &c->sbuf, &c->pot, &c->tw, &c->zpart, &c->bbox_part,
                     &c->scal, &c->counter, &c->forces, &c->gtmp, &c->part, &c->gen, &c->sortbuf,
-                    &c->hy, &c->hg, &c->big, &c->bigtw, &c->y64, &c->r64};
+                    &c->hy, &c->hg, &c->big, &c->bigtw, &c->y64, &c->r64, &c->dgrid,
+                    &c->plan_table};
   for (DevBuf* b : bufs) release(*b);
   if (c->shadow) fitsne_destroy(c->shadow);
+  if (c->h_dgrid) cudaFreeHost(c->h_dgrid);
   comm_free(c);
   free_tiled(c);
   if (c->ev_in) cudaEventDestroy(c->ev_in);
@@ -208,6 +210,11 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     if (value < 0 || value > 2) { set_error("FFT path must be 0, 1 or 2"); return FITSNE_EINVAL; }
     ctx->fft_path = value;
     if (ctx->shadow) ctx->shadow->fft_path = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_DEVICE_GRID) {
+    if (value < 0 || value > 1) { set_error("device grid mode must be 0 or 1"); return FITSNE_EINVAL; }
+    ctx->devgrid = value;
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_RELABEL) {

@@ -15,6 +15,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "fft.cuh"
 #include "interp.cuh"
 #include "internal.h"
 
@@ -493,9 +494,17 @@ k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ 
           const double* __restrict__ scal, const T* __restrict__ attr, T alpha,
           T* __restrict__ grad, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel,
           T* __restrict__ gains, int32_t* __restrict__ status, T* __restrict__ attr_clear,
-          const double* __restrict__ frep64) {
+          const double* __restrict__ frep64, const GridArgs* __restrict__ gd) {
   // frep64: F_rep precomputed by the fp64 grid pipeline (ctx->wide), else
-  // gathered here from the potentials
+  // gathered here from the potentials.  gd: the device-computed grid of the
+  // device-grid schedule (the block does nothing if it is not valid)
+  if (gd) {
+    __shared__ GridArgs s_g;
+    if (threadIdx.x == 0) s_g = *gd;
+    __syncthreads();
+    if (s_g.status != kDevGridOk) return;
+    g = s_g;
+  }
   const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   int bad = 0;
   if (i < n) {
@@ -553,18 +562,20 @@ static int side_stream(fitsne_ctx* ctx) {
 template <typename T, bool STEP>
 static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void* attr, double alpha,
                           void* grad, double momentum, double lr, void* Yout, void* vel,
-                          void* gains, int32_t* status, bool clear, cudaStream_t st) {
-  const GridArgs g = grid_args(ctx->grid);
+                          void* gains, int32_t* status, bool clear, cudaStream_t st,
+                          const GridArgs* gd = nullptr) {
+  const GridArgs g = gd ? GridArgs{} : grid_args(ctx->grid);
   const int blocks = nblocks(n);
   double* frep64 = nullptr;
-  if (ctx->wide) FITSNE_TRY(shadow_frep(ctx, Y, n, &frep64, st));
+  if (!gd && ctx->wide) FITSNE_TRY(shadow_frep(ctx, Y, n, &frep64, st));
 #define CMB(S, P)                                                                              \
   k_combine<T, S, P, STEP><<<blocks, kBlock, 0, st>>>(                                         \
       (const T*)Y, n, g, (const T*)ctx->pot.ptr, (const double*)ctx->scal.ptr, (const T*)attr, \
       (T)alpha, (T*)grad, (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, status,            \
-      clear ? (T*)attr : (T*)nullptr, frep64)
-  if (ctx->dims == 1) { if (g.p == 3) CMB(1, 3); else CMB(1, 0); }
-  else { if (g.p == 3) CMB(2, 3); else CMB(2, 0); }
+      clear ? (T*)attr : (T*)nullptr, frep64, gd)
+  const int pp = gd ? ctx->p : g.p;  // a device grid has the context's p
+  if (ctx->dims == 1) { if (pp == 3) CMB(1, 3); else CMB(1, 0); }
+  else { if (pp == 3) CMB(2, 3); else CMB(2, 0); }
 #undef CMB
   FITSNE_CHECK_LAUNCH();
   if (clear) tiled_consumed(ctx);
@@ -613,6 +624,131 @@ static int out_stream(fitsne_ctx* ctx) {
   return FITSNE_OK;
 }
 
+// ---------------------------------------------------------------------------
+// Device-grid schedule.  The grid (n_intervals, hence the FFT length) depends
+// on the data (nbody.py:134), so the host used to wait for a 40-byte bbox
+// readback before it could launch the spread and FFT stages -- ~25 us on the
+// repulsion chain, which ends after the SpMV.  Here k_bbox computes the grid
+// on the device with the host's formulas and the spread / FFT / combine
+// stages, launched at once for a capacity (the previous grid's n_intervals +
+// 8), read it from device memory.  The host still reads the box back, but
+// after everything is queued, to check the device grid against its own and
+// to handle the rare case the capacity was too small (or the grid needs the
+// fp64 / non-band pipeline): the device stages then did nothing and the host
+// path runs behind them.
+// ---------------------------------------------------------------------------
+static bool devgrid_applicable(const fitsne_ctx* ctx) {
+  return ctx->devgrid && ctx->dg_cap_nint > 0 && ctx->dtype == FITSNE_F32 && ctx->dims == 2 && ctx->p == 3 &&
+         (ctx->sorted_spread == 1 || ctx->sorted_spread == 3) && ctx->grid_f64 != 2 && ctx->fft_path != 2 &&
+         ctx->n_total < (1LL << 31);
+}
+
+// n_intervals capacity for the next call after a grid g (0: the device path
+// does not apply to grids like g: wide, too many box rows, long FFT)
+static int devgrid_capacity(const fitsne_ctx* ctx, const fitsne_grid& g) {
+  if (ctx->dtype != FITSNE_F32 || ctx->dims != 2 || g.points_per_interval != 3) return 0;
+  double widest = 0;
+  for (int d = 0; d < g.dims; ++d) widest = std::max(widest, g.hi[d] - g.lo[d]);
+  if (ctx->grid_f64 == 1 && widest > kWideSpan) return 0;
+  const int cap = std::min(1024, g.n_intervals + 8);
+  if (smooth23_at_least(2 * 3 * cap - 1) > 5184) return 0;
+  return cap;
+}
+
+static inline int cap_L(int cap_nint) { return smooth23_at_least(2 * 3 * cap_nint - 1); }
+
+// Queues bbox (side), the SpMV (st, via spmv()), then the repulsion chain on
+// the side stream; st waits for the chain.  *gd = the device grid when the
+// device-grid schedule was used (the caller passes it to the combine and
+// calls devgrid_finish after queueing it), else null (host path, grid known).
+template <typename SpmvFn>
+static int repulsion_beside_spmv(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st, SpmvFn spmv,
+                                 const GridArgs** gd) {
+  *gd = nullptr;
+  FITSNE_TRY(side_stream(ctx));
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
+  FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
+  if (devgrid_applicable(ctx)) {
+    const int cap = ctx->dg_cap_nint, n_cap = 3 * cap, L_cap = cap_L(cap);
+    FITSNE_TRY(ensure(ctx->dgrid, sizeof(DevGrid)));
+    if (!ctx->h_dgrid) FITSNE_CUDA(cudaMallocHost(&ctx->h_dgrid, sizeof(DevGrid)));
+    FITSNE_TRY(out_stream(ctx));
+    GridArgs* dg = (GridArgs*)ctx->dgrid.ptr;
+    DevGridReq rq;
+    rq.min_intervals = ctx->min_intervals;
+    rq.p = ctx->p;
+    rq.ipi = ctx->intervals_per_integer;
+    rq.cap_nint = cap;
+    rq.cap_L = L_cap;
+    rq.max_nint = 1024;
+    rq.wide_span = ctx->grid_f64 == 1 ? kWideSpan : 0.0;
+    rq.zero = band_counters(ctx, n, &rq.zero_words);
+    FITSNE_TRY(device_plan_table(ctx, 65536, &rq.plans, &rq.nplans));
+    if (!rq.zero) { set_error("device allocation failed"); return FITSNE_ENOMEM; }
+    FITSNE_TRY(bbox_launch_devgrid(ctx, Y, n, dg, rq, ctx->h_dgrid, ctx->side, ctx->out, ctx->ev_piece[0]));
+    FITSNE_TRY(spmv());
+    FITSNE_TRY(ensure_accum_nodes(ctx, (size_t)n_cap * n_cap, ctx->side));
+    FITSNE_TRY(spread_band(ctx, Y, n, ctx->accum.ptr, ctx->side, dg));
+    FITSNE_TRY(fft_tsne_dev(ctx, ctx->accum.ptr, n, dg, n_cap, L_cap, ctx->side));
+    ctx->accum_live_reps = 1;  // consumed and cleared by the FFT stage (or untouched)
+    *gd = dg;
+  } else {
+    FITSNE_TRY(bbox_launch(ctx, Y, n, ctx->side));
+    FITSNE_TRY(spmv());
+    FITSNE_TRY(make_grid_finish(ctx, ctx->side));
+    FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
+    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+    const int cap = devgrid_capacity(ctx, ctx->grid);
+    ctx->dg_cap_nint = cap;
+  }
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+  FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+  return FITSNE_OK;
+}
+
+// After the device-grid stages and their consumers are queued: read the box,
+// derive the host grid, check the device one; on a capacity miss queue the
+// host-grid chain (*fallback = true: the caller re-queues its consumers).
+static int devgrid_finish(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st, bool* fallback) {
+  *fallback = false;
+  FITSNE_CUDA(cudaEventSynchronize(ctx->ev_bbox));
+  const int S = ctx->dims;
+  const double* hb = reinterpret_cast<const DevGrid*>(ctx->h_dgrid)->bbox;
+  if (hb[2 * S] != 0.0) {
+    tiled_mark_dirty(ctx, st);  // the skipped combine did not clear F_attr
+    set_error("points must be finite");
+    return FITSNE_EPOINTS;
+  }
+  double bbox[4];
+  for (int d = 0; d < 2 * S; ++d) bbox[d] = hb[d];
+  fitsne_grid g;
+  FITSNE_TRY(grid_from_bbox(ctx, bbox, &g));
+  const GridArgs& dgh = *ctx->h_dgrid;
+  if (dgh.status == kDevGridOk) {
+    bool same = dgh.n_int == g.n_intervals && dgh.L == g.fft_len && dgh.n == g.nodes_per_dim;
+    for (int d = 0; d < g.dims; ++d) same = same && dgh.lo[d] == g.lo[d] && dgh.hi[d] == g.hi[d] && dgh.h[d] == g.spacing[d];
+    if (!same) {
+      set_error("device grid differs from the host grid formulas");
+      return FITSNE_ECUDA;
+    }
+    ctx->grid = g;
+    ctx->grid_valid = true;
+    ctx->wide = false;
+    if (g.n_intervals + 4 > ctx->dg_cap_nint) ctx->dg_cap_nint = devgrid_capacity(ctx, g);
+    return FITSNE_OK;
+  }
+  // the device stages skipped: run the host-grid chain behind them
+  *fallback = true;
+  ++ctx->dg_fallbacks;
+  FITSNE_TRY(install_grid(ctx, g, ctx->side));
+  FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
+  FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
+  FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+  ctx->dg_cap_nint = devgrid_capacity(ctx, g);
+  return FITSNE_OK;
+}
+
 static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha, void* grad,
                                     cudaStream_t st, void* grad_host);
 
@@ -621,12 +757,52 @@ int gradient_overlapped(fitsne_ctx* ctx, const void* Y, double alpha, void* grad
   return join_on_error(ctx, gradient_overlapped_impl(ctx, Y, alpha, grad, st, grad_host));
 }
 
+// the gradient's combine (optionally in point ranges with overlapped copy-out)
+static int queue_combine(fitsne_ctx* ctx, const void* Y, int64_t n, void* attr, bool clear, double alpha,
+                         void* grad, void* grad_host, const GridArgs* gd, cudaStream_t st) {
+  if (grad_host) {
+    // host result: combine in point ranges, each range's device-to-host copy
+    // (copy stream) overlapping the next range's combine
+    FITSNE_TRY(out_stream(ctx));
+    const size_t row_bytes = dsize(ctx->dtype) * (size_t)ctx->dims;
+    constexpr int kParts = 4;
+    for (int q = 0; q < kParts; ++q) {
+      const int64_t r0 = n * q / kParts, nr = n * (q + 1) / kParts - r0;
+      if (nr <= 0) continue;
+      const size_t off = row_bytes * (size_t)r0;
+      if (ctx->dtype == FITSNE_F32)
+        FITSNE_TRY((launch_combine<float, false>(ctx, (const unsigned char*)Y + off, nr,
+                                                 (unsigned char*)attr + off, alpha,
+                                                 (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
+                                                 nullptr, nullptr, clear, st, gd)));
+      else
+        FITSNE_TRY((launch_combine<double, false>(ctx, (const unsigned char*)Y + off, nr,
+                                                  (unsigned char*)attr + off, alpha,
+                                                  (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
+                                                  nullptr, nullptr, clear, st, gd)));
+      FITSNE_CUDA(cudaEventRecord(ctx->ev_piece[q], st));
+      FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_piece[q], 0));
+      FITSNE_CUDA(cudaMemcpyAsync((unsigned char*)grad_host + off, (unsigned char*)grad + off,
+                                  row_bytes * (size_t)nr, cudaMemcpyDeviceToHost, ctx->out));
+    }
+    FITSNE_CUDA(cudaEventRecord(ctx->ev_out, ctx->out));
+    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_out, 0));
+    return FITSNE_OK;
+  }
+  if (ctx->dtype == FITSNE_F32)
+    return launch_combine<float, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr, nullptr,
+                                        nullptr, clear, st, gd);
+  return launch_combine<double, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr, nullptr,
+                                       nullptr, clear, st, gd);
+}
+
 static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha, void* grad,
                                     cudaStream_t st, void* grad_host) {
   FITSNE_RANGE("gradient_schedule");
   const int64_t n = ctx->n_total;
   void* attr = nullptr;
   bool clear = false;
+  const GridArgs* gd = nullptr;
   if (ctx->overlap == 0) {
     FITSNE_TRY(make_grid(ctx, Y, n, st));
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, st));
@@ -646,53 +822,20 @@ static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha
   } else {
     // bbox kernels first on the side stream (dispatched ahead of the SpMV, so
     // they get the whole GPU for a few microseconds), then the SpMV on st,
-    // then -- once the 40-byte bbox readback lands -- spread + FFT on the side
-    // stream, which fill the SM slots the SpMV leaves
-    FITSNE_TRY(side_stream(ctx));
-    FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
-    FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
-    FITSNE_TRY(bbox_launch(ctx, Y, n, ctx->side));
-    FITSNE_TRY(spmv_for_combine(ctx, Y, false, st, &attr, &clear));
-    FITSNE_TRY(make_grid_finish(ctx, ctx->side));
-    FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
-    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
-    FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
-    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+    // then spread + FFT on the side stream, which fill the SM slots the SpMV
+    // leaves (device-grid schedule: queued at once; host path: after the
+    // 40-byte bbox readback)
+    FITSNE_TRY(repulsion_beside_spmv(ctx, Y, n, st,
+                                     [&]() { return spmv_for_combine(ctx, Y, false, st, &attr, &clear); },
+                                     &gd));
   }
-  if (grad_host) {
-    // host result: combine in point ranges, each range's device-to-host copy
-    // (copy stream) overlapping the next range's combine
-    FITSNE_TRY(out_stream(ctx));
-    const size_t row_bytes = dsize(ctx->dtype) * (size_t)ctx->dims;
-    constexpr int kParts = 4;
-    for (int q = 0; q < kParts; ++q) {
-      const int64_t r0 = n * q / kParts, nr = n * (q + 1) / kParts - r0;
-      if (nr <= 0) continue;
-      const size_t off = row_bytes * (size_t)r0;
-      if (ctx->dtype == FITSNE_F32)
-        FITSNE_TRY((launch_combine<float, false>(ctx, (const unsigned char*)Y + off, nr,
-                                                 (unsigned char*)attr + off, alpha,
-                                                 (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
-                                                 nullptr, nullptr, clear, st)));
-      else
-        FITSNE_TRY((launch_combine<double, false>(ctx, (const unsigned char*)Y + off, nr,
-                                                  (unsigned char*)attr + off, alpha,
-                                                  (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
-                                                  nullptr, nullptr, clear, st)));
-      FITSNE_CUDA(cudaEventRecord(ctx->ev_piece[q], st));
-      FITSNE_CUDA(cudaStreamWaitEvent(ctx->out, ctx->ev_piece[q], 0));
-      FITSNE_CUDA(cudaMemcpyAsync((unsigned char*)grad_host + off, (unsigned char*)grad + off,
-                                  row_bytes * (size_t)nr, cudaMemcpyDeviceToHost, ctx->out));
-    }
-    FITSNE_CUDA(cudaEventRecord(ctx->ev_out, ctx->out));
-    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_out, 0));
-    return FITSNE_OK;
+  FITSNE_TRY(queue_combine(ctx, Y, n, attr, clear, alpha, grad, grad_host, gd, st));
+  if (gd) {
+    bool fb = false;
+    FITSNE_TRY(devgrid_finish(ctx, Y, n, st, &fb));
+    if (fb) FITSNE_TRY(queue_combine(ctx, Y, n, attr, clear, alpha, grad, grad_host, nullptr, st));
   }
-  if (ctx->dtype == FITSNE_F32)
-    return launch_combine<float, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
-                                        nullptr, nullptr, clear, st);
-  return launch_combine<double, false>(ctx, Y, n, attr, alpha, grad, 0, 0, nullptr, nullptr,
-                                       nullptr, nullptr, clear, st);
+  return FITSNE_OK;
 }
 
 // Gradient with host buffers (fitsne_gradient_host).  Y is copied in on st;
@@ -808,6 +951,7 @@ static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
   void* attr = nullptr;
   bool clear = false;
+  const GridArgs* gd = nullptr;
   if (ctx->overlap == 0) {
     FITSNE_TRY(make_grid(ctx, Yin, n, st));
     FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, st));
@@ -824,29 +968,32 @@ static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void
     FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
     FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
   } else {
-    FITSNE_TRY(side_stream(ctx));
-    FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
-    FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
-    // bbox on the side stream, SpMV + KL partials on st (queued before the
-    // bbox readback blocks the host), spread + FFT on the side stream
-    FITSNE_TRY(bbox_launch(ctx, Yin, n, ctx->side));
-    FITSNE_TRY(spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear));
-    FITSNE_TRY(make_grid_finish(ctx, ctx->side));
-    FITSNE_TRY(spread_tsne(ctx, Yin, n, nullptr, ctx->side));
-    FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
-    FITSNE_CUDA(cudaEventRecord(ctx->ev_done, ctx->side));
-    FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_done, 0));
+    // bbox on the side stream, SpMV + KL partials on st, spread + FFT on the
+    // side stream (device-grid schedule or after the bbox readback)
+    FITSNE_TRY(repulsion_beside_spmv(
+        ctx, Yin, n, st, [&]() { return spmv_for_combine(ctx, Yin, kl_dev != nullptr, st, &attr, &clear); },
+        &gd));
   }
-  if (ctx->dtype == FITSNE_F32)
-    FITSNE_TRY((launch_combine<float, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
-                                             vel, gains, status_dev, clear, st)));
-  else
-    FITSNE_TRY((launch_combine<double, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
-                                              vel, gains, status_dev, clear, st)));
-  if (kl_dev) {
-    k_kl_final<<<1, 1024, 0, st>>>(ctx->kl_part, ctx->kl_nparts, (const double*)ctx->scal.ptr,
-                                  ctx->plogp, ctx->psum, kl_dev);
-    FITSNE_CHECK_LAUNCH();
+  // the step's combine + update, then the KL of the pre-step embedding
+  auto consumers = [&](const GridArgs* g) -> int {
+    if (ctx->dtype == FITSNE_F32)
+      FITSNE_TRY((launch_combine<float, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
+                                               vel, gains, status_dev, clear, st, g)));
+    else
+      FITSNE_TRY((launch_combine<double, true>(ctx, Yin, n, attr, alpha, nullptr, momentum, lr, Yout,
+                                                vel, gains, status_dev, clear, st, g)));
+    if (kl_dev) {
+      k_kl_final<<<1, 1024, 0, st>>>(ctx->kl_part, ctx->kl_nparts, (const double*)ctx->scal.ptr,
+                                    ctx->plogp, ctx->psum, kl_dev);
+      FITSNE_CHECK_LAUNCH();
+    }
+    return FITSNE_OK;
+  };
+  FITSNE_TRY(consumers(gd));
+  if (gd) {
+    bool fb = false;
+    FITSNE_TRY(devgrid_finish(ctx, Yin, n, st, &fb));
+    if (fb) FITSNE_TRY(consumers(nullptr));
   }
   return FITSNE_OK;
 }

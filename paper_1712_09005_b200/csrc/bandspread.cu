@@ -40,6 +40,17 @@ static constexpr int kBandKeys = FITSNE_BAND_KEYS;    // (box rows in a chunk) x
 static constexpr int kBandMaxRows = 1024;             // n_int bound (fp32: n_int <= 864)
 static constexpr int kBandSmem = kBandChunk * 16 + kBandKeys * 4 + kBandChunk * 4;
 
+// device-grid schedule: the stage reads the grid k_bbox computed (gd) and
+// does nothing when that grid is not for it (status != 0; the host falls back)
+__device__ __forceinline__ bool dev_grid(GridArgs& g, const GridArgs* __restrict__ gd) {
+  if (!gd) return true;
+  __shared__ GridArgs s_g;
+  if (threadIdx.x == 0) s_g = *gd;
+  __syncthreads();
+  g = s_g;
+  return g.status == kDevGridOk;
+}
+
 __device__ __forceinline__ int band_cell(float y, const GridArgs& g, int d, float* w) {
   return box_weights3_f32(y, g.lo[d], g.h[d], g.lo_f[d], g.invh_f[d], g.guard[d], g.n_int, w);
 }
@@ -84,7 +95,9 @@ __device__ __forceinline__ void band_weights(float u, float* w) {
 // arbitrary; the reduce pass sorts each piece by box anyway, and the grid
 // accumulation is an unordered sum of float reductions already.)
 __global__ void __launch_bounds__(kBandBlock)
-k_band_rowcount(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* __restrict__ rowtot) {
+k_band_rowcount(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* __restrict__ rowtot,
+                const GridArgs* __restrict__ gd) {
+  if (!dev_grid(g, gd)) return;
   __shared__ uint32_t hist[kBandMaxRows];
   for (int r = threadIdx.x; r < g.n_int; r += kBandBlock) hist[r] = 0;
   __syncthreads();
@@ -101,7 +114,8 @@ k_band_rowcount(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* _
 
 __global__ void __launch_bounds__(kBandBlock)
 k_band_place(const float2* __restrict__ Y, int64_t n, GridArgs g, const uint32_t* __restrict__ rowtot,
-             uint32_t* __restrict__ rowcur, float2* __restrict__ sorted) {
+             uint32_t* __restrict__ rowcur, float2* __restrict__ sorted, const GridArgs* __restrict__ gd) {
+  if (!dev_grid(g, gd)) return;
   __shared__ uint32_t hist[kBandMaxRows];
   __shared__ uint32_t start[kBandMaxRows];
   __shared__ uint32_t part[kBandBlock];
@@ -179,7 +193,9 @@ __device__ __forceinline__ void band_flush(float* __restrict__ acc, int nn, int 
 // reduce pass over the box-row-sorted points: in-block counting sort by box,
 // then per-thread runs of kBandRun sorted points with one flush per box
 __global__ void __launch_bounds__(kBandBlock)
-k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __restrict__ acc) {
+k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __restrict__ acc,
+              const GridArgs* __restrict__ gd) {
+  if (!dev_grid(g, gd)) return;
   // dynamic shared memory (kBandSmem bytes): hist, points, (u_x, u_y), order, keys
   extern __shared__ __align__(16) unsigned char band_smem[];
   float2* pts = reinterpret_cast<float2*>(band_smem);
@@ -310,13 +326,24 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
   if (cur >= 0) band_flush(acc, nn, ccx, ccy, s);
 }
 
+// the row counters the band spread needs zeroed (the device-grid schedule
+// has k_bbox clear them instead of a memset on the chain)
+uint32_t* band_counters(fitsne_ctx* ctx, int64_t n, int* words) {
+  const size_t off_sorted = (2 * sizeof(uint32_t) * kBandMaxRows + 255) & ~(size_t)255;
+  if (ensure(ctx->sortbuf, off_sorted + sizeof(float2) * (size_t)n) != FITSNE_OK) return nullptr;
+  *words = 2 * kBandMaxRows;
+  return (uint32_t*)ctx->sortbuf.ptr;
+}
+
 bool band_spread_applies(const fitsne_ctx* ctx, int64_t n) {
   return ctx->dtype == FITSNE_F32 && ctx->dims == 2 && ctx->grid.points_per_interval == 3 &&
          ctx->grid.n_intervals <= kBandMaxRows && n > 0 && n < (1LL << 31);
 }
 
-int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
-  const GridArgs g = grid_args(ctx->grid);
+int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st,
+                const GridArgs* gd) {
+  // gd: the device-computed grid (the host's ctx->grid is not known yet)
+  const GridArgs g = gd ? GridArgs{} : grid_args(ctx->grid);
   const int nblk = (int)((n + kBandPts - 1) / kBandPts);
   // scratch: row totals + row cursors, then the sorted points (16-byte aligned)
   const size_t off_rows = 0;
@@ -326,10 +353,10 @@ int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
   uint32_t* rowtot = (uint32_t*)(base + off_rows);
   uint32_t* rowcur = rowtot + kBandMaxRows;
   float2* sorted = (float2*)(base + off_sorted);
-  FITSNE_CUDA(cudaMemsetAsync(rowtot, 0, 2 * sizeof(uint32_t) * kBandMaxRows, st));
-  k_band_rowcount<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot);
+  if (!gd) FITSNE_CUDA(cudaMemsetAsync(rowtot, 0, 2 * sizeof(uint32_t) * kBandMaxRows, st));
+  k_band_rowcount<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, gd);
   FITSNE_CHECK_LAUNCH();
-  k_band_place<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, rowcur, sorted);
+  k_band_place<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, rowcur, sorted, gd);
   FITSNE_CHECK_LAUNCH();
   const int nred = (int)((n + kBandChunk - 1) / kBandChunk);
   {
@@ -342,7 +369,7 @@ int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
       configured.insert(ctx->device);
     }
   }
-  k_band_reduce<<<nred, kBandBlock, kBandSmem, st>>>(sorted, n, g, (float*)accum);
+  k_band_reduce<<<nred, kBandBlock, kBandSmem, st>>>(sorted, n, g, (float*)accum, gd);
   FITSNE_CHECK_LAUNCH();
   return FITSNE_OK;
 }

@@ -94,9 +94,36 @@ struct GridArgs {
   int p;
   int n;   // nodes per dim
   int L;   // FFT length
+  // device-computed grids (kDevGrid*): 0 = valid for the launched stages,
+  // else why the stages skipped it and the host must run the fallback
+  int status;
 };
 
-inline GridArgs grid_args(const fitsne_grid& g) {
+// What the device-grid schedule asks k_bbox for: the make_grid options and
+// the capacity the dependent stages were launched with
+struct DevGridReq {
+  int min_intervals = 20;
+  int p = 3;
+  double ipi = 1.0;
+  int cap_nint = 0;      // n_intervals the launch shapes cover
+  int cap_L = 0;         // FFT length they cover
+  int max_nint = 1024;   // band spread limit
+  double wide_span = 0;  // > 0: wider spans need the fp64 grid (host path)
+  uint32_t* zero = nullptr;  // words the dependent stages need zeroed (band spread row counters)
+  int zero_words = 0;
+  const void* plans = nullptr;  // FftPlan table for the 2^a 3^b lengths (ascending), host-built
+  int nplans = 0;
+};
+
+// fp32 contexts run their grid stages in fp64 beyond this span (repulsion.cu)
+constexpr double kWideSpan = 256.0;
+
+// status values of a device-computed grid
+constexpr int kDevGridOk = 0;
+constexpr int kDevGridCapacity = 100;  // larger than the capacity the stages were launched for
+constexpr int kDevGridOther = 101;     // needs another pipeline (fp64 grid, other spread, error)
+
+__host__ __device__ inline GridArgs grid_args(const fitsne_grid& g) {
   GridArgs a;
   for (int d = 0; d < 2; ++d) {
     a.lo[d] = g.lo[d];
@@ -121,6 +148,7 @@ inline GridArgs grid_args(const fitsne_grid& g) {
   a.p = g.points_per_interval;
   a.n = g.nodes_per_dim;
   a.L = g.fft_len;
+  a.status = kDevGridOk;
   return a;
 }
 
@@ -155,6 +183,7 @@ struct DevBuf {
 };
 
 struct TiledP;  // tiled copy of P (tiled.cu)
+struct GridArgs;
 struct Comm;    // NCCL communicator state (comm.cu)
 
 }  // namespace fitsne
@@ -199,6 +228,16 @@ struct fitsne_ctx {
   bool wide = false;             // the current grid runs on the fp64 shadow
   fitsne_ctx* shadow = nullptr;  // fp64 twin context holding that pipeline
   fitsne::DevBuf y64;            // points converted for the shadow
+  // device-grid schedule (attract.cu): the grid k_bbox computes on the
+  // device, its pinned host copy, and the n_intervals capacity the stages
+  // are launched for (0: not yet known -- the next call takes the host path)
+  int devgrid = 0;
+  fitsne::DevBuf dgrid;
+  fitsne::GridArgs* h_dgrid = nullptr;
+  int dg_cap_nint = 0;
+  int dg_fallbacks = 0;          // calls that fell back to the host grid (diagnostics)
+  fitsne::DevBuf plan_table;     // FftPlan of every 2^a 3^b length <= plan_table_max
+  int plan_table_max = 0, plan_table_n = 0;
   fitsne::DevBuf r64;            // shadow gather outputs (F_rep, k1, k2)
   int sorted_spread = 1;      // 0 direct scatter, 1 auto (band spread for fp32 2-D p = 3, else box-sorted when crowded), 2 box-sorted, 3 band
   int spread_replicas = 4;    // replicas of the internal spread accumulator (power of two)

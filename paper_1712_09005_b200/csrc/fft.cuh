@@ -92,6 +92,18 @@ __host__ __device__ inline void make_plan(FftPlan& pl, int L) {
   pl.L = L;
 }
 
+// Device-grid block (device-grid schedule, attract.cu): the grid k_bbox
+// computes on the device, the Stockham plan of its FFT length (built once
+// there instead of in every FFT block) and the box it came from.
+struct DevGrid {
+  GridArgs g;
+  FftPlan pl;
+  double bbox[8];
+};
+__device__ __forceinline__ const FftPlan* dev_plan(const GridArgs* gd) {
+  return &reinterpret_cast<const DevGrid*>(gd)->pl;
+}
+
 // `tw` is normally the block's shared-memory copy of the table (stage_twiddles)
 template <typename V>
 __device__ __forceinline__ V twiddle(const V* __restrict__ tw, int idx, bool inv) {

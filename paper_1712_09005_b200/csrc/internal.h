@@ -22,6 +22,15 @@ int bbox_wait(fitsne_ctx* ctx, double* bbox_host);
 int bbox_device(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, cudaStream_t st);
 int make_grid_finish(fitsne_ctx* ctx, cudaStream_t st);
 
+// device-grid schedule (the grid computed by k_bbox on the device; no host
+// round trip before the spread / FFT stages) -----------------------------------
+int bbox_launch_devgrid(fitsne_ctx* ctx, const void* Y, int64_t n, GridArgs* gd, const DevGridReq& rq,
+                        GridArgs* gd_host, cudaStream_t st, cudaStream_t copy_st, cudaEvent_t ev_k);
+int fft_tsne_dev(fitsne_ctx* ctx, void* accum, int64_t n_total, const GridArgs* gd, int n_cap, int L_cap,
+                 cudaStream_t st);
+int ensure_accum_nodes(fitsne_ctx* ctx, size_t g_nodes, cudaStream_t st);
+int device_plan_table(fitsne_ctx* ctx, int L_max, const void** table, int* count);
+
 // repulsion pipeline ------------------------------------------------------------
 // spread of the t-SNE charges (1, y_0[, y_1]) into ctx->accum (or `accum`)
 int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
@@ -84,12 +93,15 @@ int comm_free(fitsne_ctx* ctx);  // comm.cu
 // the tiled F_attr buffer's consumer (which clears it) has been queued
 void tiled_consumed(fitsne_ctx* ctx);
 bool tiled_relabeled(const fitsne_ctx* ctx);  // the tiled copy runs over relabelled points
+void tiled_mark_dirty(fitsne_ctx* ctx, cudaStream_t st);  // a queued consumer did not run
 // error exit of a multi-stream schedule: wait for the internal streams so no
 // queued work outlives the call (the next call reuses their buffers)
 int join_on_error(fitsne_ctx* ctx, int rc);
 // band spread (bandspread.cu): fp32, 2-D, p = 3, n_int <= 1024
 bool band_spread_applies(const fitsne_ctx* ctx, int64_t n);
-int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
+uint32_t* band_counters(fitsne_ctx* ctx, int64_t n, int* words);
+int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st,
+                const GridArgs* gd = nullptr);
 // The tiled SpMV as kTiledPieces launches over consecutive row ranges (each
 // over the whole persistent grid), so a consumer can start on the rows of
 // piece k while piece k + 1 runs.  Row range of piece k: [rows[k], rows[k+1]).

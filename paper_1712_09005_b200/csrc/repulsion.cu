@@ -17,6 +17,7 @@
 // the reference's sum of K1 potentials (optimizer.py:206, 241).
 #include <cmath>
 #include <algorithm>
+#include <vector>
 
 #include "common.cuh"
 #include "fft.cuh"
@@ -37,9 +38,55 @@ static inline int grid_for(int64_t n, int block = kBlock) {
 // =============================================================================
 // a1: bounding box (nbody.py:131-133) and grid formulas (nbody.py:134-143)
 // =============================================================================
+// The grid formulas of make_grid (nbody.py:131-143) on the device, operation
+// for operation as grid_from_bbox computes them on the host (explicit IEEE
+// roundings, no contraction), so both sides derive the same lo, hi, spacing
+// and n_intervals from the same box.
+__device__ int device_grid(const double* mn, const double* mx, int S, const DevGridReq& rq, fitsne_grid* out) {
+  double lo[2] = {0, 0}, hi[2] = {0, 0}, span[2] = {0, 0};
+  double widest = -INFINITY;
+  for (int d = 0; d < S; ++d) {
+    lo[d] = mn[d];
+    hi[d] = mx[d];
+    if (!isfinite(lo[d]) || !isfinite(hi[d])) return FITSNE_EPOINTS;
+    span[d] = __dsub_rn(hi[d], lo[d]);
+    widest = fmax(widest, span[d]);
+  }
+  const double cells = (rq.ipi == 1.0) ? ceil(widest) : ceil(__dmul_rn(widest, rq.ipi));
+  if (cells > 1e7) return FITSNE_ETOOBIG;
+  const int n_int = max(rq.min_intervals, (int)cells);
+  for (int d = 0; d < S; ++d) {
+    if (span[d] < 1.0) {
+      const double c = __dmul_rn(0.5, __dadd_rn(lo[d], hi[d]));
+      lo[d] = __dsub_rn(c, 0.5);
+      hi[d] = __dadd_rn(c, 0.5);
+    } else {
+      const double pad = __dmul_rn(1e-6, span[d]);
+      lo[d] = __dsub_rn(lo[d], pad);
+      hi[d] = __dadd_rn(hi[d], pad);
+    }
+  }
+  const long long nn = (long long)n_int * rq.p;
+  if (nn > (1 << 20)) return FITSNE_ETOOBIG;
+  fitsne_grid g{};
+  g.dims = S;
+  g.n_intervals = n_int;
+  g.points_per_interval = rq.p;
+  g.nodes_per_dim = (int)nn;
+  for (int d = 0; d < S; ++d) {
+    g.lo[d] = lo[d];
+    g.hi[d] = hi[d];
+    g.spacing[d] = __ddiv_rn(__dsub_rn(hi[d], lo[d]), (double)nn);
+  }
+  g.fft_len = smooth23_at_least(2 * (int)nn - 1);
+  *out = g;
+  return FITSNE_OK;
+}
+
 template <typename T, int S>
 __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ part,
-                       int* __restrict__ nonfinite, double* __restrict__ out, int negate_max) {
+                       int* __restrict__ nonfinite, double* __restrict__ out, int negate_max,
+                       GridArgs* __restrict__ dgrid, DevGridReq rq) {
   double mn[S], mx[S];
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
@@ -91,6 +138,7 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
   __syncthreads();
   if (!last) return;
   __threadfence();
+  for (int k = threadIdx.x; k < rq.zero_words; k += blockDim.x) rq.zero[k] = 0u;
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
   for (int b = threadIdx.x; b < (int)gridDim.x; b += blockDim.x) {
@@ -118,8 +166,39 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
     const double sg = negate_max ? -1.0 : 1.0;
 #pragma unroll
     for (int d = 0; d < S; ++d) { out[d] = mn[d]; out[S + d] = sg * mx[d]; }
-    out[2 * S] = sg * (double)__ldcg(nonfinite);
+    const int bad = __ldcg(nonfinite);
+    out[2 * S] = sg * (double)bad;
     nonfinite[1] = 0;  // ticket reset for the next launch
+    if (dgrid) {
+      // the grid for the stages queued behind this kernel (device-grid schedule)
+      fitsne_grid g;
+      int rc = bad ? FITSNE_EPOINTS : device_grid(mn, mx, S, rq, &g);
+      GridArgs a;
+      if (rc == FITSNE_OK) {
+        a = grid_args(g);
+        double widest = 0;
+        for (int d = 0; d < S; ++d) widest = fmax(widest, g.hi[d] - g.lo[d]);
+        if (g.n_intervals > rq.cap_nint || g.fft_len > rq.cap_L) a.status = kDevGridCapacity;
+        else if (g.n_intervals > rq.max_nint || (rq.wide_span > 0 && widest > rq.wide_span))
+          a.status = kDevGridOther;
+      } else {
+        a = GridArgs{};
+        a.status = kDevGridOther;
+      }
+      DevGrid* blk = reinterpret_cast<DevGrid*>(dgrid);
+      if (a.status == kDevGridOk) {
+        // the plan of L from the host-built table (binary search by length)
+        const FftPlan* tab = reinterpret_cast<const FftPlan*>(rq.plans);
+        int lo_i = 0, hi_i = rq.nplans - 1;
+        while (lo_i < hi_i) {
+          const int mid = (lo_i + hi_i) >> 1;
+          if (tab[mid].L < a.L) lo_i = mid + 1; else hi_i = mid;
+        }
+        if (tab[lo_i].L == a.L) blk->pl = tab[lo_i];
+        else a.status = kDevGridOther;
+      }
+      blk->g = a;
+    }
   }
 }
 
@@ -131,7 +210,8 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
 // k_bbox into out_dev (null: ctx's readback buffer) on st; negate_max for the
 // MIN-all-reduce layout of fitsne_bbox_device
 static int bbox_kernels(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, int negate_max,
-                        cudaStream_t st, double** outd_used) {
+                        cudaStream_t st, double** outd_used, GridArgs* dgrid = nullptr,
+                        DevGridReq rq = DevGridReq{}) {
   const int S = ctx->dims;
   int nblk = (int)std::min<int64_t>(std::max<int64_t>((n + kBlock - 1) / kBlock, 1), 4 * ctx->num_sms);
   FITSNE_TRY(ensure(ctx->bbox_part, sizeof(double) * (size_t)nblk * 2 * S + 64));
@@ -142,11 +222,11 @@ static int bbox_kernels(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_d
   // flag[0]: non-finite, flag[1]: last-block ticket (k_bbox folds the partials)
   FITSNE_CUDA(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
   if (ctx->dtype == FITSNE_F32) {
-    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max);
-    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max);
+    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max, dgrid, rq);
+    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max, dgrid, rq);
   } else {
-    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max);
-    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max);
+    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max, dgrid, rq);
+    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max, dgrid, rq);
   }
   FITSNE_CHECK_LAUNCH();
   if (outd_used) *outd_used = outd;
@@ -251,7 +331,11 @@ int grid_from_bbox(fitsne_ctx* ctx, const double* bbox, fitsne_grid* out) {
 }
 
 template <typename T>
-__global__ void k_twiddles(typename C2<T>::type* tw, int L) {
+__global__ void k_twiddles(typename C2<T>::type* tw, int L, const GridArgs* __restrict__ gd = nullptr) {
+  if (gd) {
+    if (gd->status != kDevGridOk) return;
+    L = gd->L;
+  }
   for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < L; m += gridDim.x * blockDim.x) {
     double s, c;
     sincospi(2.0 * (double)m / (double)L, &s, &c);
@@ -272,7 +356,6 @@ __global__ void k_twiddles(typename C2<T>::type* tw, int L) {
 // the FFT stage transforms and the gather interpolates in double, and F_rep
 // is rounded to fp32 only at the end.  The attractive SpMV is unaffected.
 // ---------------------------------------------------------------------------
-static constexpr double kWideSpan = 256.0;
 
 __global__ void k_widen(const float* __restrict__ x, int64_t m, double* __restrict__ y) {
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
@@ -678,6 +761,21 @@ int spread_general(fitsne_ctx* ctx, const void* Y, int64_t n, const void* q, int
 // =============================================================================
 enum ConvMode { MODE_TSNE = 0, MODE_GENERAL = 1 };
 
+// Device-grid schedule (gd != null): the FFT stages were launched for a
+// capacity (n_cap rows, L_cap columns, shared memory for L_cap) before the
+// host knew the grid; they read the grid k_bbox computed, blocks beyond its
+// n / L return at once, and the Stockham plan of its L is built in shared
+// memory.  Returns false when the whole block has nothing to do.
+__device__ __forceinline__ bool stage_grid(GridArgs& g, const GridArgs* __restrict__ gd, const FftPlan& pl_arg,
+                                           const FftPlan** pl_use) {
+  *pl_use = &pl_arg;
+  if (!gd) return true;
+  g = *gd;
+  if (g.status != kDevGridOk) return false;
+  *pl_use = dev_plan(gd);
+  return true;
+}
+
 template <typename T>
 __device__ __forceinline__ void kernel_pair(int i, int j, double hx, double hy, T& k1, T& k2) {
   // first[i, j] = K((i hx)^2 + (j hy)^2), nbody.py:272-275
@@ -696,18 +794,24 @@ template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int pair0, int npair,
                typename C2<T>::type* __restrict__ F, typename C2<T>::type* __restrict__ Sbuf,
-               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int merged,
-               int nrep, int64_t rstride) {
+               GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl_arg, int merged,
+               int nrep, int64_t rstride, const GridArgs* __restrict__ gd = nullptr) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftPlan* plp;
+  if (!stage_grid(g, gd, pl_arg, &plp)) return;
   const int L = g.L, n = g.n;
   const int PL = plen(L);
   const int H = L / 2 + 1;
+  // unmerged launches put the data rows first: [0, split) data, [split, 2 split) spectrum
+  const int split = gd ? (int)gridDim.x / 2 : n;
+  const bool do_data = merged || (int)blockIdx.x < split;
+  const bool do_spec = merged || (int)blockIdx.x >= split;
+  const int x = (merged || (int)blockIdx.x < split) ? (int)blockIdx.x : (int)blockIdx.x - split;
+  if (x >= n) return;  // capacity beyond the device grid
+  const FftPlan& pl = *plp;
   V* s_tw = reinterpret_cast<V*>(smem_raw);
   V* a = s_tw + L;
-  const bool do_data = merged || (int)blockIdx.x < n;
-  const bool do_spec = merged || (int)blockIdx.x >= n;
-  const int x = (merged || (int)blockIdx.x < n) ? (int)blockIdx.x : (int)blockIdx.x - n;
   const int ns = do_data ? ((MODE == MODE_TSNE) ? 2 : npair) : 0;
   const int nsig = ns + (do_spec ? 1 : 0);
   V* b = a + (size_t)nsig * PL;
@@ -803,16 +907,20 @@ constexpr int kSpecCols = 4;
 template <typename T>
 __global__ void __launch_bounds__(256)
 k_spec_cols(const typename C2<T>::type* __restrict__ Sbuf, GridArgs g,
-            const typename C2<T>::type* __restrict__ tw, FftPlan pl,
-            typename C2<T>::type* __restrict__ Khat, int cpb) {
+            const typename C2<T>::type* __restrict__ tw, FftPlan pl_arg,
+            typename C2<T>::type* __restrict__ Khat, int cpb, const GridArgs* __restrict__ gd = nullptr) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftPlan* plp;
+  if (!stage_grid(g, gd, pl_arg, &plp)) return;
   const int L = g.L, n = g.n, H = L / 2 + 1;
+  const int ky0 = blockIdx.x * cpb;  // cpb <= kSpecCols columns per block
+  if (ky0 >= H) return;
+  const FftPlan& pl = *plp;
   const int PL = plen(L);
   V* s_tw = reinterpret_cast<V*>(smem_raw);
   V* a = s_tw + L;
   V* b = a + (size_t)cpb * PL;
-  const int ky0 = blockIdx.x * cpb;  // cpb <= kSpecCols columns per block
   const int nc = min(cpb, H - ky0);
   stage_twiddles(s_tw, tw, L);
   // each row i contributes kSpecCols consecutive spectrum columns (32 B)
@@ -847,15 +955,19 @@ constexpr int kColsMax = 4;  // columns per k_cols block (upper bound)
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restrict__ Khat,
-       GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int kern,
-       int with_k1, double* __restrict__ zpart, int cpb) {
+       GridArgs g, const typename C2<T>::type* __restrict__ tw, FftPlan pl_arg, int npair, int kern,
+       int with_k1, double* __restrict__ zpart, int cpb, const GridArgs* __restrict__ gd = nullptr) {
   // cpb (<= kColsMax) adjacent columns per block: the strided column reads
   // then use whole 32-byte sectors instead of 8 bytes of each
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftPlan* plp;
+  if (!stage_grid(g, gd, pl_arg, &plp)) return;
   const int L = g.L, n = g.n;
   const int PL = plen(L);
   const int col0 = blockIdx.x * cpb;
+  if (col0 >= L) return;
+  const FftPlan& pl = *plp;
   const int nc = min(cpb, L - col0);
   const int nsig = nc * npair;  // signal c * npair + q: column col0 + c, pair q
   V* s_tw = reinterpret_cast<V*>(smem_raw);
@@ -950,17 +1062,21 @@ k_cols(typename C2<T>::type* __restrict__ F, const typename C2<T>::type* __restr
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
 k_rows_inverse(const typename C2<T>::type* __restrict__ F, GridArgs g,
-               const typename C2<T>::type* __restrict__ tw, FftPlan pl, int npair, int ncol,
+               const typename C2<T>::type* __restrict__ tw, FftPlan pl_arg, int npair, int ncol,
                int pair0, T* __restrict__ pot, T* __restrict__ out, const double* __restrict__ zpart,
-               double* __restrict__ scal, double n_total) {
+               double* __restrict__ scal, double n_total, const GridArgs* __restrict__ gd = nullptr) {
   using V = typename C2<T>::type;
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  const FftPlan* plp;
+  if (!stage_grid(g, gd, pl_arg, &plp)) return;
   const int L = g.L, n = g.n;
+  const int x = blockIdx.x;
+  if (x >= n) return;
+  const FftPlan& pl = *plp;
   const int PL = plen(L);
   V* s_tw = reinterpret_cast<V*>(smem_raw);
   V* a = s_tw + L;
   V* b = a + (size_t)npair * PL;
-  const int x = blockIdx.x;
   stage_twiddles(s_tw, tw, L);
   for (int q = 0; q < npair; ++q)
     for (int k0 = threadIdx.x; k0 < L; k0 += 4 * blockDim.x) {
@@ -1245,6 +1361,113 @@ int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaSt
     rc = run_conv<double, MODE_TSNE>(ctx, (double*)accum, nullptr, 3, 0, with_k1, nullptr, n_total, st);
   if (rc == FITSNE_OK && accum == ctx->accum.ptr) ctx->accum_clean = true;  // consumed + cleared
   return rc;
+}
+
+// FFT stage of the device-grid schedule (fp32, 2-D, t-SNE channels): launch
+// shapes and buffers for n_cap nodes per dim and length L_cap, grid read by
+// the kernels from gd.  Consumes and clears the accumulator like fft_tsne.
+int fft_tsne_dev(fitsne_ctx* ctx, void* accum_v, int64_t n_total, const GridArgs* gd, int n_cap, int L_cap,
+                 cudaStream_t st) {
+  using T = float;
+  using V = float2;
+  constexpr int MODE = MODE_TSNE;
+  const int H_cap = L_cap / 2 + 1;
+  FITSNE_TRY(ensure(ctx->fbuf, sizeof(V) * 2 * (size_t)n_cap * L_cap));
+  FITSNE_TRY(ensure(ctx->sbuf, sizeof(V) * ((size_t)n_cap * H_cap + (size_t)H_cap * L_cap)));
+  FITSNE_TRY(ensure(ctx->zpart, sizeof(double) * (size_t)L_cap));
+  FITSNE_TRY(ensure(ctx->pot, sizeof(T) * (size_t)n_cap * n_cap * kNodeSlots));
+  FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
+  FITSNE_TRY(ensure(ctx->tw, sizeof(V) * (size_t)L_cap));
+  T* accum = (T*)accum_v;
+  V* F = (V*)ctx->fbuf.ptr;
+  V* Sb = (V*)ctx->sbuf.ptr;
+  V* Kh = Sb + (size_t)n_cap * H_cap;
+  double* zp = (double*)ctx->zpart.ptr;
+  V* tw = (V*)ctx->tw.ptr;
+  const GridArgs g0{};
+  const FftPlan pl0{};
+  k_twiddles<T><<<grid_for(L_cap), kBlock, 0, st>>>(tw, L_cap, gd);
+  FITSNE_CHECK_LAUNCH();
+  ctx->tw_len = -1;  // the table now follows the device grid
+  const int merged = sizeof(V) * ((size_t)L_cap + 2 * 3 * (size_t)plen(L_cap)) <= 113 * 1024 ? 1 : 0;
+  const size_t smem_r = sizeof(V) * ((size_t)L_cap + 2 * (size_t)(merged ? 3 : 2) * plen(L_cap));
+  FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
+  k_rows_forward<T, MODE><<<merged ? n_cap : 2 * n_cap, 256, smem_r, st>>>(
+      accum, nullptr, 3, 0, 2, F, Sb, g0, tw, pl0, merged, 1, 0, gd);
+  FITSNE_CHECK_LAUNCH();
+  int cpb = kSpecCols;
+  auto smem_spec = [&](int c) { return sizeof(V) * ((size_t)L_cap + 2 * (size_t)c * plen(L_cap)); };
+  while (cpb > 1 && smem_spec(cpb) > 227 * 1024) cpb /= 2;
+  FITSNE_TRY(set_smem<T>((const void*)k_spec_cols<T>, smem_spec(cpb)));
+  k_spec_cols<T><<<(H_cap + cpb - 1) / cpb, 256, smem_spec(cpb), st>>>(Sb, g0, tw, pl0, Kh, cpb, gd);
+  FITSNE_CHECK_LAUNCH();
+  auto smem_cols = [&](int c) { return sizeof(V) * ((size_t)L_cap + 2 * (size_t)c * 2 * plen(L_cap)); };
+  int ccols = std::min(kColsMax, ctx->cols_per_block);
+  while (ccols > 1 && smem_cols(ccols) > 227 * 1024) ccols /= 2;
+  FITSNE_TRY(set_smem<T>((const void*)k_cols<T, MODE>, smem_cols(ccols)));
+  k_cols<T, MODE><<<(L_cap + ccols - 1) / ccols, 256, smem_cols(ccols), st>>>(F, Kh, g0, tw, pl0, 2, 0, 0, zp,
+                                                                               ccols, gd);
+  FITSNE_CHECK_LAUNCH();
+  const size_t smem_i = sizeof(V) * ((size_t)L_cap + 2 * 2 * (size_t)plen(L_cap));
+  FITSNE_TRY(set_smem<T>((const void*)k_rows_inverse<T, MODE>, smem_i));
+  k_rows_inverse<T, MODE><<<n_cap, 256, smem_i, st>>>(F, g0, tw, pl0, 2, 3, 0, (T*)ctx->pot.ptr, nullptr, zp,
+                                                      (double*)ctx->scal.ptr, (double)n_total, gd);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
+// the internal accumulator sized for G_cap nodes (one replica suffices for the
+// band spread, but the direct scatter of a fallback may use all replicas)
+int ensure_accum_nodes(fitsne_ctx* ctx, size_t g_nodes, cudaStream_t st) {
+  const size_t bytes = g_nodes * kNodeSlots * dsize(ctx->dtype) * (size_t)ctx->spread_replicas;
+  if (ctx->accum.cap < bytes) {
+    FITSNE_TRY(ensure(ctx->accum, bytes));
+    ctx->accum_clean = false;
+  }
+  if (!ctx->accum_clean) {
+    FITSNE_CUDA(cudaMemsetAsync(ctx->accum.ptr, 0, ctx->accum.cap, st));
+    ctx->accum_clean = true;
+  }
+  return FITSNE_OK;
+}
+
+// device-grid schedule: bbox kernels that also compute the grid into gd
+// Stockham plans of every 2^a 3^b length up to L_max (ascending), built on the
+// host once per context and kept on the device for the device-grid schedule
+int device_plan_table(fitsne_ctx* ctx, int L_max, const void** table, int* count) {
+  if (ctx->plan_table_max < L_max) {
+    std::vector<FftPlan> plans;
+    for (long long p2 = 1; p2 <= L_max; p2 *= 2)
+      for (long long v = p2; v <= L_max; v *= 3) {
+        FftPlan pl;
+        make_plan(pl, (int)v);
+        plans.push_back(pl);
+      }
+    std::sort(plans.begin(), plans.end(), [](const FftPlan& a, const FftPlan& b) { return a.L < b.L; });
+    FITSNE_TRY(ensure(ctx->plan_table, sizeof(FftPlan) * plans.size()));
+    FITSNE_CUDA(cudaMemcpy(ctx->plan_table.ptr, plans.data(), sizeof(FftPlan) * plans.size(),
+                           cudaMemcpyHostToDevice));
+    ctx->plan_table_max = L_max;
+    ctx->plan_table_n = (int)plans.size();
+  }
+  *table = ctx->plan_table.ptr;
+  *count = ctx->plan_table_n;
+  return FITSNE_OK;
+}
+
+// gd points at a DevGrid block {grid, plan, bbox}; the readback of that
+// block goes on copy_st (behind an event), so the stages queued on st after
+// the bbox kernel do not wait for it
+int bbox_launch_devgrid(fitsne_ctx* ctx, const void* Y, int64_t n, GridArgs* gd, const DevGridReq& rq,
+                        GridArgs* gd_host, cudaStream_t st, cudaStream_t copy_st, cudaEvent_t ev_k) {
+  double* outd = reinterpret_cast<DevGrid*>(gd)->bbox;
+  FITSNE_TRY(bbox_kernels(ctx, Y, n, outd, 0, st, nullptr, gd, rq));
+  FITSNE_CUDA(cudaEventRecord(ev_k, st));
+  FITSNE_CUDA(cudaStreamWaitEvent(copy_st, ev_k, 0));
+  FITSNE_CUDA(cudaMemcpyAsync(gd_host, gd, sizeof(DevGrid), cudaMemcpyDeviceToHost, copy_st));
+  if (!ctx->ev_bbox) FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_bbox, cudaEventDisableTiming));
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_bbox, copy_st));
+  return FITSNE_OK;
 }
 
 int matvec_general(fitsne_ctx* ctx, int kernel, const void* coeffs, int ncol, void* out,

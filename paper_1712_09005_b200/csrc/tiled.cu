@@ -1458,6 +1458,12 @@ static int tiled_begin(fitsne_ctx* ctx, cudaStream_t st) {
 
 bool tiled_relabeled(const fitsne_ctx* ctx) { return ctx->tiled && ctx->tiled->relabeled; }
 
+void tiled_mark_dirty(fitsne_ctx* ctx, cudaStream_t st) {
+  if (!ctx->tiled) return;
+  ctx->tiled->dirty = true;
+  ctx->tiled->dirty_stream = st;
+}
+
 void tiled_consumed(fitsne_ctx* ctx) {
   if (ctx->tiled) ctx->tiled->dirty = false;
 }

@@ -420,3 +420,54 @@ class TestErrors:
         with pytest.raises(FloatingPointError):
             opt.step(state, np.zeros((1, 2)), np.array([[np.nan, 0.0]]))
         assert state.iteration == 0
+
+
+class TestDeviceGrid:
+    """The device-grid schedule (grid computed by k_bbox, stages queued before
+    the host sees it) against the host-grid schedule and the oracle, across
+    calls whose span grows past the launch capacity (host fallback) and
+    shrinks, for the gradient (device and host buffers) and the fused step."""
+
+    def _P(self, n, rng):
+        from paper_1712_09005_b200.affinities import SparseAffinities
+        r = np.repeat(np.arange(n), 10)
+        cc = rng.integers(0, n - 1, n * 10)
+        cc = cc + (cc >= r)
+        key = np.unique(np.minimum(r, cc) * n + np.maximum(r, cc))
+        v = rng.exponential(1.0, key.size)
+        return SparseAffinities(n=n, rows=key // n, cols=key % n, values=v / (2 * v.sum()))
+
+    def test_growing_and_shrinking_spans(self, fs):
+        from paper_1712_09005_b200 import _lib
+        _, _, opt, _ = fs
+        rng = np.random.default_rng(31)
+        n = 30_000
+        P = self._P(n, rng)
+        base = rng.standard_normal((n, 2))
+        with _lib.option(_lib.OPT_DEVICE_GRID, 1):
+            for scale in (20.0, 22.0, 40.0, 41.0, 80.0, 30.0, 10.0, 0.05, 60.0, 140.0):
+                y = (base * scale).astype(np.float32)
+                ref = O.grad(P.rows, P.cols, P.values, y.astype(np.float64), 4.0, 50, 3, "fft")
+                g_dev = opt.gradient(P, torch.from_numpy(y).cuda(), 4.0, 50, 3, "fft").double().cpu().numpy()
+                g_host = opt.gradient(P, y, 4.0, 50, 3, "fft")
+                assert rel_l2(g_dev, ref) <= 1e-3, scale
+                assert rel_l2(g_host, ref) <= 1e-3, scale
+        with _lib.option(_lib.OPT_DEVICE_GRID, 0):
+            g0 = opt.gradient(P, torch.from_numpy(y).cuda(), 4.0, 50, 3, "fft").double().cpu().numpy()
+        assert rel_l2(g_dev, g0) <= 1e-5
+
+    def test_fused_run_matches_host_grid_schedule(self, fs):
+        from paper_1712_09005_b200 import _lib
+        _, _, opt, _ = fs
+        rng = np.random.default_rng(32)
+        P = self._P(20_000, rng)
+        cfg = opt.TsneConfig(dims=2, n_iter=300, learning_rate=2000.0, min_intervals=50,
+                             exaggeration=opt.ExaggerationSchedule(12.0, 100), seed=0, pca_dims=None,
+                             repulsion_method="fft", dtype="float32")
+        with _lib.option(_lib.OPT_DEVICE_GRID, 1):
+            a = opt.run_tsne(affinities=P, config=cfg)
+        with _lib.option(_lib.OPT_DEVICE_GRID, 0):
+            b = opt.run_tsne(affinities=P, config=cfg)
+        # same schedule of the same math: identical up to float atomics order
+        assert np.max(np.abs(a.kl_log[:20] - b.kl_log[:20]) / b.kl_log[:20]) <= 1e-5
+        assert abs(a.kl_log[-1] - b.kl_log[-1]) / b.kl_log[-1] <= 2e-2
