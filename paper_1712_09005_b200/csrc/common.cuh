@@ -160,9 +160,16 @@ constexpr int kMaxP = 8;
 // p^2-node gather reads 9 x 16 B = 144 contiguous bytes (p = 3) instead of
 // three 48-byte pieces n records apart.  (Boxes own their nodes: node x
 // belongs to box x / p.)  1-D: the node order is already box-major.
+// records per box: p^2 rounded up to even, so each box starts 32-byte
+// aligned in fp32 (p = 3: 10 records = 160 B, read with five 256-bit loads)
+__host__ __device__ __forceinline__ int pot_box_records(int p) { return (p * p + 1) & ~1; }
 __host__ __device__ __forceinline__ int64_t pot_box_node(int64_t bx, int64_t by, int a, int b, int p,
                                                          int n_int) {
-  return ((bx * n_int + by) * p + a) * p + b;
+  return (bx * n_int + by) * pot_box_records(p) + a * p + b;
+}
+// records of the potential buffer for a grid (2-D box-major, 1-D node order)
+__host__ __device__ __forceinline__ int64_t pot_records(int dims, int n_int, int p) {
+  return dims == 1 ? (int64_t)n_int * p : (int64_t)n_int * n_int * pot_box_records(p);
 }
 __host__ __device__ __forceinline__ int64_t pot_node(int64_t x, int64_t y, int p, int n_int) {
   const int64_t bx = x / p, by = y / p;

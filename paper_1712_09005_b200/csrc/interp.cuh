@@ -121,8 +121,29 @@ __device__ __forceinline__ void point_gather(const T (&yi)[S], const GridArgs& g
       c1 = box_weights3_f32((float)yi[S - 1], g.lo[S - 1], g.h[S - 1], g.lo_f[S - 1],
                             g.invh_f[S - 1], g.guard[S - 1], g.n_int, w1);
     FITSNE_DCHECK(c0 >= 0 && c0 < g.n_int && c1 >= 0 && c1 < g.n_int);
-    // box-major potentials: the 9 records of box (c0, c1) are contiguous
-    const int64_t box0 = (S == 1) ? (int64_t)c0 * 3 : pot_box_node(c0, c1, 0, 0, 3, g.n_int);
+    if constexpr (S == 2) {
+      // box-major potentials: the 9 records of box (c0, c1) are one 32-byte
+      // aligned 160-byte block, read with five 256-bit loads
+      const float* bp = reinterpret_cast<const float*>(pot) + pot_box_node(c0, c1, 0, 0, 3, g.n_int) * kNodeSlots;
+      float r[40];
+#pragma unroll
+      for (int k = 0; k < 5; ++k)
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[8 * k]), "=f"(r[8 * k + 1]), "=f"(r[8 * k + 2]), "=f"(r[8 * k + 3]),
+                       "=f"(r[8 * k + 4]), "=f"(r[8 * k + 5]), "=f"(r[8 * k + 6]), "=f"(r[8 * k + 7])
+                     : "l"(bp + 8 * k));
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b) {
+          const float wt = w0[a] * w1[b];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) phi[c] += r[(a * 3 + b) * 4 + c] * wt;
+        }
+      return;
+    }
+    // 1-D: the three records of the box are contiguous
+    const int64_t box0 = (int64_t)c0 * 3;
 #pragma unroll
     for (int a = 0; a < 3; ++a) {
       const int64_t rowbase = box0 + a * ((S == 1) ? 1 : 3);

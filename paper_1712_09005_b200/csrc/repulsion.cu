@@ -1352,7 +1352,9 @@ int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaSt
   }
   if (accum == nullptr) accum = ctx->accum.ptr;
   size_t G = accum_elems(ctx->grid) / kNodeSlots;
-  FITSNE_TRY(ensure(ctx->pot, G * kNodeSlots * dsize(ctx->dtype)));
+  FITSNE_TRY(ensure(ctx->pot, (size_t)pot_records(ctx->grid.dims, ctx->grid.n_intervals, ctx->grid.points_per_interval) *
+                                  kNodeSlots * dsize(ctx->dtype)));
+  (void)G;
   FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
   int rc;
   if (ctx->dtype == FITSNE_F32)
@@ -1375,7 +1377,7 @@ int fft_tsne_dev(fitsne_ctx* ctx, void* accum_v, int64_t n_total, const GridArgs
   FITSNE_TRY(ensure(ctx->fbuf, sizeof(V) * 2 * (size_t)n_cap * L_cap));
   FITSNE_TRY(ensure(ctx->sbuf, sizeof(V) * ((size_t)n_cap * H_cap + (size_t)H_cap * L_cap)));
   FITSNE_TRY(ensure(ctx->zpart, sizeof(double) * (size_t)L_cap));
-  FITSNE_TRY(ensure(ctx->pot, sizeof(T) * (size_t)n_cap * n_cap * kNodeSlots));
+  FITSNE_TRY(ensure(ctx->pot, sizeof(T) * (size_t)pot_records(2, n_cap / 3, 3) * kNodeSlots));
   FITSNE_TRY(ensure(ctx->scal, 64 * sizeof(double)));
   FITSNE_TRY(ensure(ctx->tw, sizeof(V) * (size_t)L_cap));
   T* accum = (T*)accum_v;
