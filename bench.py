@@ -386,19 +386,21 @@ def count_launches(fn):
             torch.cuda.synchronize()
         evs = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA
                and not e.name.startswith("Memcpy") and not e.name.startswith("Memset")]
-        return len(evs)
+        return len(evs) or None  # 0: CUPTI unavailable (e.g. under ncu), not a count
     except Exception:  # noqa: BLE001 - profiler unavailable: no count (never a guess)
         return None
 
 
-def timed(fn, steps, stream):
+def timed(fn, steps, stream, range_name="bench_timed"):
     import torch
     s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
+    torch.cuda.nvtx.range_push(range_name)  # ncu --nvtx --nvtx-include <range_name>/
     s.record(stream)
     for _ in range(steps):
         fn()
     e.record(stream)
+    torch.cuda.nvtx.range_pop()
     e.synchronize()
     return s.elapsed_time(e) / steps  # ms
 
@@ -445,7 +447,7 @@ def run_ours(args):
         dist.barrier()
         torch.cuda.synchronize()
         with ClockSampler(dev) as clk:
-            ms = timed(step, args.steps, stream)
+            ms = timed(step, args.steps, stream, "bench_step")
         # e2e per rank: this rank's Y rows from pinned host memory in, its
         # gradient rows out, every step (max over ranks of the same timing)
         st_ = ev.stages if args.torch_comm else None
@@ -552,7 +554,7 @@ def run_ours(args):
         step()
     torch.cuda.synchronize()
     with ClockSampler(dev) as clk:
-        ms = timed(step, args.steps, stream)
+        ms = timed(step, args.steps, stream, "bench_step")
     clocks = clk.summary()
 
     # grid facts for the record
