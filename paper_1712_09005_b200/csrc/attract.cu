@@ -100,48 +100,75 @@ __device__ __forceinline__ float cauchy_weight<float>(float p, float d2) {
 // w_ij = p_ij / (1 + d_ij^2), and (KL) klr += p_ij log1p(d_ij^2).  Each lane
 // first issues the (col, val) loads of kU stored entries, then their kU
 // neighbour gathers, so 2 kU independent loads are in flight per lane.
+constexpr int kRowU = 4;
+
+// (col, val) of the stored entries k0 + 32 u (u < kRowU) of a row ending at end
+template <typename T>
+__device__ __forceinline__ void row_chunk_load(const int32_t* __restrict__ col, const T* __restrict__ val,
+                                               int64_t k0, int64_t end, int32_t (&j)[kRowU],
+                                               T (&p)[kRowU]) {
+#pragma unroll
+  for (int u = 0; u < kRowU; ++u) {
+    const int64_t k = k0 + 32 * u;
+    const bool ok = k < end;
+    j[u] = ok ? __ldcs(col + k) : 0;
+    p[u] = ok ? __ldcs(val + k) : (T)0;
+  }
+}
+
+// gathers y_j of one loaded chunk and accumulates its terms
+template <typename T, int S, bool KL>
+__device__ __forceinline__ void row_chunk_reduce(const T* __restrict__ Y, int64_t k0, int64_t end,
+                                                 const int32_t (&j)[kRowU], const T (&p)[kRowU],
+                                                 const T (&yi)[S], T (&acc)[S], T& klr, uint64_t pol) {
+  T yj[kRowU][S];
+#pragma unroll
+  for (int u = 0; u < kRowU; ++u) {
+    if (k0 + 32 * u < end) load_point_el<T, S>(Y, j[u], yj[u], pol);
+    else {
+#pragma unroll
+      for (int d = 0; d < S; ++d) yj[u][d] = yi[d];
+    }
+  }
+#pragma unroll
+  for (int u = 0; u < kRowU; ++u) {
+    T df[S], s2 = 0;
+#pragma unroll
+    for (int d = 0; d < S; ++d) {
+      df[d] = yi[d] - yj[u][d];
+      s2 += df[d] * df[d];
+    }
+    const T w = cauchy_weight<T>(p[u], s2);
+#pragma unroll
+    for (int d = 0; d < S; ++d) acc[d] += w * df[d];
+    if (KL) {
+      if (p[u] > (T)0) klr += p[u] * fast_log1p<T>(s2);
+    }
+  }
+}
+
+// One warp reduces CSR row [beg, end) against y_i: acc += sum_j w_ij (y_i - y_j),
+// w_ij = p_ij / (1 + d_ij^2), and (KL) klr += p_ij log1p(d_ij^2).  Each lane
+// first issues the (col, val) loads of kRowU stored entries, then their
+// neighbour gathers, so 2 kRowU independent loads are in flight per lane.
+// skip: stored entries of the row already reduced by the caller (row
+// pipelining in k_attract reduces the first chunk itself).
 template <typename T, int S, bool KL>
 __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, const T* __restrict__ val,
                                            const T* __restrict__ Y, int64_t beg, int64_t end,
                                            int lane, const T (&yi)[S], T (&acc)[S], T& klr,
-                                           uint64_t pol) {
-  constexpr int kU = 4;
-  for (int64_t k0 = beg + lane; k0 < end; k0 += 32 * kU) {
-    int32_t j[kU];
-    T p[kU];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      const int64_t k = k0 + 32 * u;
-      const bool ok = k < end;
-      j[u] = ok ? __ldcs(col + k) : 0;
-      p[u] = ok ? __ldcs(val + k) : (T)0;
-    }
-    T yj[kU][S];
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      if (k0 + 32 * u < end) load_point_el<T, S>(Y, j[u], yj[u], pol);
-      else {
-#pragma unroll
-        for (int d = 0; d < S; ++d) yj[u][d] = yi[d];
-      }
-    }
-#pragma unroll
-    for (int u = 0; u < kU; ++u) {
-      T df[S], s2 = 0;
-#pragma unroll
-      for (int d = 0; d < S; ++d) {
-        df[d] = yi[d] - yj[u][d];
-        s2 += df[d] * df[d];
-      }
-      const T w = cauchy_weight<T>(p[u], s2);
-#pragma unroll
-      for (int d = 0; d < S; ++d) acc[d] += w * df[d];
-      if (KL) {
-        if (p[u] > (T)0) klr += p[u] * fast_log1p<T>(s2);
-      }
-    }
+                                           uint64_t pol, int skip = 0) {
+  for (int64_t k0 = beg + lane + skip; k0 < end; k0 += 32 * kRowU) {
+    int32_t j[kRowU];
+    T p[kRowU];
+    row_chunk_load<T>(col, val, k0, end, j, p);
+    row_chunk_reduce<T, S, KL>(Y, k0, end, j, p, yi, acc, klr, pol);
   }
 }
+
+#ifndef FITSNE_CSR_PIPE
+#define FITSNE_CSR_PIPE 1
+#endif
 
 // ---------------------------------------------------------------------------
 // warp-per-row CSR SpMV.  MODE 0: F_attr out.  MODE 1: gradient
@@ -151,7 +178,10 @@ __device__ __forceinline__ void row_reduce(const int32_t* __restrict__ col, cons
 // potential grid (lanes 0..p^s-1 each interpolate one node), so F_rep never
 // round-trips through HBM.
 template <typename T, int S, int MODE, bool KL, int P>
-__global__ void __launch_bounds__(kBlock, 6)
+#ifndef FITSNE_CSR_MINB
+#define FITSNE_CSR_MINB (FITSNE_CSR_PIPE ? 5 : 6)
+#endif
+__global__ void __launch_bounds__(kBlock, FITSNE_CSR_MINB)
 k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
           const T* __restrict__ val, const T* __restrict__ Y, int64_t n_rows, int64_t row_begin,
           const T* __restrict__ frep, T alpha, T* __restrict__ out, double* __restrict__ klpart,
@@ -192,6 +222,15 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
     }
     __syncwarp();
     const int mcount = (n_rows - t * 32 < 32) ? (int)(n_rows - t * 32) : 32;
+#if FITSNE_CSR_PIPE
+    // row pipelining: the first (col, val) chunk of row m + 1 is loaded before
+    // row m's neighbour gathers, so the HBM stream latency of the next row
+    // overlaps the gather latency of this one (short random-graph rows are
+    // one chunk each)
+    int32_t jn[kRowU];
+    T pn[kRowU];
+    row_chunk_load<T>(col, val, s_rb[wbase] + lane, s_re[wbase], jn, pn);
+#endif
     for (int m = 0; m < mcount; ++m) {
       T yi[S];
 #pragma unroll
@@ -202,7 +241,18 @@ k_attract(const int64_t* __restrict__ rowptr, const int32_t* __restrict__ col,
 #pragma unroll
       for (int d = 0; d < S; ++d) acc[d] = 0;
       T klr = 0;
+#if FITSNE_CSR_PIPE
+      int32_t jc[kRowU];
+      T pc[kRowU];
+#pragma unroll
+      for (int u = 0; u < kRowU; ++u) { jc[u] = jn[u]; pc[u] = pn[u]; }
+      if (m + 1 < mcount)
+        row_chunk_load<T>(col, val, s_rb[wbase + m + 1] + lane, s_re[wbase + m + 1], jn, pn);
+      row_chunk_reduce<T, S, KL>(Y, beg + lane, end, jc, pc, yi, acc, klr, pol);
+      row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr, pol, 32 * kRowU);
+#else
       row_reduce<T, S, KL>(col, val, Y, beg, end, lane, yi, acc, klr, pol);
+#endif
 #pragma unroll
       for (int d = 0; d < S; ++d) acc[d] = warp_sum(acc[d]);
       if (lane == m) {

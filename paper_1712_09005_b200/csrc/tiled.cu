@@ -78,6 +78,17 @@ static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
 #ifndef FITSNE_TILED_FASTPATH
 #define FITSNE_TILED_FASTPATH 0
 #endif
+// cross-tile pipelining: a consumer warp loads the first batch of its run in
+// the next tile before the tail of the current one (the run bounds follow
+// from the tile's TileLoad, so the header is not needed for it)
+#ifndef FITSNE_TILED_XPF
+#define FITSNE_TILED_XPF 0
+#endif
+// slabs cut by a warp-range boundary: 1 = add into the shared row-block
+// accumulator with a compare-and-swap loop, 0 = vector reduction to global
+#ifndef FITSNE_TILED_SCUT
+#define FITSNE_TILED_SCUT 1
+#endif
 static constexpr int kTiledU = FITSNE_TILED_U;    // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
 
@@ -1059,6 +1070,16 @@ template <> struct TPt<2> {
   static __device__ __forceinline__ T make(float a, float b) { return make_float2(a, b); }
   static __device__ __forceinline__ T add(T a, T b) { return make_float2(a.x + b.x, a.y + b.y); }
   static __device__ __forceinline__ bool nonzero(T a) { return a.x != 0.f || a.y != 0.f; }
+  // *p += (a, b) on shared memory, concurrent-safe (64-bit compare-and-swap)
+  static __device__ __forceinline__ void smem_add(T* p, float a, float b) {
+    unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
+    unsigned long long old = *q, was;
+    do {
+      was = old;
+      const float2 v = make_float2(__uint_as_float((uint32_t)was) + a, __uint_as_float((uint32_t)(was >> 32)) + b);
+      old = atomicCAS(q, was, ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x));
+    } while (old != was);
+  }
   // accumulate w (y_i - y_j), w = p / (1 + |y_i - y_j|^2); returns 1 + d^2
   static __device__ __forceinline__ float accum(T yi, T yj, float p, float& ax, float& ay) {
     const float dx = yi.x - yj.x, dy = yi.y - yj.y;
@@ -1077,6 +1098,7 @@ template <> struct TPt<1> {
   static __device__ __forceinline__ T make(float a, float) { return a; }
   static __device__ __forceinline__ T add(T a, T b) { return a + b; }
   static __device__ __forceinline__ bool nonzero(T a) { return a != 0.f; }
+  static __device__ __forceinline__ void smem_add(T* p, float a, float) { atomicAdd(p, a); }
   static __device__ __forceinline__ float accum(T yi, T yj, float p, float& ax, float&) {
     const float dx = yi - yj;
     const float q = 1.0f + dx * dx;
@@ -1196,6 +1218,23 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       if (Tr::nonzero(v)) atomicAdd(fattr + (rowmap ? (int64_t)rowmap[r0 + i] : r0 + i), v);
     }
   };
+  unsigned short cA[kTiledU], cB[kTiledU];
+  float pA[kTiledU], pB[kTiledU];
+#if FITSNE_TILED_XPF
+  // cB / pB: the first batch of this warp's run in the next tile
+  auto load_first = [&](int t) {
+    const TileLoad& d = tiles[t];
+    const int64_t gs = (int64_t)(uint32_t)d.g0 + tiled_run_lo(d.ng, warp);
+    const uint16_t* c = cols + (size_t)slot_index(gs, lane);
+    const float* v = vals + (size_t)slot_index(gs, lane);
+#pragma unroll
+    for (int u = 0; u < kTiledU; ++u) {
+      cB[u] = __ldcs(reinterpret_cast<const unsigned short*>(c) + u * 32);
+      pB[u] = __ldcs(v + u * 32);
+    }
+  };
+  if (t0 < t1) load_first(t0);
+#endif
   for (int t = t0; t < t1; ++t) {
     const int it = t - t0, b = it % kTiledStages;
     const unsigned char* st = ring + (size_t)b * stage_sz;
@@ -1226,6 +1265,11 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
     PT* accp = acc + (size_t)(it & 1) * R;
     const int lo = tiled_run_lo(ng, warp);
     const int hi = tiled_run_lo(ng, warp + 1);
+#if FITSNE_TILED_XPF
+#pragma unroll
+    for (int u = 0; u < kTiledU; ++u) { cA[u] = cB[u]; pA[u] = pB[u]; }
+    if (lo >= hi && t + 1 < t1) load_first(t + 1);
+#endif
     if (lo < hi) {
       int s = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
       int s_end = (int)goff[s + 1];
@@ -1237,12 +1281,15 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       // the (relabelled) row map's L2 latency is hidden behind the slab
       int64_t orow = 0;
       auto out_row = [&]() {
-        if (shared_slab && row != 0xFFFF) orow = rowmap ? (int64_t)__ldg(rowmap + r0 + row) : r0 + row;
+        if (!FITSNE_TILED_SCUT && shared_slab && row != 0xFFFF)
+          orow = rowmap ? (int64_t)__ldg(rowmap + r0 + row) : r0 + row;
       };
       out_row();
       auto flush_row = [&]() {
         if (row == 0xFFFF) return;
-        if (shared_slab) {
+        if (FITSNE_TILED_SCUT && shared_slab) {
+          Tr::smem_add(accp + row, ax, ay);  // the slab's other warps add to the same row
+        } else if (shared_slab) {
           // rows of a slab cut by a warp-range boundary are updated by two or
           // more warps of this tile: add straight to the output with a vector
           // reduction in L2 instead of a shared-memory compare-and-swap loop
@@ -1274,13 +1321,13 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       };
       const uint16_t* cp = cols + (size_t)slot_index(g0 + lo, lane);
       const float* vp = vals + (size_t)slot_index(g0 + lo, lane);
-      unsigned short cA[kTiledU], cB[kTiledU];
-      float pA[kTiledU], pB[kTiledU];
+#if !FITSNE_TILED_XPF
 #pragma unroll
       for (int u = 0; u < kTiledU; ++u) {
         cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
         pA[u] = __ldcs(vp + u * 32);
       }
+#endif
 #if FITSNE_TILED_DEPTH >= 3
       // two batches in flight: B holds the next batch, C is loaded ahead of it
       unsigned short cC[kTiledU];
@@ -1348,6 +1395,9 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         cp += kTiledU * 32;
         vp += kTiledU * 32;
       }
+#if FITSNE_TILED_XPF
+      if (t + 1 < t1) load_first(t + 1);
+#endif
 #pragma unroll
       for (int u = 0; u < kTiledU - 1; ++u)
         if (g + u < hi) step(g + u, cA[u], pA[u]);
