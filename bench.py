@@ -97,13 +97,17 @@ def parse():
                          "parallel.ShardedGradient) instead of the library's NCCL communicator")
     ap.add_argument("--spread-mode", type=int, default=1, choices=[0, 1, 2, 3],
                     help="0 direct atomics, 1 auto (default), 2 box-sorted")
-    ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2, 3],
+    ap.add_argument("--overlap-mode", type=int, default=1, choices=[0, 1, 2, 3, 4],
                     help="0 serial, 1 (default) SpMV || repulsion, 2 + priority repulsion stream")
     ap.add_argument("--spmv-blocks", type=int, default=0, help="persistent SpMV blocks per SM (0: one tile per warp)")
     ap.add_argument("--spread-replicas", type=int, default=4, help="spread accumulator replicas")
     ap.add_argument("--fft-cols", type=int, default=0, choices=[0, 1, 2, 4],
                     help="FITSNE_OPT_FFT_COLS: columns per block of the column FFT stage (0 = default)")
     ap.add_argument("--tile", default=None, help="ROWSxCOLS tile shape of the tiled SpMV (A/B)")
+    ap.add_argument("--side-gather", type=int, default=1, choices=[0, 1],
+                    help="gather F_rep on the repulsion stream beside the SpMV (A/B)")
+    ap.add_argument("--spmv-join", type=int, default=1, choices=[0, 1],
+                    help="second SpMV launch behind the repulsion chain joins the dynamic schedule (A/B)")
     ap.add_argument("--tiled-ctas", type=int, default=0,
                     help="FITSNE_OPT_TILED_CTAS: persistent grid of the tiled SpMV (0 = default)")
     return ap.parse_args()
@@ -536,6 +540,8 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_RELABEL, args.relabel), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_CTAS, args.tiled_ctas), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_DEVICE_GRID, args.device_grid), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SIDE_GATHER, args.side_gather), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SPMV_JOIN, args.spmv_join), "set_option")
     if args.tile:
         tr, tc = (int(v) for v in args.tile.lower().split("x"))
         _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILE_ROWS, tr), "set_option")

@@ -104,7 +104,9 @@ enum fitsne_option {
   FITSNE_OPT_FFT_PATH = 12,
   FITSNE_OPT_GRID_F64 = 13,
   FITSNE_OPT_RELABEL = 14,
-  FITSNE_OPT_DEVICE_GRID = 15
+  FITSNE_OPT_DEVICE_GRID = 15,
+  FITSNE_OPT_SIDE_GATHER = 16,
+  FITSNE_OPT_SPMV_JOIN = 17
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -141,6 +143,13 @@ enum fitsne_option {
  *   neighbourhoods get contiguous labels; results stay in the caller's
  *   order).  0 = caller's order; 1 (default) = relabel when that at least
  *   halves the (row, column chunk) segments of the tiles; 2 = always.
+ *   FITSNE_OPT_SIDE_GATHER: 1 (default) = with the band spread (fp32 2-D p = 3)
+ *   F_rep is gathered on the repulsion stream, in the spread's box order,
+ *   while the attractive SpMV still runs, and the combine after the SpMV only
+ *   streams 4 (alpha F_attr - F_rep); 0 = the combine gathers F_rep itself.
+ *   FITSNE_OPT_SPMV_JOIN: 1 (default) = when the repulsion chain beside the
+ *   tiled SpMV is done, a second SpMV launch on its stream joins the dynamic
+ *   work-unit schedule with the SMs the chain used; 0 = one launch only.
  *   FITSNE_OPT_DEVICE_GRID: 1 = fitsne_gradient / _host / _iterate compute
  *   the grid on the device and queue the spread and FFT stages without
  *   waiting for the bbox readback (the host checks the grid after queueing

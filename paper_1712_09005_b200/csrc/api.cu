@@ -162,7 +162,7 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_OVERLAP) {
-    if (value < 0 || value > 3) { set_error("overlap mode must be 0, 1, 2 or 3"); return FITSNE_EINVAL; }
+    if (value < 0 || value > 4) { set_error("overlap mode must be 0 .. 4"); return FITSNE_EINVAL; }
     if (ctx->side && value != ctx->overlap) {  // priority is fixed at creation
       cudaStreamSynchronize(ctx->side);
       cudaStreamDestroy(ctx->side);
@@ -241,6 +241,16 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
   if (option == FITSNE_OPT_TILED_BANK_ORDER) {
     if (value < 0 || value > 2) { set_error("bank order must be 0, 1 or 2"); return FITSNE_EINVAL; }
     ctx->tiled_bank_order = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_SPMV_JOIN) {
+    if (value < 0 || value > 1) { set_error("spmv join must be 0 or 1"); return FITSNE_EINVAL; }
+    ctx->spmv_join = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_SIDE_GATHER) {
+    if (value < 0 || value > 1) { set_error("side gather must be 0 or 1"); return FITSNE_EINVAL; }
+    ctx->side_gather = value;
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_TILED_CTAS) {

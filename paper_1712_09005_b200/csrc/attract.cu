@@ -544,9 +544,11 @@ k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ 
           const double* __restrict__ scal, const T* __restrict__ attr, T alpha,
           T* __restrict__ grad, T momentum, T lr, T* __restrict__ Yout, T* __restrict__ vel,
           T* __restrict__ gains, int32_t* __restrict__ status, T* __restrict__ attr_clear,
-          const double* __restrict__ frep64, const GridArgs* __restrict__ gd) {
-  // frep64: F_rep precomputed by the fp64 grid pipeline (ctx->wide), else
-  // gathered here from the potentials.  gd: the device-computed grid of the
+          const double* __restrict__ frep64, const GridArgs* __restrict__ gd,
+          const T* __restrict__ frep_t = nullptr) {
+  // frep64: F_rep precomputed by the fp64 grid pipeline (ctx->wide); frep_t:
+  // F_rep gathered on the repulsion stream while the SpMV ran (gather_band);
+  // else gathered here from the potentials.  gd: the device-computed grid of the
   // device-grid schedule (the block does nothing if it is not valid)
   if (gd) {
     __shared__ GridArgs s_g;
@@ -566,12 +568,12 @@ k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ 
       for (int d = 0; d < S; ++d) attr_clear[i * S + d] = (T)0;
     }
     T phi[4] = {0, 0, 0, 0};
-    if (!frep64) point_gather<T, S, P>(yi, g, pot, phi);
+    if (!frep64 && !frep_t) point_gather<T, S, P>(yi, g, pot, phi);
     const T Z = (T)scal[0];
 #pragma unroll
     for (int d = 0; d < S; ++d) {
       const int64_t o = i * S + d;
-      const T fr = frep64 ? (T)frep64[i * S + d] : frep_from_phi<T, S>(yi, phi, Z, d, g);
+      const T fr = frep_t ? frep_t[o] : (frep64 ? (T)frep64[o] : frep_from_phi<T, S>(yi, phi, Z, d, g));
       const T gd = (T)4 * (alpha * at[d] - fr);
       if (!STEP) {
         grad[o] = gd;
@@ -595,6 +597,34 @@ k_combine(const T* __restrict__ Y, int64_t n, GridArgs g, const T* __restrict__ 
   }
 }
 
+// The combine when F_rep was gathered beside the SpMV: a pure stream over the
+// points, grad = 4 (alpha F_attr - F_rep), F_attr cleared for the next pass.
+// 4 points (float2 each) per thread in flight.
+__global__ void __launch_bounds__(256)
+k_finish_stream(float2* __restrict__ attr, const float2* __restrict__ frep, int64_t n, float alpha,
+                float2* __restrict__ grad, int clear) {
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n; i += 4 * stride) {
+    float2 a[4], f[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      a[u] = attr[i + u * stride];
+      f[u] = __ldg(frep + i + u * stride);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      grad[i + u * stride] = make_float2(4.f * (alpha * a[u].x - f[u].x), 4.f * (alpha * a[u].y - f[u].y));
+      if (clear) attr[i + u * stride] = make_float2(0.f, 0.f);
+    }
+  }
+  for (; i < n; i += stride) {
+    const float2 a = attr[i], f = frep[i];
+    grad[i] = make_float2(4.f * (alpha * a.x - f.x), 4.f * (alpha * a.y - f.y));
+    if (clear) attr[i] = make_float2(0.f, 0.f);
+  }
+}
+
 // The repulsion pipeline runs on a HIGH-priority internal stream: the SpMV's
 // thousands of blocks would otherwise be dispatched before the bbox / FFT
 // blocks queued behind them and the overlap would collapse.
@@ -613,16 +643,29 @@ template <typename T, bool STEP>
 static int launch_combine(fitsne_ctx* ctx, const void* Y, int64_t n, const void* attr, double alpha,
                           void* grad, double momentum, double lr, void* Yout, void* vel,
                           void* gains, int32_t* status, bool clear, cudaStream_t st,
-                          const GridArgs* gd = nullptr) {
+                          const GridArgs* gd = nullptr, size_t frep_off = 0) {
   const GridArgs g = gd ? GridArgs{} : grid_args(ctx->grid);
   const int blocks = nblocks(n);
   double* frep64 = nullptr;
-  if (!gd && ctx->wide) FITSNE_TRY(shadow_frep(ctx, Y, n, &frep64, st));
+  // F_rep already gathered beside the SpMV (frep_off: byte offset of this point range)
+  const T* frep_t = (!gd && ctx->frep_ready && sizeof(T) == 4)
+                        ? (const T*)((const unsigned char*)ctx->frep32.ptr + frep_off) : nullptr;
+  if (!gd && ctx->wide && !frep_t) FITSNE_TRY(shadow_frep(ctx, Y, n, &frep64, st));
+  if constexpr (!STEP && sizeof(T) == 4) {
+    if (frep_t && ctx->dims == 2) {
+      const int sblocks = (int)std::min<int64_t>((n + 1023) / 1024, 4 * (int64_t)ctx->num_sms);
+      k_finish_stream<<<std::max(sblocks, 1), 256, 0, st>>>((float2*)attr, (const float2*)frep_t, n, (float)alpha,
+                                                          (float2*)grad, clear ? 1 : 0);
+      FITSNE_CHECK_LAUNCH();
+      if (clear) tiled_consumed(ctx);
+      return FITSNE_OK;
+    }
+  }
 #define CMB(S, P)                                                                              \
   k_combine<T, S, P, STEP><<<blocks, kBlock, 0, st>>>(                                         \
       (const T*)Y, n, g, (const T*)ctx->pot.ptr, (const double*)ctx->scal.ptr, (const T*)attr, \
       (T)alpha, (T*)grad, (T)momentum, (T)lr, (T*)Yout, (T*)vel, (T*)gains, status,            \
-      clear ? (T*)attr : (T*)nullptr, frep64, gd)
+      clear ? (T*)attr : (T*)nullptr, frep64, gd, frep_t)
   const int pp = gd ? ctx->p : g.p;  // a device grid has the context's p
   if (ctx->dims == 1) { if (pp == 3) CMB(1, 3); else CMB(1, 0); }
   else { if (pp == 3) CMB(2, 3); else CMB(2, 0); }
@@ -651,8 +694,10 @@ static int spmv_for_combine(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_
     ctx->kl_part = part;
     ctx->kl_nparts = np;
     *clear = true;
+    ctx->spmv_tiled_live = true;
     return FITSNE_OK;
   }
+  ctx->spmv_tiled_live = false;
   FITSNE_TRY(ensure(ctx->forces, dsize(ctx->dtype) * (size_t)ctx->n_total * ctx->dims));
   *attr = ctx->forces.ptr;
   *clear = false;
@@ -715,6 +760,8 @@ template <typename SpmvFn>
 static int repulsion_beside_spmv(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st, SpmvFn spmv,
                                  const GridArgs** gd) {
   *gd = nullptr;
+  ctx->frep_ready = false;
+  ctx->spmv_tiled_live = false;
   FITSNE_TRY(side_stream(ctx));
   FITSNE_CUDA(cudaEventRecord(ctx->ev_in, st));
   FITSNE_CUDA(cudaStreamWaitEvent(ctx->side, ctx->ev_in, 0));
@@ -743,11 +790,26 @@ static int repulsion_beside_spmv(fitsne_ctx* ctx, const void* Y, int64_t n, cuda
     ctx->accum_live_reps = 1;  // consumed and cleared by the FFT stage (or untouched)
     *gd = dg;
   } else {
+    // mode 4: the SpMV is dispatched first and the bbox runs on the SMs it leaves
+    if (ctx->overlap == 4) FITSNE_TRY(spmv());
     FITSNE_TRY(bbox_launch(ctx, Y, n, ctx->side));
-    FITSNE_TRY(spmv());
+    if (ctx->overlap != 4) FITSNE_TRY(spmv());
     FITSNE_TRY(make_grid_finish(ctx, ctx->side));
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
+    if (ctx->side_gather && ctx->band_sorted && ctx->band_n == n && !ctx->wide && ctx->dtype == FITSNE_F32) {
+      // F_rep gathered here, in the band spread's box order, while the SpMV
+      // still runs: the combine after the SpMV is then a pure stream
+      FITSNE_TRY(ensure(ctx->frep32, sizeof(float) * 2 * (size_t)n));
+      FITSNE_TRY(gather_band(ctx, n, ctx->frep32.ptr, ctx->side));
+      ctx->frep_ready = true;
+    }
+    if (ctx->spmv_join && ctx->spmv_tiled_live) {
+      // the chain is done: its SMs join the SpMV's dynamic schedule
+      int np = ctx->kl_nparts;
+      FITSNE_TRY(attract_tiled_join(ctx, Y, -1, ctx->side, &np));
+      ctx->kl_nparts = np;
+    }
     const int cap = devgrid_capacity(ctx, ctx->grid);
     ctx->dg_cap_nint = cap;
   }
@@ -824,7 +886,7 @@ static int queue_combine(fitsne_ctx* ctx, const void* Y, int64_t n, void* attr, 
         FITSNE_TRY((launch_combine<float, false>(ctx, (const unsigned char*)Y + off, nr,
                                                  (unsigned char*)attr + off, alpha,
                                                  (unsigned char*)grad + off, 0, 0, nullptr, nullptr,
-                                                 nullptr, nullptr, clear, st, gd)));
+                                                 nullptr, nullptr, clear, st, gd, off)));
       else
         FITSNE_TRY((launch_combine<double, false>(ctx, (const unsigned char*)Y + off, nr,
                                                   (unsigned char*)attr + off, alpha,
@@ -849,6 +911,7 @@ static int queue_combine(fitsne_ctx* ctx, const void* Y, int64_t n, void* attr, 
 static int gradient_overlapped_impl(fitsne_ctx* ctx, const void* Y, double alpha, void* grad,
                                     cudaStream_t st, void* grad_host) {
   FITSNE_RANGE("gradient_schedule");
+  ctx->frep_ready = false;
   const int64_t n = ctx->n_total;
   void* attr = nullptr;
   bool clear = false;
@@ -904,6 +967,7 @@ int gradient_host(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_
 static int gradient_host_impl(fitsne_ctx* ctx, const void* Y_host, double alpha, void* grad_host,
                               cudaStream_t st) {
   const int64_t n = ctx->n_total;
+  ctx->frep_ready = false;
   const size_t row_bytes = dsize(ctx->dtype) * (size_t)ctx->dims;
   const size_t bytes = row_bytes * (size_t)n;
   FITSNE_TRY(ensure(ctx->hy, bytes));
@@ -997,6 +1061,7 @@ static int iterate_fused_impl(fitsne_ctx* ctx, const void* Yin, void* Yout, void
                               double alpha, double momentum, double lr, double* kl_dev,
                               int32_t* status_dev, cudaStream_t st) {
   FITSNE_RANGE("iterate_schedule");
+  ctx->frep_ready = false;
   const int64_t n = ctx->n_total;
   if (!ctx->plogp_valid) FITSNE_TRY(compute_plogp(ctx, st));
   void* attr = nullptr;

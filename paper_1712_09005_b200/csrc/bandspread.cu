@@ -23,6 +23,7 @@
 
 #include "common.cuh"
 #include "internal.h"
+#include "interp.cuh"
 
 namespace fitsne {
 
@@ -114,7 +115,8 @@ k_band_rowcount(const float2* __restrict__ Y, int64_t n, GridArgs g, uint32_t* _
 
 __global__ void __launch_bounds__(kBandBlock)
 k_band_place(const float2* __restrict__ Y, int64_t n, GridArgs g, const uint32_t* __restrict__ rowtot,
-             uint32_t* __restrict__ rowcur, float2* __restrict__ sorted, const GridArgs* __restrict__ gd) {
+             uint32_t* __restrict__ rowcur, float2* __restrict__ sorted, uint32_t* __restrict__ sidx,
+             const GridArgs* __restrict__ gd) {
   if (!dev_grid(g, gd)) return;
   __shared__ uint32_t hist[kBandMaxRows];
   __shared__ uint32_t start[kBandMaxRows];
@@ -174,6 +176,7 @@ k_band_place(const float2* __restrict__ Y, int64_t n, GridArgs g, const uint32_t
     const uint32_t at = atomicAdd(&hist[band_cell(y.x, g, 0, w)], 1u);
     FITSNE_DCHECK(at < n);
     sorted[at] = y;
+    sidx[at] = (uint32_t)i;
   }
 }
 
@@ -193,8 +196,11 @@ __device__ __forceinline__ void band_flush(float* __restrict__ acc, int nn, int 
 // reduce pass over the box-row-sorted points: in-block counting sort by box,
 // then per-thread runs of kBandRun sorted points with one flush per box
 __global__ void __launch_bounds__(kBandBlock)
-k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __restrict__ acc,
+k_band_reduce(const float2* __restrict__ ys, const uint32_t* __restrict__ sidx, int64_t n, GridArgs g,
+              float* __restrict__ acc, float2* __restrict__ bs_pts, uint32_t* __restrict__ bs_idx,
               const GridArgs* __restrict__ gd) {
+  // bs_pts / bs_idx: the chunk's points and original indices in box order,
+  // kept for the box-ordered gather of F_rep (k_band_gather)
   if (!dev_grid(g, gd)) return;
   // dynamic shared memory (kBandSmem bytes): hist, points, (u_x, u_y), order, keys
   extern __shared__ __align__(16) unsigned char band_smem[];
@@ -234,6 +240,8 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
           s[a][b][2] = w * (y.y - g.cf[1]);
         }
       band_flush(acc, nn, cx, cy, s);
+      bs_pts[c0 + k] = y;
+      bs_idx[c0 + k] = sidx[c0 + k];
     }
     return;
   }
@@ -290,6 +298,11 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
     order[atomicAdd(&hist[keyof[k]], 1u)] = (uint16_t)k;
   }
   __syncthreads();
+  for (int q = tid; q < cnt; q += kBandBlock) {
+    const int k = order[q];
+    bs_pts[c0 + q] = pts[k];
+    bs_idx[c0 + q] = sidx[c0 + k];
+  }
   // runs of kBandRun sorted points per thread: register sums per box
   const int s0 = tid * kBandRun, s1 = min(cnt, s0 + kBandRun);
   float s[3][3][3];
@@ -326,11 +339,98 @@ k_band_reduce(const float2* __restrict__ ys, int64_t n, GridArgs g, float* __res
   if (cur >= 0) band_flush(acc, nn, ccx, ccy, s);
 }
 
+// F_rep of every point from the potentials (gather_potentials, nbody.py:344-350;
+// optimizer.py:203-210, 244), in the box order the reduce pass left: a thread
+// walks kBandRun consecutive points, which mostly share a box, and re-reads the
+// box's 160-byte record block only when the box changes; neighbouring threads
+// read neighbouring boxes.  Same arithmetic per point as k_combine's
+// point_gather + frep_from_phi (bit-identical F_rep), written at the point's
+// original index.
+__global__ void __launch_bounds__(kBandBlock)
+k_band_gather(const float2* __restrict__ bs_pts, const uint32_t* __restrict__ bs_idx, int64_t n, GridArgs g,
+              const float* __restrict__ pot, const double* __restrict__ scal, float2* __restrict__ frep) {
+  const int64_t q0 = (blockIdx.x * (int64_t)kBandBlock + threadIdx.x) * kBandRun;
+  if (q0 >= n) return;
+  const float Z = (float)scal[0];
+  float r[40];
+  int b0 = -1, b1 = -1;
+  const int cnt = (int)min((int64_t)kBandRun, n - q0);
+  for (int k = 0; k < cnt; ++k) {
+    const float2 y = bs_pts[q0 + k];
+    float w0[3], w1[3];
+    const int c0 = band_cell(y.x, g, 0, w0), c1 = band_cell(y.y, g, 1, w1);
+    if (c0 != b0 || c1 != b1) {
+      b0 = c0;
+      b1 = c1;
+      const float* bp = pot + pot_box_node(c0, c1, 0, 0, 3, g.n_int) * kNodeSlots;
+#pragma unroll
+      for (int j = 0; j < 5; ++j)
+        asm volatile("ld.global.nc.v8.f32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                     : "=f"(r[8 * j]), "=f"(r[8 * j + 1]), "=f"(r[8 * j + 2]), "=f"(r[8 * j + 3]),
+                       "=f"(r[8 * j + 4]), "=f"(r[8 * j + 5]), "=f"(r[8 * j + 6]), "=f"(r[8 * j + 7])
+                     : "l"(bp + 8 * j));
+    }
+    float phi[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+    for (int a = 0; a < 3; ++a)
+#pragma unroll
+      for (int b = 0; b < 3; ++b) {
+        const float wt = w0[a] * w1[b];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) phi[c] += r[(a * 3 + b) * 4 + c] * wt;
+      }
+    const float yi[2] = {y.x, y.y};
+    frep[bs_idx[q0 + k]] = make_float2(frep_from_phi<float, 2>(yi, phi, Z, 0, g),
+                                       frep_from_phi<float, 2>(yi, phi, Z, 1, g));
+  }
+}
+
+// scratch layout: row totals + row cursors, then (256-byte aligned) the
+// row-sorted points and indices, then their box-ordered copies
+struct BandBufs {
+  uint32_t *rowtot, *rowcur, *sidx, *bs_idx;
+  float2 *sorted, *bs_pts;
+};
+static inline size_t band_align(size_t x) { return (x + 255) & ~(size_t)255; }
+static size_t band_bytes(int64_t n) {
+  return band_align(2 * sizeof(uint32_t) * kBandMaxRows) + 2 * band_align(sizeof(float2) * (size_t)n) +
+         2 * band_align(sizeof(uint32_t) * (size_t)n);
+}
+static BandBufs band_bufs(unsigned char* base, int64_t n) {
+  BandBufs b;
+  b.rowtot = (uint32_t*)base;
+  b.rowcur = b.rowtot + kBandMaxRows;
+  unsigned char* p = base + band_align(2 * sizeof(uint32_t) * kBandMaxRows);
+  b.sorted = (float2*)p;
+  p += band_align(sizeof(float2) * (size_t)n);
+  b.sidx = (uint32_t*)p;
+  p += band_align(sizeof(uint32_t) * (size_t)n);
+  b.bs_pts = (float2*)p;
+  p += band_align(sizeof(float2) * (size_t)n);
+  b.bs_idx = (uint32_t*)p;
+  return b;
+}
+
+// F_rep (n x 2 floats, original point order) from ctx->pot and Z (ctx->scal[0])
+// for the points of the last spread_band call (same grid)
+int gather_band(fitsne_ctx* ctx, int64_t n, void* frep, cudaStream_t st) {
+  if (!ctx->band_sorted || ctx->band_n != n || !ctx->sortbuf.ptr) {
+    set_error("band gather without a band spread of the same points");
+    return FITSNE_EINVAL;
+  }
+  const BandBufs b = band_bufs((unsigned char*)ctx->sortbuf.ptr, n);
+  const GridArgs g = grid_args(ctx->grid);
+  const int nblk = (int)((n + (int64_t)kBandBlock * kBandRun - 1) / ((int64_t)kBandBlock * kBandRun));
+  k_band_gather<<<nblk, kBandBlock, 0, st>>>(b.bs_pts, b.bs_idx, n, g, (const float*)ctx->pot.ptr,
+                                             (const double*)ctx->scal.ptr, (float2*)frep);
+  FITSNE_CHECK_LAUNCH();
+  return FITSNE_OK;
+}
+
 // the row counters the band spread needs zeroed (the device-grid schedule
 // has k_bbox clear them instead of a memset on the chain)
 uint32_t* band_counters(fitsne_ctx* ctx, int64_t n, int* words) {
-  const size_t off_sorted = (2 * sizeof(uint32_t) * kBandMaxRows + 255) & ~(size_t)255;
-  if (ensure(ctx->sortbuf, off_sorted + sizeof(float2) * (size_t)n) != FITSNE_OK) return nullptr;
+  if (ensure(ctx->sortbuf, band_bytes(n)) != FITSNE_OK) return nullptr;
   *words = 2 * kBandMaxRows;
   return (uint32_t*)ctx->sortbuf.ptr;
 }
@@ -345,18 +445,15 @@ int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
   // gd: the device-computed grid (the host's ctx->grid is not known yet)
   const GridArgs g = gd ? GridArgs{} : grid_args(ctx->grid);
   const int nblk = (int)((n + kBandPts - 1) / kBandPts);
-  // scratch: row totals + row cursors, then the sorted points (16-byte aligned)
-  const size_t off_rows = 0;
-  const size_t off_sorted = (2 * sizeof(uint32_t) * kBandMaxRows + 255) & ~(size_t)255;
-  FITSNE_TRY(ensure(ctx->sortbuf, off_sorted + sizeof(float2) * (size_t)n));
-  unsigned char* base = (unsigned char*)ctx->sortbuf.ptr;
-  uint32_t* rowtot = (uint32_t*)(base + off_rows);
-  uint32_t* rowcur = rowtot + kBandMaxRows;
-  float2* sorted = (float2*)(base + off_sorted);
+  FITSNE_TRY(ensure(ctx->sortbuf, band_bytes(n)));
+  const BandBufs bb = band_bufs((unsigned char*)ctx->sortbuf.ptr, n);
+  uint32_t* rowtot = bb.rowtot;
+  uint32_t* rowcur = bb.rowcur;
+  float2* sorted = bb.sorted;
   if (!gd) FITSNE_CUDA(cudaMemsetAsync(rowtot, 0, 2 * sizeof(uint32_t) * kBandMaxRows, st));
   k_band_rowcount<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, gd);
   FITSNE_CHECK_LAUNCH();
-  k_band_place<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, rowcur, sorted, gd);
+  k_band_place<<<nblk, kBandBlock, 0, st>>>((const float2*)Y, n, g, rowtot, rowcur, sorted, bb.sidx, gd);
   FITSNE_CHECK_LAUNCH();
   const int nred = (int)((n + kBandChunk - 1) / kBandChunk);
   {
@@ -369,8 +466,12 @@ int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
       configured.insert(ctx->device);
     }
   }
-  k_band_reduce<<<nred, kBandBlock, kBandSmem, st>>>(sorted, n, g, (float*)accum, gd);
+  k_band_reduce<<<nred, kBandBlock, kBandSmem, st>>>(sorted, bb.sidx, n, g, (float*)accum, bb.bs_pts,
+                                                     bb.bs_idx, gd);
   FITSNE_CHECK_LAUNCH();
+  // the box-ordered copy is usable by gather_band only with a host-known grid
+  ctx->band_sorted = gd == nullptr;
+  ctx->band_n = n;
   return FITSNE_OK;
 }
 

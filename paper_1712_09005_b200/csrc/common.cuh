@@ -224,6 +224,13 @@ struct fitsne_ctx {
   fitsne::DevBuf part;      // per-block partial sums (double)
   fitsne::DevBuf gen;       // generic scratch
   fitsne::DevBuf sortbuf;   // box sort keys / values / histograms
+  bool band_sorted = false; // sortbuf holds the last band spread's box-ordered points (for gather_band)
+  int64_t band_n = 0;       //   ... of this many points
+  fitsne::DevBuf frep32;    // (N, 2) fp32 F_rep gathered on the repulsion stream
+  int spmv_join = 1;        // a second tiled-SpMV launch behind the repulsion chain joins the dynamic schedule
+  bool spmv_tiled_live = false;  // the evaluation being queued runs the tiled SpMV
+  bool frep_ready = false;  // frep32 holds F_rep of the evaluation being queued
+  int side_gather = 1;      // gather F_rep on the repulsion stream (band spread), stream-combine after the SpMV
   fitsne::DevBuf big;       // four-step FFT planes (bigfft.cu)
   fitsne::DevBuf bigtw;     // its sub-length twiddle tables
   int big_tw_l1 = 0, big_tw_l2 = 0;

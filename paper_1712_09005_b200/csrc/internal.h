@@ -84,6 +84,7 @@ int iterate_fused(fitsne_ctx* ctx, const void* Yin, void* Yout, void* vel, void*
 bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st);
 // F_attr -> *fattr (zeroed buffer owned by the tiled copy; the consumer clears
 // it), KL partials -> (*part)[0, *nparts)
+int attract_tiled_join(fitsne_ctx* ctx, const void* Y, int ctas, cudaStream_t st, int* nparts);
 int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void** fattr,
                   double** part, int* nparts);
 // out = F_attr (mode 0) or 4 (alpha F_attr - frep) (mode 1); clears F_attr
@@ -100,6 +101,7 @@ int join_on_error(fitsne_ctx* ctx, int rc);
 // band spread (bandspread.cu): fp32, 2-D, p = 3, n_int <= 1024
 bool band_spread_applies(const fitsne_ctx* ctx, int64_t n);
 uint32_t* band_counters(fitsne_ctx* ctx, int64_t n, int* words);
+int gather_band(fitsne_ctx* ctx, int64_t n, void* frep, cudaStream_t st);
 int spread_band(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st,
                 const GridArgs* gd = nullptr);
 // The tiled SpMV as kTiledPieces launches over consecutive row ranges (each

@@ -572,6 +572,7 @@ static int ensure_accum(fitsne_ctx* ctx, cudaStream_t st) {
 
 int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st) {
   FITSNE_RANGE("spread");
+  ctx->band_sorted = false;  // set again by the band spread below
   if (!ctx->grid_valid) { set_error("no grid"); return FITSNE_EINVAL; }
   if (ctx->wide) {  // fp64 grid: a caller's accumulator is double (fitsne_grid_accum_dtype)
     const double* y = widen_points(ctx, Y, n, st);

@@ -39,7 +39,9 @@ namespace fitsne {
 // tile's header blob is.  The blob (16-byte aligned, copied into shared memory
 // with the chunk) holds
 //   int32 meta[4] = {row block, slab count, first group, group count}
+//   int32 wlo[32]            first group of consumer warp w's run (cost-balanced cuts)
 //   int32 wstart[32]         slab holding the first group of consumer warp w
+//                            (whole-slab split: warp w owns slabs [wstart[w], wstart[w + 1]))
 //   uint32 goff[nslab + 1]   group offsets of the slabs (padded to 4 entries)
 //   uint16 rows[nslab][32]   tile-local row of each lane (0xFFFF: empty lane)
 // where a "group" is 32 consecutive slots, one per lane.
@@ -53,7 +55,8 @@ struct TileLoad {
 
 __host__ __device__ inline int hdr_goff_words(int nslab) { return (nslab + 1 + 3) & ~3; }
 constexpr int kHdrWstart = 16;                 // int32 wstart[32] after meta
-constexpr int kHdrGoff = kHdrWstart + 128;     // uint32 goff[] after wstart
+constexpr int kHdrWlo = kHdrWstart + 128;      // int32 wlo[32]: first group of consumer warp w's run
+constexpr int kHdrGoff = kHdrWlo + 128;        // uint32 goff[] after wlo
 __host__ __device__ inline int hdr_bytes_for(int nslab) {
   return kHdrGoff + 4 * hdr_goff_words(nslab) + 64 * nslab;
 }
@@ -78,17 +81,60 @@ static constexpr int kTiledConsumers = kTiledThreads / 32 - 1;
 #ifndef FITSNE_TILED_FASTPATH
 #define FITSNE_TILED_FASTPATH 0
 #endif
-// cross-tile pipelining: a consumer warp loads the first batch of its run in
-// the next tile before the tail of the current one (the run bounds follow
-// from the tile's TileLoad, so the header is not needed for it)
-#ifndef FITSNE_TILED_XPF
-#define FITSNE_TILED_XPF 0
-#endif
 // slabs cut by a warp-range boundary: 1 = add into the shared row-block
 // accumulator with a compare-and-swap loop, 0 = vector reduction to global
 #ifndef FITSNE_TILED_SCUT
 #define FITSNE_TILED_SCUT 1
 #endif
+// whole-slab work split: every slab of a tile belongs to one consumer warp
+// (slabs are dealt to the warps longest-first at build time and stored in
+// that order), so no slab is cut by a warp-range boundary, each slab's header
+// words / row points / accumulators are touched once, and every flush is a
+// plain shared-memory read-modify-write.  The rows of a tile are also ordered
+// so that the 16 (2-D) / 32 (1-D) rows of a half-warp / warp fall in distinct
+// shared-memory banks.  0 = equal group ranges per warp (cut slabs).
+#ifndef FITSNE_TILED_WSLAB
+#define FITSNE_TILED_WSLAB 0
+#endif
+// dynamic schedule: the tail of every CTA's static share is cut into small
+// work units drawn from a global counter (0 = static shares only)
+#ifndef FITSNE_TILED_DYN
+#define FITSNE_TILED_DYN 1
+#endif
+// share of a CTA's static run kept as its first (large) unit, in percent
+#ifndef FITSNE_TILED_DYN_HEAD
+#define FITSNE_TILED_DYN_HEAD 70
+#endif
+// small units per mean CTA share (a unit costs about share / this)
+#ifndef FITSNE_TILED_DYN_UNIT
+#define FITSNE_TILED_DYN_UNIT 24
+#endif
+// probe: per-CTA busy time written to the KL partials, printed by fitsne_tiled_stats
+#ifndef FITSNE_TILED_TIMING
+#define FITSNE_TILED_TIMING 0
+#endif
+static constexpr bool kWslab = FITSNE_TILED_WSLAB != 0;
+// rows of a tile ordered so that the lanes of a slab hit distinct shared-memory
+// banks with their row point / accumulator (second sort pass of the build)
+#ifndef FITSNE_TILED_BANKROWS
+#define FITSNE_TILED_BANKROWS 1
+#endif
+static constexpr bool kBankRows = FITSNE_TILED_BANKROWS != 0;
+// Consumer-warp runs inside a tile: cut points balance groups + BETA per slab
+// start (a slab boundary costs about that many groups), and a cut within SNAP
+// groups of a slab boundary moves onto it (the slab is then not shared by two
+// warps).  Tenths of a group; 0 / 0 = equal group counts.
+#ifndef FITSNE_TILED_CUT_BETA
+#define FITSNE_TILED_CUT_BETA 15
+#endif
+#ifndef FITSNE_TILED_CUT_SNAP
+#define FITSNE_TILED_CUT_SNAP 10
+#endif
+#ifndef FITSNE_TILED_WSLAB_BCOST
+#define FITSNE_TILED_WSLAB_BCOST 1
+#endif
+static constexpr int kWslabBoundaryCost = FITSNE_TILED_WSLAB_BCOST;  // slab boundary, in groups
+static constexpr int kKeyTileShift = 32;  // sort key: tile << 32 | (0xFFFF - count) << 16 | rank << 5 | bank
 static constexpr int kTiledU = FITSNE_TILED_U;    // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
 
@@ -110,6 +156,14 @@ __host__ __device__ inline int tiled_run_lo(int ng, int w) {
 
 struct TiledP {
   DevBuf tiles, sched, psched, slab_off, rows, hdr, cols, vals, fattr, part;
+  DevBuf units, counter;  // dynamic schedule: work units (int2 tile ranges) and the ticket counter
+  int nunits = 0;
+  unsigned ticket_base = 0;  // first ticket of the next launch
+  // the pass in flight (attract_tiled), for the joining launch (attract_tiled_join)
+  unsigned cur_base = 0;
+  bool cur_kl = false, cur_dynamic = false;
+  int join_grid = 0;         // CTAs of the last joining launch (0: none)
+  cudaEvent_t ev_perm = nullptr;  // relabelled Y copy ready
   // locality relabelling (reorder.cu): tiles are built over P[order][:, order];
   // order[new] = old.  The kernel reads Y through yp = Y[order] and adds each
   // row's force at its original index.
@@ -164,8 +218,9 @@ static int alloc_exact(DevBuf& b, size_t bytes) {
 void free_tiled(fitsne_ctx* ctx) {
   if (!ctx->tiled) return;
   TiledP* t = ctx->tiled;
+  if (t->ev_perm) cudaEventDestroy(t->ev_perm);
   DevBuf* bufs[] = {&t->tiles, &t->sched, &t->psched, &t->slab_off, &t->rows, &t->hdr, &t->cols,
-                    &t->vals, &t->fattr, &t->part, &t->order, &t->yp};
+                    &t->vals, &t->fattr, &t->part, &t->order, &t->yp, &t->units, &t->counter};
   for (DevBuf* b : bufs) release_buf(*b);
   delete t;
   ctx->tiled = nullptr;
@@ -226,7 +281,7 @@ __global__ void k_seg_emit(const int64_t* __restrict__ rowptr, const int32_t* __
       const int64_t s = base + __popc(m & ((1u << lane) - 1u));
       seg_begin[s] = k;
       seg_row[s] = (int32_t)r;
-      key[s] = (uint64_t)(tile_row + ch) << 16;  // count filled in by k_seg_finish
+      key[s] = (uint64_t)(tile_row + ch) << kKeyTileShift;  // count filled in by k_seg_finish
     }
     base += __popc(m);
   }
@@ -234,32 +289,52 @@ __global__ void k_seg_emit(const int64_t* __restrict__ rowptr, const int32_t* __
 
 __global__ void k_seg_finish(const int64_t* __restrict__ rowptr, const int64_t* __restrict__ segstart,
                              const int64_t* __restrict__ seg_begin, const int32_t* __restrict__ seg_row,
-                             int64_t nseg, uint64_t* __restrict__ key, uint32_t* __restrict__ idx,
-                             int32_t* __restrict__ seg_cnt) {
+                             int64_t nseg, int R, int bank_mask, uint64_t* __restrict__ key,
+                             uint32_t* __restrict__ idx, int32_t* __restrict__ seg_cnt) {
   const int64_t s = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (s >= nseg) return;
   const int32_t r = seg_row[s];
   const int64_t end = (s + 1 < segstart[r + 1]) ? seg_begin[s + 1] : rowptr[r + 1];
   const int32_t c = (int32_t)(end - seg_begin[s]);
   seg_cnt[s] = c;
-  // larger counts first inside a tile (sliced-ELL sorting window = the tile)
-  key[s] |= (uint64_t)(0xFFFF - c);
+  // larger counts first inside a tile (sliced-ELL sorting window = the tile);
+  // then the shared-memory bank of the row's point / accumulator
+  key[s] |= ((uint64_t)(0xFFFF - c) << 16) | (uint64_t)((r % R) & bank_mask);
   idx[s] = (uint32_t)s;
 }
+
+// Second sort key.  After the first sort the segments of one (tile, count,
+// bank) class are contiguous; rank = position inside the class.  Sorting by
+// (tile, count, rank, bank) deals a class's banks round-robin, so consecutive
+// rows -- the lanes of a slab -- fall in distinct banks.
+__global__ void k_run_heads(const uint64_t* __restrict__ key, int64_t nseg, int64_t* __restrict__ head) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  head[q] = (q == 0 || key[q] != key[q - 1]) ? q : 0;
+}
+__global__ void k_rank_key(uint64_t* __restrict__ key, const int64_t* __restrict__ head, int64_t nseg) {
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (q >= nseg) return;
+  const int64_t rank = q - head[q];
+  key[q] |= (uint64_t)(rank < 2047 ? rank : 2047) << 5;
+}
+struct MaxI64 {
+  __host__ __device__ int64_t operator()(int64_t a, int64_t b) const { return a > b ? a : b; }
+};
 
 __global__ void k_tile_bounds(const uint64_t* __restrict__ key, int64_t nseg,
                               int32_t* __restrict__ tfirst, int32_t* __restrict__ tcount) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nseg) return;
-  const uint64_t t = key[q] >> 16;
-  if (q == 0 || (key[q - 1] >> 16) != t) {
+  const uint64_t t = key[q] >> kKeyTileShift;
+  if (q == 0 || (key[q - 1] >> kKeyTileShift) != t) {
     int64_t e = q + 1;
     // count: find the end of this tile's run (runs are short relative to nseg;
     // binary search over the sorted keys)
     int64_t lo = q, hi = nseg;  // first index with tile > t
     while (lo < hi) {
       const int64_t mid = (lo + hi) >> 1;
-      if ((key[mid] >> 16) > t) hi = mid; else lo = mid + 1;
+      if ((key[mid] >> kKeyTileShift) > t) hi = mid; else lo = mid + 1;
     }
     e = lo;
     tfirst[t] = (int32_t)q;
@@ -283,7 +358,8 @@ __global__ void k_slab_kmax(const int32_t* __restrict__ tfirst, const int32_t* _
 
 __global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __restrict__ sidx,
                             int64_t nseg, const int32_t* __restrict__ tfirst,
-                            const int32_t* __restrict__ slab_begin, const uint32_t* __restrict__ slab_off,
+                            const int32_t* __restrict__ slab_begin, const int32_t* __restrict__ slab_pos,
+                            const uint32_t* __restrict__ slab_off,
                             const int64_t* __restrict__ seg_begin, const int32_t* __restrict__ seg_row,
                             const int32_t* __restrict__ seg_cnt, const int32_t* __restrict__ col,
                             const float* __restrict__ val, int nch, int R, int C,
@@ -291,9 +367,10 @@ __global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __
                             float* __restrict__ vals) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (q >= nseg) return;
-  const int64_t t = (int64_t)(key[q] >> 16);
+  const int64_t t = (int64_t)(key[q] >> kKeyTileShift);
   const int64_t rel = q - tfirst[t];
-  const int64_t slab = slab_begin[t] + rel / 32;
+  // slab_pos: the slab's place in the tile's stored order (whole-slab split)
+  const int64_t slab = slab_begin[t] + (slab_pos ? slab_pos[slab_begin[t] + rel / 32] : rel / 32);
   const int lane = (int)(rel & 31);
   const uint32_t s = sidx[q];
   const int32_t r = seg_row[s];
@@ -464,7 +541,8 @@ static size_t bankorder_long_smem() {
 __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_t* __restrict__ t_sb,
                                const int32_t* __restrict__ t_ns, const int64_t* __restrict__ t_hoff,
                                int64_t ntiles, int nch, const uint32_t* __restrict__ slab_off,
-                               const uint16_t* __restrict__ rows, unsigned char* __restrict__ hdr) {
+                               const uint16_t* __restrict__ rows, const int32_t* __restrict__ t_wfirst,
+                               unsigned char* __restrict__ hdr) {
   const int lane = threadIdx.x & 31;
   const int64_t t = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   if (t >= ntiles) return;
@@ -482,15 +560,38 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
     meta[2] = (int32_t)g0;
     meta[3] = (int32_t)ng;
   }
-  {
-    // consumer warp `lane` starts at group ng * lane / kTiledConsumers: the
-    // last slab whose offset is <= that group
-    const uint32_t lo = (uint32_t)tiled_run_lo((int)ng, lane);  // as the kernel
-    int a = 0, z = ns;
-    while (z - a > 1) {
-      const int m = (a + z) >> 1;
-      if (slab_off[sb + m] - g0 <= lo) a = m; else z = m;
+  int32_t* wlo = reinterpret_cast<int32_t*>(h + kHdrWlo);
+  if (t_wfirst) {
+    // whole-slab split: warp `lane` owns the stored slabs [wstart[lane], wstart[lane + 1])
+    wstart[lane] = t_wfirst[t * 32 + lane];
+    wlo[lane] = (int32_t)(slab_off[sb + wstart[lane]] - g0);
+  } else {
+    // consumer warp `lane` starts where the cumulative cost (groups + beta per
+    // slab start) reaches lane / kTiledConsumers of the tile's
+    const float beta = FITSNE_TILED_CUT_BETA * 0.1f, snap = FITSNE_TILED_CUT_SNAP * 0.1f;
+    auto cum = [&](int j) { return (float)(slab_off[sb + j] - g0) + beta * (float)j; };  // cost before slab j
+    uint32_t lo;
+    int a = 0;
+    if (lane >= kTiledConsumers) {
+      lo = ng;
+      a = ns - 1;
+    } else {
+      const float target = cum(ns) * (float)lane / (float)kTiledConsumers;
+      int z = ns;
+      while (z - a > 1) {  // last slab whose start cost is <= target
+        const int m = (a + z) >> 1;
+        if (cum(m) <= target) a = m; else z = m;
+      }
+      const uint32_t s0 = slab_off[sb + a] - g0, s1 = slab_off[sb + a + 1] - g0;
+      float into = target - cum(a) - beta;  // groups of slab a before the cut
+      if (into < snap) into = 0.f;                          // onto the slab's start
+      if ((float)(s1 - s0) - into < snap) into = (float)(s1 - s0);  // onto its end
+      lo = s0 + (uint32_t)(into + 0.5f);
+      if (lo > s1) lo = s1;
+      if (lo == s1 && a + 1 < ns) a = a + 1;  // the run starts with the next slab
+      if (lane == 0) { lo = 0; a = 0; }
     }
+    wlo[lane] = (int32_t)lo;
     wstart[lane] = a;
   }
   for (int j = lane; j < hdr_goff_words(ns); j += 32) goff[j] = j <= ns ? slab_off[sb + j] - g0 : 0u;
@@ -750,17 +851,42 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   k_seg_emit<<<nb(n_rows * 32, 256), 256, 0, st>>>(rowptr, col, n_rows, C, (int)nch, R,
                                                    segstart, seg_begin, seg_row, key);
   FITSNE_CHECK_LAUNCH();
-  k_seg_finish<<<nb(nseg, 256), 256, 0, st>>>(rowptr, segstart, seg_begin, seg_row, nseg, key,
+  // bank of a row's point / accumulator in shared memory: 8-byte float2 (2-D)
+  // conflicts inside a half-warp on row mod 16, 4-byte float (1-D) on row mod 32
+  const int bank_mask = kBankRows ? (ctx->dims == 1 ? 31 : 15) : 0;
+  k_seg_finish<<<nb(nseg, 256), 256, 0, st>>>(rowptr, segstart, seg_begin, seg_row, nseg, R, bank_mask, key,
                                               idx, seg_cnt);
   FITSNE_CHECK_LAUNCH();
-  int end_bit = 16;
-  while ((1LL << (end_bit - 16)) < ntd) ++end_bit;
-  {
+  int end_bit = kKeyTileShift;
+  while ((1LL << (end_bit - kKeyTileShift)) < ntd) ++end_bit;
+  auto sort_pairs = [&](uint64_t* kin, uint64_t* kout, uint32_t* vin, uint32_t* vout) -> int {
     size_t bytes = 0;
-    FITSNE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, key, key2, idx, idx2, nseg, 0, end_bit, st));
+    FITSNE_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, kin, kout, vin, vout, nseg, 0, end_bit, st));
     unsigned char* tb;
     FITSNE_TRY(tmp.alloc(&tb, bytes));
-    FITSNE_CUDA(cub::DeviceRadixSort::SortPairs(tb, bytes, key, key2, idx, idx2, nseg, 0, end_bit, st));
+    FITSNE_CUDA(cub::DeviceRadixSort::SortPairs(tb, bytes, kin, kout, vin, vout, nseg, 0, end_bit, st));
+    return FITSNE_OK;
+  };
+  FITSNE_TRY(sort_pairs(key, key2, idx, idx2));
+  if (kBankRows) {
+    // second pass: (tile, count, rank inside the (tile, count, bank) class, bank)
+    int64_t *head, *hpos;
+    FITSNE_TRY(tmp.alloc(&head, nseg));
+    FITSNE_TRY(tmp.alloc(&hpos, nseg));
+    k_run_heads<<<nb(nseg, 256), 256, 0, st>>>(key2, nseg, head);
+    FITSNE_CHECK_LAUNCH();
+    {
+      size_t bytes = 0;
+      FITSNE_CUDA(cub::DeviceScan::InclusiveScan(nullptr, bytes, head, hpos, MaxI64(), nseg, st));
+      unsigned char* tb;
+      FITSNE_TRY(tmp.alloc(&tb, bytes));
+      FITSNE_CUDA(cub::DeviceScan::InclusiveScan(tb, bytes, head, hpos, MaxI64(), nseg, st));
+    }
+    k_rank_key<<<nb(nseg, 256), 256, 0, st>>>(key2, hpos, nseg);
+    FITSNE_CHECK_LAUNCH();
+    FITSNE_TRY(sort_pairs(key2, key, idx2, idx));
+    std::swap(key, key2);   // key2 / idx2: the final order, as below
+    std::swap(idx, idx2);
   }
   int32_t *tfirst, *tcount, *nslab, *slab_begin;
   FITSNE_TRY(tmp.alloc(&tfirst, ntd));
@@ -784,6 +910,58 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   FITSNE_CUDA(cudaMemsetAsync(kmax, 0, sizeof(uint32_t) * ((size_t)nslabs + 1), st));
   k_slab_kmax<<<nb(ntd, 256), 256, 0, st>>>(tfirst, nslab, slab_begin, idx2, seg_cnt, ntd, kmax);
   FITSNE_CHECK_LAUNCH();
+  std::vector<int32_t> h_nslab(ntd), h_sb(ntd);
+  FITSNE_CUDA(cudaMemcpyAsync(h_nslab.data(), nslab, sizeof(int32_t) * ntd, cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaMemcpyAsync(h_sb.data(), slab_begin, sizeof(int32_t) * ntd, cudaMemcpyDeviceToHost, st));
+  // Whole-slab split (host): deal each tile's slabs, longest first, to the
+  // consumer warp with the least work so far (a slab costs its groups plus a
+  // fixed boundary term); store the slabs warp by warp.  slab_pos[j] = stored
+  // position of the tile's j-th slab of the sorted order, wfirst[w] = first
+  // stored slab of warp w.
+  int32_t* slab_pos = nullptr;
+  std::vector<int32_t> h_wfirst;  // per dense tile with slabs: 32 entries, filled below
+  std::vector<int64_t> wf_of(kWslab ? ntd : 0, -1);
+  if (kWslab) {
+    std::vector<uint32_t> h_kmax((size_t)nslabs + 1), h_kperm((size_t)nslabs + 1, 0u);
+    std::vector<int32_t> h_pos((size_t)nslabs);
+    FITSNE_CUDA(cudaMemcpyAsync(h_kmax.data(), kmax, sizeof(uint32_t) * ((size_t)nslabs + 1),
+                                cudaMemcpyDeviceToHost, st));
+    FITSNE_CUDA(cudaStreamSynchronize(st));
+    std::vector<int> owner;
+    for (int64_t t = 0; t < ntd; ++t) {
+      const int ns = h_nslab[t];
+      if (ns == 0) continue;
+      const int64_t sb = h_sb[t];
+      owner.assign(ns, 0);
+      int64_t load[32] = {};
+      int cnt[32] = {};
+      for (int j = 0; j < ns; ++j) {  // sorted order: longest slabs first
+        int best = 0;
+        for (int w = 1; w < kTiledConsumers; ++w)
+          if (load[w] < load[best]) best = w;
+        owner[j] = best;
+        load[best] += (int64_t)h_kmax[sb + j] + kWslabBoundaryCost;
+        ++cnt[best];
+      }
+      wf_of[t] = (int64_t)h_wfirst.size();
+      int first[33];
+      first[0] = 0;
+      for (int w = 0; w < 32; ++w) first[w + 1] = first[w] + (w < kTiledConsumers ? cnt[w] : 0);
+      for (int w = 0; w < 32; ++w) h_wfirst.push_back(first[w]);
+      int at[32];
+      for (int w = 0; w < 32; ++w) at[w] = first[w];
+      for (int j = 0; j < ns; ++j) {
+        const int p = at[owner[j]]++;
+        h_pos[sb + j] = p;
+        h_kperm[sb + p] = h_kmax[sb + j];
+      }
+    }
+    FITSNE_TRY(tmp.alloc(&slab_pos, (size_t)nslabs));
+    FITSNE_CUDA(cudaMemcpyAsync(slab_pos, h_pos.data(), sizeof(int32_t) * (size_t)nslabs, cudaMemcpyHostToDevice, st));
+    FITSNE_CUDA(cudaMemcpyAsync(kmax, h_kperm.data(), sizeof(uint32_t) * ((size_t)nslabs + 1),
+                                cudaMemcpyHostToDevice, st));
+    FITSNE_CUDA(cudaStreamSynchronize(st));  // the host vectors go out of scope
+  }
   FITSNE_TRY(alloc_exact(T->slab_off, sizeof(uint32_t) * ((size_t)nslabs + 1)));
   uint32_t* slab_off = (uint32_t*)T->slab_off.ptr;
   FITSNE_TRY(excl_scan(tmp, kmax, slab_off, (int64_t)nslabs + 1, st));
@@ -800,7 +978,7 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   FITSNE_CUDA(cudaMemsetAsync(T->rows.ptr, 0xFF, sizeof(uint16_t) * (size_t)nslabs * 32, st));
   FITSNE_CUDA(cudaMemsetAsync(T->cols.ptr, 0, sizeof(uint16_t) * (size_t)(nslots + kTiledPad), st));
   FITSNE_CUDA(cudaMemsetAsync(T->vals.ptr, 0, sizeof(float) * (size_t)(nslots + kTiledPad), st));
-  k_tile_fill<<<nb(nseg, 256), 256, 0, st>>>(key2, idx2, nseg, tfirst, slab_begin, slab_off, seg_begin,
+  k_tile_fill<<<nb(nseg, 256), 256, 0, st>>>(key2, idx2, nseg, tfirst, slab_begin, slab_pos, slab_off, seg_begin,
                                              seg_row, seg_cnt, col, val,
                                              (int)nch, R, C, (uint16_t*)T->rows.ptr,
                                              (uint16_t*)T->cols.ptr, (float*)T->vals.ptr);
@@ -820,10 +998,7 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   }
 
   // host: compact tile list, header blobs, static schedule balanced on cost
-  std::vector<int32_t> h_nslab(ntd), h_sb(ntd);
   std::vector<uint32_t> h_off((size_t)nslabs + 1);
-  FITSNE_CUDA(cudaMemcpyAsync(h_nslab.data(), nslab, sizeof(int32_t) * ntd, cudaMemcpyDeviceToHost, st));
-  FITSNE_CUDA(cudaMemcpyAsync(h_sb.data(), slab_begin, sizeof(int32_t) * ntd, cudaMemcpyDeviceToHost, st));
   FITSNE_CUDA(cudaMemcpyAsync(h_off.data(), slab_off, sizeof(uint32_t) * ((size_t)nslabs + 1),
                               cudaMemcpyDeviceToHost, st));
   FITSNE_CUDA(cudaStreamSynchronize(st));
@@ -861,8 +1036,16 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   const int64_t nt = (int64_t)tiles.size();
   FITSNE_TRY(alloc_exact(T->hdr, (size_t)std::max<int64_t>(hoff, 16)));
   {
-    int32_t *d_dense, *d_sb, *d_ns;
+    int32_t *d_dense, *d_sb, *d_ns, *d_wfirst = nullptr;
     int64_t* d_hoff;
+    if (kWslab) {
+      std::vector<int32_t> wf((size_t)nt * 32);
+      for (int64_t i = 0; i < nt; ++i)
+        std::memcpy(wf.data() + (size_t)i * 32, h_wfirst.data() + wf_of[t_dense[i]], 32 * sizeof(int32_t));
+      FITSNE_TRY(tmp.alloc(&d_wfirst, (size_t)nt * 32));
+      FITSNE_CUDA(cudaMemcpyAsync(d_wfirst, wf.data(), sizeof(int32_t) * (size_t)nt * 32, cudaMemcpyHostToDevice, st));
+      FITSNE_CUDA(cudaStreamSynchronize(st));
+    }
     FITSNE_TRY(tmp.alloc(&d_dense, nt));
     FITSNE_TRY(tmp.alloc(&d_sb, nt));
     FITSNE_TRY(tmp.alloc(&d_ns, nt));
@@ -872,7 +1055,7 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
     FITSNE_CUDA(cudaMemcpyAsync(d_ns, t_ns.data(), sizeof(int32_t) * nt, cudaMemcpyHostToDevice, st));
     FITSNE_CUDA(cudaMemcpyAsync(d_hoff, t_hoff.data(), sizeof(int64_t) * nt, cudaMemcpyHostToDevice, st));
     k_tile_headers<<<nb(nt * 32, 256), 256, 0, st>>>(d_dense, d_sb, d_ns, d_hoff, nt, (int)nch, slab_off,
-                                                    (const uint16_t*)T->rows.ptr,
+                                                    (const uint16_t*)T->rows.ptr, d_wfirst,
                                                     (unsigned char*)T->hdr.ptr);
     FITSNE_CHECK_LAUNCH();
     FITSNE_CUDA(cudaStreamSynchronize(st));
@@ -894,6 +1077,44 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   };
   std::vector<int32_t> sched(grid + 1), psched((size_t)kTiledPieces * (grid + 1));
   balance(0, nt, sched.data());
+  // dynamic schedule: unit b < grid = the head of CTA b's static share
+  // (FITSNE_TILED_DYN_HEAD percent of its cost), then every share's tail in
+  // units of FITSNE_TILED_DYN_UNIT tiles, in tile order
+  std::vector<int2> units;
+  if (FITSNE_TILED_DYN) {
+    std::vector<int32_t> cut(grid);
+    for (int b = 0; b < grid; ++b) {
+      double total = 0, acc = 0;
+      for (int64_t t = sched[b]; t < sched[b + 1]; ++t) total += cost[t];
+      int64_t t = sched[b];
+      for (; t < sched[b + 1]; ++t) {
+        if (acc + cost[t] > total * (FITSNE_TILED_DYN_HEAD / 100.0)) break;
+        acc += cost[t];
+      }
+      cut[b] = (int32_t)t;
+      units.push_back(make_int2(sched[b], cut[b]));
+    }
+    // tails: units of about 1 / FITSNE_TILED_DYN_UNIT of a CTA's mean share
+    // (by cost; a tile is never split, so the heavy diagonal tiles make large
+    // units), drawn largest first so the small ones level the finish
+    double total = 0;
+    for (int64_t t = 0; t < nt; ++t) total += cost[t];
+    const double target = total / grid / FITSNE_TILED_DYN_UNIT;
+    std::vector<std::pair<double, int2>> tail;
+    for (int b = 0; b < grid; ++b) {
+      int32_t t = cut[b];
+      while (t < sched[b + 1]) {
+        double acc = 0;
+        int32_t e = t;
+        do { acc += cost[e]; ++e; } while (e < sched[b + 1] && acc + 0.5 * cost[e] <= target);
+        tail.push_back({acc, make_int2(t, e)});
+        t = e;
+      }
+    }
+    std::stable_sort(tail.begin(), tail.end(),
+                     [](const std::pair<double, int2>& a, const std::pair<double, int2>& b) { return a.first > b.first; });
+    for (const auto& u : tail) units.push_back(u.second);
+  }
   // piece schedules: row blocks split in kTiledPieces near-equal-cost ranges
   {
     const int64_t nrb = (n_rows + R - 1) / R;
@@ -928,7 +1149,15 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
                               cudaMemcpyHostToDevice, st));
   FITSNE_TRY(alloc_exact(T->fattr, sizeof(float) * 2 * (size_t)std::max<int64_t>(n_rows, 1)));
   FITSNE_CUDA(cudaMemsetAsync(T->fattr.ptr, 0, sizeof(float) * 2 * (size_t)n_rows, st));
-  FITSNE_TRY(alloc_exact(T->part, sizeof(double) * (grid + 1)));
+  FITSNE_TRY(alloc_exact(T->part, sizeof(double) * (grid + ctx->num_sms + 1)));  // + a joining launch
+  T->nunits = (int)units.size();
+  T->ticket_base = 0;
+  if (!units.empty()) {
+    FITSNE_TRY(alloc_exact(T->units, sizeof(int2) * units.size()));
+    FITSNE_TRY(alloc_exact(T->counter, sizeof(unsigned)));
+    FITSNE_CUDA(cudaMemcpyAsync(T->units.ptr, units.data(), sizeof(int2) * units.size(), cudaMemcpyHostToDevice, st));
+    FITSNE_CUDA(cudaMemsetAsync(T->counter.ptr, 0, sizeof(unsigned), st));
+  }
   FITSNE_CUDA(cudaStreamSynchronize(st));  // host vectors and temporaries go out of scope
   release_buf(T->rows);      // folded into the header blobs
   release_buf(T->slab_off);
@@ -991,7 +1220,7 @@ bool tiled_usable(fitsne_ctx* ctx, const void* Y, cudaStream_t st) {
     cudaStreamSynchronize(st);
     cudaGetLastError();
     DevBuf* bufs[] = {&T->tiles, &T->sched, &T->psched, &T->slab_off, &T->rows, &T->hdr, &T->cols,
-                      &T->vals, &T->fattr, &T->part, &T->order, &T->yp};
+                      &T->vals, &T->fattr, &T->part, &T->order, &T->yp, &T->units, &T->counter};
     for (DevBuf* b : bufs) release_buf(*b);
     T->failed = true;
     return false;
@@ -1137,7 +1366,13 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
                 const float* __restrict__ vals, const typename TPt<S>::T* __restrict__ Y, int64_t row_begin,
                 int64_t n_rows, int64_t n_total, int R, int C, int stage_sz,
                 typename TPt<S>::T* __restrict__ fattr, double* __restrict__ klpart,
-                const int* __restrict__ rowmap) {
+                const int* __restrict__ rowmap, const int2* __restrict__ units, int nunits,
+                unsigned* __restrict__ counter, unsigned base) {
+  // units != null: dynamic schedule.  The producer draws work units (tile
+  // ranges [x, y)) from a global counter: the first `grid` units are the large
+  // heads of the static shares, the rest their tails cut into small units, so
+  // CTAs that finish early take over the tails of slow ones.  The counter is
+  // never reset: launch k draws tickets base .. base + nunits + grid - 1.
   using PT = typename TPt<S>::T;
   using Tr = TPt<S>;
   // rowmap (relabelled P): the output index of tile row r is rowmap[r]
@@ -1148,8 +1383,12 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   unsigned char* ring = smem_raw + ((3 * (size_t)R * sizeof(PT) + 15) & ~(size_t)15);
   __shared__ __align__(8) uint64_t full[kTiledStages], empty[kTiledStages];
   __shared__ double red[kTiledConsumers];
+  __shared__ int live[kTiledStages];  // 1: the stage holds a tile, 0: end of this CTA's work
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int t0 = sched[blockIdx.x], t1 = sched[blockIdx.x + 1];
+#if FITSNE_TILED_TIMING
+  unsigned long long t_begin = 0;
+  if (tid == 0) asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_begin));
+#endif
   if (tid == 0) {
     for (int b = 0; b < kTiledStages; ++b) {
       mbar_init(&full[b], 1);
@@ -1163,8 +1402,9 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
     // ---------------- producer ----------------
     if (lane == 0) {
       const uint64_t pol_y = policy_evict_last();
-      for (int t = t0; t < t1; ++t) {
-        const int it = t - t0, b = it % kTiledStages;
+      int it = 0;
+      auto stage_tile = [&](int t) {
+        const int b = it % kTiledStages;
         if (it >= kTiledStages) mbar_wait(&empty[b], (uint32_t)(((it / kTiledStages) - 1) & 1));
         const TileLoad d = tiles[t];
         unsigned char* st = ring + (size_t)b * stage_sz;
@@ -1175,9 +1415,11 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         constexpr int64_t kAl = 16 / (int64_t)sizeof(PT);  // points per 16 bytes
         const int64_t cbulk = cnt / kAl * kAl;
         const uint32_t cbytes = (uint32_t)cbulk * (uint32_t)sizeof(PT);
-        // tail points (bulk copies move multiples of 16 bytes): plain stores,
-        // published to the consumers by the release of the arrive below
+        // tail points (bulk copies move multiples of 16 bytes) and the live
+        // flag: plain stores, published to the consumers by the release of
+        // the arrive below
         for (int64_t k = cbulk; k < cnt; ++k) cdst[k] = Y[c0 + k];
+        live[b] = 1;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive_tx(&full[b], cbytes + (uint32_t)d.hdr_bytes);
         if (cbytes) bulk_g2s_hint(cdst, Y + c0, cbytes, &full[b], pol_y);
@@ -1194,6 +1436,25 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
           for (uint32_t o = 0; o < vb; o += 65536u) bulk_prefetch_l2(vbeg + o, min(65536u, vb - o));
         }
 #endif
+        ++it;
+      };
+      if (units) {
+        for (;;) {
+          const unsigned u = atomicAdd(counter, 1u) - base;
+          if (u >= (unsigned)nunits) break;
+          const int2 r = units[u];
+          for (int t = r.x; t < r.y; ++t) stage_tile(t);
+        }
+      } else {
+        const int t0 = sched[blockIdx.x], t1 = sched[blockIdx.x + 1];
+        for (int t = t0; t < t1; ++t) stage_tile(t);
+      }
+      // end marker: one more stage with live = 0
+      {
+        const int b = it % kTiledStages;
+        if (it >= kTiledStages) mbar_wait(&empty[b], (uint32_t)(((it / kTiledStages) - 1) & 1));
+        live[b] = 0;
+        mbar_arrive(&full[b]);
       }
     }
     return;
@@ -1220,27 +1481,13 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   };
   unsigned short cA[kTiledU], cB[kTiledU];
   float pA[kTiledU], pB[kTiledU];
-#if FITSNE_TILED_XPF
-  // cB / pB: the first batch of this warp's run in the next tile
-  auto load_first = [&](int t) {
-    const TileLoad& d = tiles[t];
-    const int64_t gs = (int64_t)(uint32_t)d.g0 + tiled_run_lo(d.ng, warp);
-    const uint16_t* c = cols + (size_t)slot_index(gs, lane);
-    const float* v = vals + (size_t)slot_index(gs, lane);
-#pragma unroll
-    for (int u = 0; u < kTiledU; ++u) {
-      cB[u] = __ldcs(reinterpret_cast<const unsigned short*>(c) + u * 32);
-      pB[u] = __ldcs(v + u * 32);
-    }
-  };
-  if (t0 < t1) load_first(t0);
-#endif
-  for (int t = t0; t < t1; ++t) {
-    const int it = t - t0, b = it % kTiledStages;
+  for (int it = 0;; ++it) {
+    const int b = it % kTiledStages;
     const unsigned char* st = ring + (size_t)b * stage_sz;
     const PT* cb = reinterpret_cast<const PT*>(st);
     const unsigned char* h = st + (size_t)C * sizeof(PT);
     mbar_wait(&full[b], (uint32_t)((it / kTiledStages) & 1));
+    if (!live[b]) break;
     const int32_t* meta = reinterpret_cast<const int32_t*>(h);
     const int rb = meta[0], ns = meta[1];
     FITSNE_DCHECK(rb >= 0 && (int64_t)rb * R < n_rows && ns >= 1 && ns <= (R + 31) / 32 + 1 &&
@@ -1263,17 +1510,25 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       consumer_sync();
     }
     PT* accp = acc + (size_t)(it & 1) * R;
-    const int lo = tiled_run_lo(ng, warp);
-    const int hi = tiled_run_lo(ng, warp + 1);
-#if FITSNE_TILED_XPF
-#pragma unroll
-    for (int u = 0; u < kTiledU; ++u) { cA[u] = cB[u]; pA[u] = pB[u]; }
-    if (lo >= hi && t + 1 < t1) load_first(t + 1);
+#if FITSNE_TILED_WSLAB
+    // this warp's slabs [ws0, ws1) and their groups [lo, hi)
+    const int ws0 = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
+    const int ws1 = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp + 1];
+    const int lo = (int)goff[ws0], hi = (int)goff[ws1];
+#else
+    const int lo = reinterpret_cast<const int32_t*>(h + kHdrWlo)[warp];
+    const int hi = reinterpret_cast<const int32_t*>(h + kHdrWlo)[warp + 1];
 #endif
     if (lo < hi) {
+#if FITSNE_TILED_WSLAB
+      int s = ws0;
+      int s_end = (int)goff[s + 1];
+      constexpr bool shared_slab = false;  // every slab belongs to one warp
+#else
       int s = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
       int s_end = (int)goff[s + 1];
       bool shared_slab = (int)goff[s] < lo || s_end > hi;
+#endif
       int row = hrows[s * 32 + lane];
       PT yi = row != 0xFFFF ? ys[row] : Tr::zero();
       float ax = 0.f, ay = 0.f;
@@ -1304,7 +1559,9 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         ax = ay = 0.f;
         ++s;
         s_end = (int)goff[s + 1];
+#if !FITSNE_TILED_WSLAB
         shared_slab = s_end > hi;
+#endif
         row = hrows[s * 32 + lane];
         yi = row != 0xFFFF ? ys[row] : Tr::zero();
         out_row();
@@ -1321,13 +1578,11 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       };
       const uint16_t* cp = cols + (size_t)slot_index(g0 + lo, lane);
       const float* vp = vals + (size_t)slot_index(g0 + lo, lane);
-#if !FITSNE_TILED_XPF
 #pragma unroll
       for (int u = 0; u < kTiledU; ++u) {
         cA[u] = __ldcs(reinterpret_cast<const unsigned short*>(cp) + u * 32);
         pA[u] = __ldcs(vp + u * 32);
       }
-#endif
 #if FITSNE_TILED_DEPTH >= 3
       // two batches in flight: B holds the next batch, C is loaded ahead of it
       unsigned short cC[kTiledU];
@@ -1395,9 +1650,6 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         cp += kTiledU * 32;
         vp += kTiledU * 32;
       }
-#if FITSNE_TILED_XPF
-      if (t + 1 < t1) load_first(t + 1);
-#endif
 #pragma unroll
       for (int u = 0; u < kTiledU - 1; ++u)
         if (g + u < hi) step(g + u, cA[u], pA[u]);
@@ -1409,6 +1661,14 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   }
   consumer_sync();
   if (cur_rb >= 0) flush_block();
+#if FITSNE_TILED_TIMING
+  // probe build: the CTA's busy time (ns) in the (otherwise unused) KL partial
+  if (!KL && tid == 0) {
+    unsigned long long t_end;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t_end));
+    klpart[blockIdx.x] = (double)(t_end - t_begin);
+  }
+#endif
   if (KL) {
     kld = warp_sum(kld);
     if (lane == 0) red[warp] = kld;
@@ -1443,7 +1703,10 @@ __global__ void k_permute_points(const PT* __restrict__ Y, const int* __restrict
 // Runs the tiled SpMV: F_attr accumulates into the tiled copy's zeroed buffer
 // (*fattr_out; the consumer must clear it), KL partials -> T->part[0, grid).
 template <int S>
-static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched, cudaStream_t st) {
+static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched, cudaStream_t st,
+                          int join_ctas) {
+  // join_ctas > 0: a second launch that only draws work units of the pass in
+  // flight (same ticket base), for SMs that become free while it runs
   using PT = typename TPt<S>::T;
   TiledP* T = ctx->tiled;
   const size_t smem = tiled_smem(T->R, T->C, T->hdr_max, sizeof(PT));
@@ -1463,33 +1726,58 @@ static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t
       have = smem;
     }
   }
-  double* part = (double*)T->part.ptr;
+  double* part = (double*)T->part.ptr + (join_ctas > 0 ? T->grid : 0);
   const int* rowmap = nullptr;
   if (T->relabeled) {
     // the tiles index the relabelled points: stage Y in that order
-    k_permute_points<PT><<<nb(ctx->n_total, 256), 256, 0, st>>>((const PT*)Y, (const int*)T->order.ptr,
-                                                                ctx->n_total, (PT*)T->yp.ptr);
-    FITSNE_CHECK_LAUNCH();
+    if (!T->ev_perm) FITSNE_CUDA(cudaEventCreateWithFlags(&T->ev_perm, cudaEventDisableTiming));
+    if (join_ctas > 0) {
+      FITSNE_CUDA(cudaStreamWaitEvent(st, T->ev_perm, 0));
+    } else {
+      k_permute_points<PT><<<nb(ctx->n_total, 256), 256, 0, st>>>((const PT*)Y, (const int*)T->order.ptr,
+                                                                  ctx->n_total, (PT*)T->yp.ptr);
+      FITSNE_CHECK_LAUNCH();
+      FITSNE_CUDA(cudaEventRecord(T->ev_perm, st));
+    }
     Y = T->yp.ptr;
     rowmap = (const int*)T->order.ptr;
   }
 #define TILED_ARGS                                                                                  \
   (const TileLoad*)T->tiles.ptr, sched, (const unsigned char*)T->hdr.ptr,                          \
       (const uint16_t*)T->cols.ptr, (const float*)T->vals.ptr, (const PT*)Y, ctx->row_begin,        \
-      ctx->n_rows, ctx->n_total, T->R, T->C, stage_sz, (PT*)T->fattr.ptr, part, rowmap
+      ctx->n_rows, ctx->n_total, T->R, T->C, stage_sz, (PT*)T->fattr.ptr, part, rowmap, units, T->nunits, \
+      (unsigned*)T->counter.ptr, base
+  // the whole-matrix schedule draws its units dynamically; the piece
+  // schedules (host-buffer gradient) stay static
+  const int2* units = (sched == (const int32_t*)T->sched.ptr && T->nunits > 0) ? (const int2*)T->units.ptr : nullptr;
+  const unsigned base = join_ctas > 0 ? T->cur_base : T->ticket_base;
+  const int launch_grid = join_ctas > 0 ? join_ctas : T->grid;
+  if (join_ctas > 0 && !units) { set_error("joining launch without a dynamic schedule"); return FITSNE_EINVAL; }
   if (kl)
-    k_attract_tiled<S, true><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
+    k_attract_tiled<S, true><<<launch_grid, kTiledThreads, smem, st>>>(TILED_ARGS);
   else
-    k_attract_tiled<S, false><<<T->grid, kTiledThreads, smem, st>>>(TILED_ARGS);
+    k_attract_tiled<S, false><<<launch_grid, kTiledThreads, smem, st>>>(TILED_ARGS);
 #undef TILED_ARGS
   FITSNE_CHECK_LAUNCH();
+  // every CTA draws tickets until one is past the last unit
+  if (join_ctas > 0) {
+    T->ticket_base += (unsigned)join_ctas;
+    T->join_grid = join_ctas;
+  } else {
+    T->cur_base = T->ticket_base;
+    T->cur_kl = kl;
+    T->cur_dynamic = units != nullptr;
+    T->join_grid = 0;
+    if (units) T->ticket_base += (unsigned)T->nunits + (unsigned)T->grid;
+  }
   return FITSNE_OK;
 }
 
 static int launch_tiled(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched,
-                        cudaStream_t st) {
+                        cudaStream_t st, int join_ctas = 0) {
   FITSNE_RANGE("tiled_spmv");
-  return ctx->dims == 1 ? launch_tiled_s<1>(ctx, Y, kl, sched, st) : launch_tiled_s<2>(ctx, Y, kl, sched, st);
+  return ctx->dims == 1 ? launch_tiled_s<1>(ctx, Y, kl, sched, st, join_ctas)
+                        : launch_tiled_s<2>(ctx, Y, kl, sched, st, join_ctas);
 }
 
 // Start of an SpMV pass over fattr: clear a stale accumulation first (see
@@ -1530,6 +1818,21 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
   return FITSNE_OK;
 }
 
+// Second launch of the pass queued by attract_tiled, on another stream: `ctas`
+// more CTAs draw work units from the same counter (they exit at once when the
+// pass is already done).  Queued by the gradient schedule behind the repulsion
+// chain, so the SMs the chain used go back to the SpMV.  *nparts grows by the
+// joining CTAs' KL partials.
+int attract_tiled_join(fitsne_ctx* ctx, const void* Y, int ctas, cudaStream_t st, int* nparts) {
+  TiledP* T = ctx->tiled;
+  if (ctas < 0 && T) ctas = ctx->num_sms - T->grid;  // the SMs the first launch left
+  if (!T || !T->cur_dynamic || ctas <= 0) return FITSNE_OK;
+  ctas = std::min(ctas, ctx->num_sms);
+  FITSNE_TRY(launch_tiled(ctx, Y, T->cur_kl, (const int32_t*)T->sched.ptr, st, ctas));
+  if (nparts) *nparts = T->grid + ctas;
+  return FITSNE_OK;
+}
+
 int attract_tiled_piece(fitsne_ctx* ctx, const void* Y, int piece, cudaStream_t st, void** fattr_out) {
   TiledP* T = ctx->tiled;
   if (piece == 0) FITSNE_TRY(tiled_begin(ctx, st));
@@ -1554,6 +1857,23 @@ int tiled_stats(fitsne_ctx* ctx, const void* Y, int64_t* out, cudaStream_t st) {
   out[5] = ctx->nnz;
   out[6] = use && T->relabeled ? 1 : 0;
   out[7] = use ? (T->nseg_natural ? T->nseg_natural : T->nseg) : 0;
+#if FITSNE_TILED_TIMING
+  if (use) {
+    std::vector<double> h(T->grid + T->join_grid);
+    cudaDeviceSynchronize();
+    cudaMemcpy(h.data(), T->part.ptr, sizeof(double) * h.size(), cudaMemcpyDeviceToHost);
+    double jsum = 0;
+    for (int i = 0; i < T->join_grid; ++i) jsum += h[T->grid + i];
+    h.resize(T->grid);
+    std::sort(h.begin(), h.end());
+    double sum = 0;
+    for (double v : h) sum += v;
+    fprintf(stderr, "tiled CTA busy time (us): min %.1f p25 %.1f median %.1f p75 %.1f max %.1f mean %.1f (grid %d, units %d; %d joining CTAs, mean %.1f)\n",
+            h[0] * 1e-3, h[T->grid / 4] * 1e-3, h[T->grid / 2] * 1e-3, h[3 * T->grid / 4] * 1e-3,
+            h[T->grid - 1] * 1e-3, sum / T->grid * 1e-3, T->grid, T->nunits, T->join_grid,
+            T->join_grid ? jsum / T->join_grid * 1e-3 : 0.0);
+  }
+#endif
   return FITSNE_OK;
 }
 
