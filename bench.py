@@ -679,6 +679,18 @@ def run_ours(args):
         check = {"vs": ref.api, "rel_l2": err, "bar": bar, "ok": err <= bar,
                  "path": "the timed step (fitsne_gradient, production schedule)"}
 
+    # the same kernel alone on every SM (the step gives it a share of the SMs,
+    # the repulsion chain runs on the rest): extra information, not the headline
+    all_sms = None
+    if tst[0] and args.tiled_ctas == 0:
+        nsm = torch.cuda.get_device_properties(dev).multi_processor_count
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_CTAS, nsm), "set_option")
+        for _ in range(3):
+            spmv()
+        ms_all = timed(spmv, args.steps, stream)
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILED_CTAS, 0), "set_option")
+        all_sms = {"ctas": nsm, "launch_ms": ms_all, "frac": b_spmv / (ms_all * 1e-3) / 1e9 / peak}
+
     line = {
         "metric": metric_name(n, dims),
         "value": 1e3 / ms, "unit": "grad_evals/s", "n_gpus": 1, "steps": args.steps,
@@ -695,6 +707,8 @@ def run_ours(args):
                      "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                      "peak_source": peak_src, "algorithmic_bytes": b_spmv,
                      "launch_ms": ms_spmv, "share_of_step": ms_spmv / ms,
+                     "ctas": "the step's grid (the SMs the overlapped schedule gives the SpMV)",
+                     "alone_on_all_sms": all_sms,
                      "traffic": traffic_from_profiles(traffic_key) if args.workload == "c3" else None},
         "cpu_baseline": cpu,
         "check": check,

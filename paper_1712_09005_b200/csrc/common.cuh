@@ -281,6 +281,7 @@ struct fitsne_ctx {
 
   fitsne_grid* h_grid = nullptr;  // pinned mirror
   double* h_scal = nullptr;       // pinned scalars
+  unsigned long long bbox_seq = 0;  // sequence number of the last bbox_launch (polled in h_scal[15])
   int32_t* h_status = nullptr;    // pinned status
 
   // affinities (borrowed device pointers)

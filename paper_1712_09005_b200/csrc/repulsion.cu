@@ -19,6 +19,8 @@
 #include <algorithm>
 #include <vector>
 
+#include <atomic>
+
 #include "common.cuh"
 #include "fft.cuh"
 #include "interp.cuh"
@@ -86,7 +88,11 @@ __device__ int device_grid(const double* mn, const double* mx, int S, const DevG
 template <typename T, int S>
 __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ part,
                        int* __restrict__ nonfinite, double* __restrict__ out, int negate_max,
-                       GridArgs* __restrict__ dgrid, DevGridReq rq) {
+                       GridArgs* __restrict__ dgrid, DevGridReq rq, double* hout = nullptr,
+                       unsigned long long seq = 0) {
+  // hout: pinned host memory the last block also writes the box to, followed
+  // by the sequence number seq at hout[7] -- the host polls that word instead
+  // of waiting for a copy and an event (bbox_wait)
   double mn[S], mx[S];
 #pragma unroll
   for (int d = 0; d < S; ++d) { mn[d] = INFINITY; mx[d] = -INFINITY; }
@@ -169,6 +175,13 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
     const int bad = __ldcg(nonfinite);
     out[2 * S] = sg * (double)bad;
     nonfinite[1] = 0;  // ticket reset for the next launch
+    if (hout) {
+#pragma unroll
+      for (int d = 0; d < S; ++d) { hout[d] = mn[d]; hout[S + d] = sg * mx[d]; }
+      hout[2 * S] = sg * (double)bad;
+      __threadfence_system();
+      *reinterpret_cast<volatile unsigned long long*>(hout + 7) = seq;
+    }
     if (dgrid) {
       // the grid for the stages queued behind this kernel (device-grid schedule)
       fitsne_grid g;
@@ -211,7 +224,7 @@ __global__ void k_bbox(const T* __restrict__ Y, int64_t n, double* __restrict__ 
 // MIN-all-reduce layout of fitsne_bbox_device
 static int bbox_kernels(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, int negate_max,
                         cudaStream_t st, double** outd_used, GridArgs* dgrid = nullptr,
-                        DevGridReq rq = DevGridReq{}) {
+                        DevGridReq rq = DevGridReq{}, double* hout = nullptr, unsigned long long seq = 0) {
   const int S = ctx->dims;
   int nblk = (int)std::min<int64_t>(std::max<int64_t>((n + kBlock - 1) / kBlock, 1), 4 * ctx->num_sms);
   FITSNE_TRY(ensure(ctx->bbox_part, sizeof(double) * (size_t)nblk * 2 * S + 64));
@@ -222,11 +235,11 @@ static int bbox_kernels(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_d
   // flag[0]: non-finite, flag[1]: last-block ticket (k_bbox folds the partials)
   FITSNE_CUDA(cudaMemsetAsync(flag, 0, 2 * sizeof(int), st));
   if (ctx->dtype == FITSNE_F32) {
-    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max, dgrid, rq);
-    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max, dgrid, rq);
+    if (S == 1) k_bbox<float, 1><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max, dgrid, rq, hout, seq);
+    else k_bbox<float, 2><<<nblk, kBlock, 0, st>>>((const float*)Y, n, part, flag, outd, negate_max, dgrid, rq, hout, seq);
   } else {
-    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max, dgrid, rq);
-    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max, dgrid, rq);
+    if (S == 1) k_bbox<double, 1><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max, dgrid, rq, hout, seq);
+    else k_bbox<double, 2><<<nblk, kBlock, 0, st>>>((const double*)Y, n, part, flag, outd, negate_max, dgrid, rq, hout, seq);
   }
   FITSNE_CHECK_LAUNCH();
   if (outd_used) *outd_used = outd;
@@ -240,9 +253,11 @@ int bbox_device(fitsne_ctx* ctx, const void* Y, int64_t n, double* out_dev, cuda
 int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
   const int S = ctx->dims;
   double* outd = nullptr;
-  FITSNE_TRY(bbox_kernels(ctx, Y, n, nullptr, 0, st, &outd));
-  FITSNE_CUDA(cudaMemcpyAsync(ctx->h_scal + 8, outd, sizeof(double) * (2 * S + 1),
-                              cudaMemcpyDeviceToHost, st));
+  // the kernel's last block writes the box and then a sequence number straight
+  // into the pinned h_scal[8 .. 15] (bbox_wait polls it); the event is the
+  // fallback and the error path
+  ++ctx->bbox_seq;
+  FITSNE_TRY(bbox_kernels(ctx, Y, n, nullptr, 0, st, &outd, nullptr, DevGridReq{}, ctx->h_scal + 8, ctx->bbox_seq));
   if (!ctx->ev_bbox) FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_bbox, cudaEventDisableTiming));
   FITSNE_CUDA(cudaEventRecord(ctx->ev_bbox, st));
   return FITSNE_OK;
@@ -251,7 +266,19 @@ int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
 int bbox_wait(fitsne_ctx* ctx, double* bbox_host) {
   FITSNE_RANGE("bbox_wait");
   const int S = ctx->dims;
-  FITSNE_CUDA(cudaEventSynchronize(ctx->ev_bbox));
+  {
+    // poll the sequence word (a few microseconds after the kernel's last
+    // block); give up after ~2 ms of polling and wait for the event instead
+    volatile unsigned long long* seq = reinterpret_cast<volatile unsigned long long*>(ctx->h_scal + 15);
+    bool seen = false;
+    for (int spin = 0; spin < 4000000; ++spin) {
+      if (*seq == ctx->bbox_seq) { seen = true; break; }
+      if ((spin & 1023) == 1023 && cudaEventQuery(ctx->ev_bbox) != cudaErrorNotReady) break;
+    }
+    if (!seen) FITSNE_CUDA(cudaEventSynchronize(ctx->ev_bbox));
+    std::atomic_thread_fence(std::memory_order_acquire);
+    if (*seq != ctx->bbox_seq) { set_error("bounding box kernel did not complete"); return FITSNE_ECUDA; }
+  }
   if (ctx->h_scal[8 + 2 * S] != 0.0) {
     set_error("points must be finite");
     return FITSNE_EPOINTS;

@@ -125,10 +125,10 @@ static constexpr bool kBankRows = FITSNE_TILED_BANKROWS != 0;
 // groups of a slab boundary moves onto it (the slab is then not shared by two
 // warps).  Tenths of a group; 0 / 0 = equal group counts.
 #ifndef FITSNE_TILED_CUT_BETA
-#define FITSNE_TILED_CUT_BETA 15
+#define FITSNE_TILED_CUT_BETA 10
 #endif
 #ifndef FITSNE_TILED_CUT_SNAP
-#define FITSNE_TILED_CUT_SNAP 10
+#define FITSNE_TILED_CUT_SNAP 15
 #endif
 #ifndef FITSNE_TILED_WSLAB_BCOST
 #define FITSNE_TILED_WSLAB_BCOST 1
@@ -598,15 +598,15 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
   for (int64_t k = lane; k < (int64_t)ns * 32; k += 32) hr[k] = rows[(int64_t)sb * 32 + k];
 }
 
-// Persistent grid: with the overlapped schedule 1/12 of the SMs stay free
-// for the spread / FFT stages running concurrently on the side stream (the
-// tiled kernel fills an SM: 1024 threads x 64 registers, ~218 KB of shared
-// memory); serial schedules use every SM.  At C3 the step time is flat from
-// ~120 to ~136 CTAs (the repulsion chain and the SpMV trade places as the
-// critical path); the SpMV is most efficient at the top of that range.
+// Persistent grid: with the overlapped schedule ~3/16 of the SMs stay free
+// for the bbox / spread / FFT / gather chain running concurrently on the side
+// stream (the tiled kernel fills an SM: 1024 threads x 64 registers, ~218 KB
+// of shared memory); serial schedules use every SM.  The chain is ~1/3 of the
+// step's SM-time at C3: with 120 of 148 SMs on the SpMV both end together
+// (104: 1876, 112: 1879, 120: 1907, 128: 1868, 136: 1838 evaluations/s).
 static int tiled_grid(const fitsne_ctx* ctx) {
   if (ctx->tiled_ctas > 0) return ctx->tiled_ctas;
-  if (ctx->overlap != 0) return std::max(1, ctx->num_sms - ctx->num_sms / 12);
+  if (ctx->overlap != 0) return std::max(1, ctx->num_sms - (3 * ctx->num_sms + 8) / 16);
   return ctx->num_sms;
 }
 

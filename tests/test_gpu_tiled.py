@@ -136,6 +136,55 @@ def test_tiled_kl_and_gradient(cuda):
     assert rel_l2(res[2][1], want) <= 1e-3
 
 
+@pytest.mark.parametrize("ctas", [3, 7, 40])
+def test_schedule_options_agree(cuda, ctas):
+    """F_rep gathered beside the SpMV + streaming combine (FITSNE_OPT_SIDE_GATHER)
+    and the joining SpMV launch (FITSNE_OPT_SPMV_JOIN) against the combine that
+    gathers F_rep itself and a single launch: same gradient, every switch
+    combination, over repeated calls (the dynamic schedule's ticket counter runs
+    on), and in the fused iteration."""
+    from paper_1712_09005_b200 import _lib
+    n = 6007
+    rr, cc, v, Y = _graph(n, 30, seed=11)
+    csr = _csr(n, rr, cc, v)
+    y = torch.from_numpy(Y.astype(np.float32)).cuda()
+    want = O.grad(rr, cc, v, Y.astype(np.float32).astype(np.float64), 4.0, min_intervals=20, p=3)
+    got = {}
+    for sg in (0, 1):
+        for join in (0, 1):
+            ctx = _ctx(2, 128, 512, ctas)
+            _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SIDE_GATHER, sg), "set_option")
+            _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SPMV_JOIN, join), "set_option")
+            ctx.set_affinities(csr)
+            g = torch.empty_like(y)
+            for _ in range(3):
+                g.fill_(float("nan"))
+                _lib.check(ctx.lib.fitsne_gradient(ctx.h, _lib.ptr(y), 4.0, _lib.ptr(g), None, ctx.stream),
+                           "gradient")
+                torch.cuda.synchronize()
+                a = g.cpu().numpy().astype(np.float64)
+                assert rel_l2(a, want) <= 1e-3
+                got.setdefault((sg, join), a)
+                assert rel_l2(a, got[(sg, join)]) <= 2e-5  # summation order of the fp32 atomics only
+            # fused iteration with the KL: the joining CTAs' KL partials are counted
+            yo, vel, gains = torch.empty_like(y), torch.zeros_like(y), torch.ones_like(y)
+            kl = torch.zeros(1, dtype=torch.float64, device=y.device)
+            st = torch.zeros(1, dtype=torch.int32, device=y.device)
+            _lib.check(ctx.lib.fitsne_iterate(ctx.h, _lib.ptr(y), _lib.ptr(yo), _lib.ptr(vel), _lib.ptr(gains),
+                                              4.0, 0.5, 200.0, _lib.ptr(kl), _lib.ptr(st), ctx.stream), "iterate")
+            torch.cuda.synchronize()
+            got[(sg, join, "kl")] = float(kl.item())
+            got[(sg, join, "y")] = yo.cpu().numpy().astype(np.float64)
+    base = got[(0, 0)]
+    for key, a in got.items():
+        if len(key) == 2:
+            assert rel_l2(a, base) <= 2e-5, key
+        elif key[2] == "kl":
+            assert abs(a - got[(0, 0, "kl")]) <= 1e-9 * abs(got[(0, 0, "kl")]), key
+        else:
+            assert rel_l2(a, got[(0, 0, "y")]) <= 1e-5, key
+
+
 @pytest.mark.parametrize("pieces", [0, 1, 2])
 @pytest.mark.parametrize("shape", [(128, 512, 5), (64, 256, 0), (2048, 4096, 2)])
 def test_gradient_host_pieces(cuda, shape, pieces):
