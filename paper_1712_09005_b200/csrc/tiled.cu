@@ -42,6 +42,9 @@ namespace fitsne {
 //   int32 wlo[32]            first group of consumer warp w's run (cost-balanced cuts)
 //   int32 wstart[32]         slab holding the first group of consumer warp w
 //                            (whole-slab split: warp w owns slabs [wstart[w], wstart[w + 1]))
+//   int32 wdesc[32][4]       consumer warp w's run in one 16-byte word: {first group, end group,
+//                            first slab | (first slab is shared with another warp) << 31,
+//                            end group of the first slab}
 //   uint32 goff[nslab + 1]   group offsets of the slabs (padded to 4 entries)
 //   uint16 rows[nslab][32]   tile-local row of each lane (0xFFFF: empty lane)
 // where a "group" is 32 consecutive slots, one per lane.
@@ -56,7 +59,8 @@ struct TileLoad {
 __host__ __device__ inline int hdr_goff_words(int nslab) { return (nslab + 1 + 3) & ~3; }
 constexpr int kHdrWstart = 16;                 // int32 wstart[32] after meta
 constexpr int kHdrWlo = kHdrWstart + 128;      // int32 wlo[32]: first group of consumer warp w's run
-constexpr int kHdrGoff = kHdrWlo + 128;        // uint32 goff[] after wlo
+constexpr int kHdrWdesc = kHdrWlo + 128;       // int4 wdesc[32]: {lo, hi, first slab | shared << 31, its end}
+constexpr int kHdrGoff = kHdrWdesc + 512;      // uint32 goff[] after wdesc
 __host__ __device__ inline int hdr_bytes_for(int nslab) {
   return kHdrGoff + 4 * hdr_goff_words(nslab) + 64 * nslab;
 }
@@ -138,9 +142,23 @@ static constexpr int kKeyTileShift = 32;  // sort key: tile << 32 | (0xFFFF - co
 static constexpr int kTiledU = FITSNE_TILED_U;    // groups per lane per pipeline step
 static constexpr int kTiledPad = 4 * kTiledU * 32;  // tail padding of the slot arrays
 
-// Slot layout: group-major, lane-minor (a warp reads one group's columns and
-// values with one coalesced 64-byte and one 128-byte load).
+// Slot layout.  FITSNE_TILED_VEC = 1 (default): batches of four groups, lane-
+// major inside a batch -- slot (g, lane) at (g / 4) * 128 + lane * 4 + g % 4 --
+// so a lane reads a batch's four columns with one 8-byte and its four values
+// with one 16-byte load (two coalesced global loads per four groups instead of
+// eight).  FITSNE_TILED_VEC = 0: group-major, lane-minor (one 64-byte and one
+// 128-byte warp load per group).
+#ifndef FITSNE_TILED_VEC
+#define FITSNE_TILED_VEC 1
+#endif
+#if FITSNE_TILED_VEC
+static_assert(FITSNE_TILED_U == 4, "the vector slot layout is built for batches of four groups");
+__host__ __device__ inline int64_t slot_index(int64_t g, int lane) {
+  return ((g >> 2) << 7) + ((int64_t)lane << 2) + (g & 3);
+}
+#else
 __host__ __device__ inline int64_t slot_index(int64_t g, int lane) { return g * 32 + lane; }
+#endif
 #ifndef FITSNE_TILED_STAGES
 #define FITSNE_TILED_STAGES 2
 #endif
@@ -596,6 +614,29 @@ __global__ void k_tile_headers(const int32_t* __restrict__ t_dense, const int32_
   }
   for (int j = lane; j < hdr_goff_words(ns); j += 32) goff[j] = j <= ns ? slab_off[sb + j] - g0 : 0u;
   for (int64_t k = lane; k < (int64_t)ns * 32; k += 32) hr[k] = rows[(int64_t)sb * 32 + k];
+  {
+    // the run of consumer warp `lane` in one 16-byte word
+    const int lo = wlo[lane], a = wstart[lane];
+    int hi = __shfl_down_sync(0xffffffffu, lo, 1);
+    if (lane >= kTiledConsumers - 1) hi = (int)ng;
+    if (lane >= kTiledConsumers) hi = lo;
+    const int a_lo = (int)(slab_off[sb + a] - g0), a_end = (int)(slab_off[sb + a + 1] - g0);
+    const bool shared = a_lo < lo || a_end > hi;
+    int4 d;
+    d.x = lo;
+    d.y = hi;
+    d.z = a | (shared ? (int)0x80000000u : 0);
+    d.w = a_end;
+    reinterpret_cast<int4*>(h + kHdrWdesc)[lane] = d;
+  }
+}
+
+// The stored column of a slot becomes its byte offset inside the staged chunk
+// (column x sizeof(point): < 65536 for 8192 2-D or 16384 1-D points), so the
+// consumers add it to the chunk's base without a shift.  Last build pass.
+__global__ void k_cols_to_offsets(uint16_t* __restrict__ cols, int64_t nslots, int shift) {
+  const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (i < nslots) cols[i] = (uint16_t)((uint32_t)cols[i] << shift);
 }
 
 // Persistent grid: with the overlapped schedule ~3/16 of the SMs stay free
@@ -781,6 +822,10 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   const int R = ctx->tile_rows, C = tile_cols_eff(ctx);
   const int64_t nrb = (n_rows + R - 1) / R, nch = (n_total + C - 1) / C;
   const int64_t ntd = nrb * nch;  // dense tile count
+  if ((int64_t)C * (ctx->dims == 1 ? 4 : 8) > 65536) {
+    set_error("tile_cols too large: a staged chunk holds at most 64 KB of points");
+    return FITSNE_EINVAL;
+  }
   if (ntd >= (1LL << 31) || nnz >= (1LL << 31) || nrb >= (1LL << 31)) {
     set_error("P too large for the tiled layout");
     return FITSNE_ETOOBIG;
@@ -996,6 +1041,11 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
       FITSNE_CHECK_LAUNCH();
     }
   }
+  // columns -> byte offsets inside the staged chunk (after the bank ordering,
+  // which reads columns)
+  k_cols_to_offsets<<<nb(nslots + kTiledPad, 256), 256, 0, st>>>((uint16_t*)T->cols.ptr, nslots + kTiledPad,
+                                                               ctx->dims == 1 ? 2 : 3);
+  FITSNE_CHECK_LAUNCH();
 
   // host: compact tile list, header blobs, static schedule balanced on cost
   std::vector<uint32_t> h_off((size_t)nslabs + 1);
@@ -1299,6 +1349,33 @@ template <> struct TPt<2> {
   static __device__ __forceinline__ T make(float a, float b) { return make_float2(a, b); }
   static __device__ __forceinline__ T add(T a, T b) { return make_float2(a.x + b.x, a.y + b.y); }
   static __device__ __forceinline__ bool nonzero(T a) { return a.x != 0.f || a.y != 0.f; }
+  // the point at shared-memory address a (a staged chunk: read-only while the
+  // tile is processed, so the load may be scheduled freely)
+  static __device__ __forceinline__ T lds(uint32_t a) {
+    T v;
+    asm("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a));
+    return v;
+  }
+  // accumulator read / write by shared-memory address (ordered: volatile)
+  static __device__ __forceinline__ T lds_acc(uint32_t a) {
+    T v;
+    asm volatile("ld.shared.v2.f32 {%0, %1}, [%2];" : "=f"(v.x), "=f"(v.y) : "r"(a) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ void sts_acc(uint32_t a, T v) {
+    asm volatile("st.shared.v2.f32 [%0], {%1, %2};" ::"r"(a), "f"(v.x), "f"(v.y) : "memory");
+  }
+  // *a += (x, y), concurrent-safe (64-bit compare-and-swap)
+  static __device__ __forceinline__ void smem_add_s(uint32_t a, float x, float y) {
+    unsigned long long old, was;
+    asm volatile("ld.shared.b64 %0, [%1];" : "=l"(old) : "r"(a) : "memory");
+    do {
+      was = old;
+      const float2 v = make_float2(__uint_as_float((uint32_t)was) + x, __uint_as_float((uint32_t)(was >> 32)) + y);
+      const unsigned long long nv = ((unsigned long long)__float_as_uint(v.y) << 32) | __float_as_uint(v.x);
+      asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(was), "l"(nv) : "memory");
+    } while (old != was);
+  }
   // *p += (a, b) on shared memory, concurrent-safe (64-bit compare-and-swap)
   static __device__ __forceinline__ void smem_add(T* p, float a, float b) {
     unsigned long long* q = reinterpret_cast<unsigned long long*>(p);
@@ -1327,6 +1404,22 @@ template <> struct TPt<1> {
   static __device__ __forceinline__ T make(float a, float) { return a; }
   static __device__ __forceinline__ T add(T a, T b) { return a + b; }
   static __device__ __forceinline__ bool nonzero(T a) { return a != 0.f; }
+  static __device__ __forceinline__ T lds(uint32_t a) {
+    T v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a));
+    return v;
+  }
+  static __device__ __forceinline__ T lds_acc(uint32_t a) {
+    T v;
+    asm volatile("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(a) : "memory");
+    return v;
+  }
+  static __device__ __forceinline__ void sts_acc(uint32_t a, T v) {
+    asm volatile("st.shared.f32 [%0], %1;" ::"r"(a), "f"(v) : "memory");
+  }
+  static __device__ __forceinline__ void smem_add_s(uint32_t a, float x, float) {
+    asm volatile("red.shared.add.f32 [%0], %1;" ::"r"(a), "f"(x) : "memory");
+  }
   static __device__ __forceinline__ void smem_add(T* p, float a, float) { atomicAdd(p, a); }
   static __device__ __forceinline__ float accum(T yi, T yj, float p, float& ax, float&) {
     const float dx = yi - yj;
@@ -1429,9 +1522,16 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         // one-batch register pipeline; staging the slots in L2 one to two
         // tiles ahead turns their DRAM latency into L2 latency
         {
-          const char* cbeg = reinterpret_cast<const char*>(cols + (size_t)slot_index(d.g0, 0));
-          const char* vbeg = reinterpret_cast<const char*>(vals + (size_t)slot_index(d.g0, 0));
-          uint32_t cb = (uint32_t)d.ng * 64u, vb = (uint32_t)d.ng * 128u;
+#if FITSNE_TILED_VEC
+          const int64_t gb = (int64_t)d.g0 & ~(int64_t)3;  // the batch holding the tile's first group
+          const uint32_t ngb = (uint32_t)(((int64_t)d.g0 + d.ng + 3 - gb) & ~(int64_t)3);
+#else
+          const int64_t gb = d.g0;
+          const uint32_t ngb = (uint32_t)d.ng;
+#endif
+          const char* cbeg = reinterpret_cast<const char*>(cols + (size_t)slot_index(gb, 0));
+          const char* vbeg = reinterpret_cast<const char*>(vals + (size_t)slot_index(gb, 0));
+          uint32_t cb = ngb * 64u, vb = ngb * 128u;
           for (uint32_t o = 0; o < cb; o += 65536u) bulk_prefetch_l2(cbeg + o, min(65536u, cb - o));
           for (uint32_t o = 0; o < vb; o += 65536u) bulk_prefetch_l2(vbeg + o, min(65536u, vb - o));
         }
@@ -1468,6 +1568,11 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
   // one tile apart (the producer refills a stage only after every consumer
   // released it), so even and odd tiles accumulate into separate arrays and
   // those flushes are plain shared-memory read-modify-writes.
+  // shared-memory address of the row block's points; kept in a register (the
+  // empty asm hides how it was computed, so it is not rematerialised -- a
+  // special-register read and three integer instructions -- at every use)
+  uint32_t ys_s = (uint32_t)__cvta_generic_to_shared(ys);
+  asm volatile("" : "+r"(ys_s));
   float kl = 0.f;
   double kld = 0.0;
   int cur_rb = -1;
@@ -1479,16 +1584,19 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       if (Tr::nonzero(v)) atomicAdd(fattr + (rowmap ? (int64_t)rowmap[r0 + i] : r0 + i), v);
     }
   };
+#if !FITSNE_TILED_VEC
   unsigned short cA[kTiledU], cB[kTiledU];
   float pA[kTiledU], pB[kTiledU];
+#endif
   for (int it = 0;; ++it) {
     const int b = it % kTiledStages;
     const unsigned char* st = ring + (size_t)b * stage_sz;
-    const PT* cb = reinterpret_cast<const PT*>(st);
     const unsigned char* h = st + (size_t)C * sizeof(PT);
+    const uint32_t st_s = (uint32_t)__cvta_generic_to_shared(st);  // the staged chunk's shared-memory address
     mbar_wait(&full[b], (uint32_t)((it / kTiledStages) & 1));
     if (!live[b]) break;
-    const int32_t* meta = reinterpret_cast<const int32_t*>(h);
+    const int4 meta4 = *reinterpret_cast<const int4*>(h);
+    const int32_t meta[4] = {meta4.x, meta4.y, meta4.z, meta4.w};
     const int rb = meta[0], ns = meta[1];
     FITSNE_DCHECK(rb >= 0 && (int64_t)rb * R < n_rows && ns >= 1 && ns <= (R + 31) / 32 + 1 &&
                   meta[3] >= 0);
@@ -1509,15 +1617,16 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       }
       consumer_sync();
     }
-    PT* accp = acc + (size_t)(it & 1) * R;
+    // this tile's accumulator (even / odd): address of row 0
+    const uint32_t accp_s = ys_s + (uint32_t)((1 + (it & 1)) * R) * (uint32_t)sizeof(PT);
 #if FITSNE_TILED_WSLAB
     // this warp's slabs [ws0, ws1) and their groups [lo, hi)
     const int ws0 = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
     const int ws1 = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp + 1];
     const int lo = (int)goff[ws0], hi = (int)goff[ws1];
 #else
-    const int lo = reinterpret_cast<const int32_t*>(h + kHdrWlo)[warp];
-    const int hi = reinterpret_cast<const int32_t*>(h + kHdrWlo)[warp + 1];
+    const int4 wd = reinterpret_cast<const int4*>(h + kHdrWdesc)[warp];
+    const int lo = wd.x, hi = wd.y;
 #endif
     if (lo < hi) {
 #if FITSNE_TILED_WSLAB
@@ -1525,12 +1634,12 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       int s_end = (int)goff[s + 1];
       constexpr bool shared_slab = false;  // every slab belongs to one warp
 #else
-      int s = reinterpret_cast<const int32_t*>(h + kHdrWstart)[warp];
-      int s_end = (int)goff[s + 1];
-      bool shared_slab = (int)goff[s] < lo || s_end > hi;
+      int s = wd.z & 0x7FFFFFFF;
+      int s_end = wd.w;
+      bool shared_slab = wd.z < 0;
 #endif
       int row = hrows[s * 32 + lane];
-      PT yi = row != 0xFFFF ? ys[row] : Tr::zero();
+      PT yi = row != 0xFFFF ? Tr::lds(ys_s + (uint32_t)row * (uint32_t)sizeof(PT)) : Tr::zero();
       float ax = 0.f, ay = 0.f;
       // output index of a shared slab's row, loaded when the slab starts so
       // the (relabelled) row map's L2 latency is hidden behind the slab
@@ -1542,15 +1651,16 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       out_row();
       auto flush_row = [&]() {
         if (row == 0xFFFF) return;
+        const uint32_t ra = accp_s + (uint32_t)row * (uint32_t)sizeof(PT);
         if (FITSNE_TILED_SCUT && shared_slab) {
-          Tr::smem_add(accp + row, ax, ay);  // the slab's other warps add to the same row
+          Tr::smem_add_s(ra, ax, ay);  // the slab's other warps add to the same row
         } else if (shared_slab) {
           // rows of a slab cut by a warp-range boundary are updated by two or
           // more warps of this tile: add straight to the output with a vector
           // reduction in L2 instead of a shared-memory compare-and-swap loop
           atomicAdd(fattr + orow, Tr::make(ax, ay));
         } else {
-          accp[row] = Tr::add(accp[row], Tr::make(ax, ay));
+          Tr::sts_acc(ra, Tr::add(Tr::lds_acc(ra), Tr::make(ax, ay)));
         }
       };
       // slab boundary (warp-uniform): flush the finished row, load the next
@@ -1563,7 +1673,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         shared_slab = s_end > hi;
 #endif
         row = hrows[s * 32 + lane];
-        yi = row != 0xFFFF ? ys[row] : Tr::zero();
+        yi = row != 0xFFFF ? Tr::lds(ys_s + (uint32_t)row * (uint32_t)sizeof(PT)) : Tr::zero();
         out_row();
       };
       auto accum = [&](PT yj, float p) {
@@ -1571,11 +1681,85 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         if (KL) kl += p * __logf(q);
       };
       // one group: slab boundary check, gather, accumulate (tail groups)
-      auto step = [&](int gg, unsigned short c, float p) {
+      // (off: the column's byte offset inside the staged chunk)
+      auto step = [&](int gg, uint32_t off, float p) {
         if (gg == s_end) advance();
-        FITSNE_DCHECK(c < C && s < ns && (row == 0xFFFF || row < R));
-        accum(cb[c], p);
+        FITSNE_DCHECK(off < (uint32_t)C * sizeof(PT) && off % sizeof(PT) == 0 && s < ns &&
+                      (row == 0xFFFF || row < R));
+        accum(Tr::lds(st_s + off), p);
       };
+#if FITSNE_TILED_VEC
+      // batches [bb, be) of four groups hold this warp's run; the first and
+      // the last may be shared with the neighbouring runs (groups outside
+      // [lo, hi) are skipped: `guarded`).  One batch of loads in flight ahead
+      // of the one being consumed; reads past the run stay inside the padded
+      // arrays.
+      const int64_t bb = (g0 + lo) >> 2;
+      const uint2* cp = reinterpret_cast<const uint2*>(cols) + bb * 32 + lane;
+      const float4* vp = reinterpret_cast<const float4*>(vals) + bb * 32 + lane;
+      uint2 cv = __ldcs(cp);
+      float4 pv = __ldcs(vp);
+      int g = (int)((bb << 2) - g0);  // tile-relative group of the batch's first slot (may precede lo)
+      auto full = [&](const uint2 c, const float4 p, const int gb) {
+        step(gb, c.x & 0xFFFFu, p.x);
+        step(gb + 1, c.x >> 16, p.y);
+        step(gb + 2, c.y & 0xFFFFu, p.z);
+        step(gb + 3, c.y >> 16, p.w);
+      };
+      auto guarded = [&](const uint2 c, const float4 p, const int gb) {
+#pragma unroll 1
+        for (int u = 0; u < 4; ++u) {
+          const uint32_t w = (u & 2) ? c.y : c.x;
+          const float pu = u == 0 ? p.x : u == 1 ? p.y : u == 2 ? p.z : p.w;
+          if (gb + u >= lo && gb + u < hi) step(gb + u, (u & 1) ? (w >> 16) : (w & 0xFFFFu), pu);
+        }
+      };
+      if (g < lo) {  // head batch shared with the previous run
+        const uint2 cn = __ldcs(cp + 32);
+        const float4 pn = __ldcs(vp + 32);
+        if (hi >= g + 4) {
+          const int k = lo - g;  // the batch's first k = 1..3 groups belong to the previous run
+          if (k == 1) step(g + 1, cv.x >> 16, pv.y);
+          if (k <= 2) step(g + 2, cv.y & 0xFFFFu, pv.z);
+          step(g + 3, cv.y >> 16, pv.w);
+        } else {
+          guarded(cv, pv, g);  // (rare) the run also ends inside this batch
+        }
+        cv = cn;
+        pv = pn;
+        cp += 32;
+        vp += 32;
+        g += 4;
+      }
+      int nfull = (hi - g) >> 2;  // whole batches from g (negative: the run ended inside the head batch)
+      for (; nfull >= 2; nfull -= 2) {
+        const uint2 c1 = __ldcs(cp + 32);
+        const float4 p1 = __ldcs(vp + 32);
+        full(cv, pv, g);
+        cv = __ldcs(cp + 64);
+        pv = __ldcs(vp + 64);
+        full(c1, p1, g + 4);
+        cp += 64;
+        vp += 64;
+        g += 8;
+      }
+      if (nfull == 1) {
+        const uint2 cn = __ldcs(cp + 32);
+        const float4 pn = __ldcs(vp + 32);
+        full(cv, pv, g);
+        cv = cn;
+        pv = pn;
+        g += 4;
+      }
+      if (g < hi) {  // tail batch shared with the next run: its first 1..3 groups
+        const int k = hi - g;
+        step(g, cv.x & 0xFFFFu, pv.x);
+        if (k > 1) step(g + 1, cv.x >> 16, pv.y);
+        if (k > 2) step(g + 2, cv.y & 0xFFFFu, pv.z);
+      }
+      flush_row();
+      if (KL) { kld += (double)kl; kl = 0.f; }
+#else
       const uint16_t* cp = cols + (size_t)slot_index(g0 + lo, lane);
       const float* vp = vals + (size_t)slot_index(g0 + lo, lane);
 #pragma unroll
@@ -1614,7 +1798,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         // written while the tile is processed; the flushes write accumulators)
         PT yj[kTiledU];
 #pragma unroll
-        for (int u = 0; u < kTiledU; ++u) yj[u] = cb[cA[u]];
+        for (int u = 0; u < kTiledU; ++u) yj[u] = Tr::lds(st_s + cA[u]);
         if (s_end >= g + kTiledU) {
           // no slab boundary inside the batch: straight-line accumulation
 #pragma unroll
@@ -1630,7 +1814,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         if (s_end >= g + kTiledU) {
           // no slab boundary inside the batch: straight-line accumulation
 #pragma unroll
-          for (int u = 0; u < kTiledU; ++u) accum(cb[cA[u]], pA[u]);
+          for (int u = 0; u < kTiledU; ++u) accum(Tr::lds(st_s + cA[u]), pA[u]);
         } else {
 #pragma unroll
           for (int u = 0; u < kTiledU; ++u) step(g + u, cA[u], pA[u]);
@@ -1655,6 +1839,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
         if (g + u < hi) step(g + u, cA[u], pA[u]);
       flush_row();
       if (KL) { kld += (double)kl; kl = 0.f; }
+#endif
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&empty[b]);

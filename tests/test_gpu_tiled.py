@@ -180,7 +180,7 @@ def test_schedule_options_agree(cuda, ctas):
         if len(key) == 2:
             assert rel_l2(a, base) <= 2e-5, key
         elif key[2] == "kl":
-            assert abs(a - got[(0, 0, "kl")]) <= 1e-9 * abs(got[(0, 0, "kl")]), key
+            assert abs(a - got[(0, 0, "kl")]) <= 1e-7 * abs(got[(0, 0, "kl")]), key  # fp32 partial sums
         else:
             assert rel_l2(a, got[(0, 0, "y")]) <= 1e-5, key
 
@@ -249,8 +249,12 @@ def test_tiled_run_tsne_matches_csr(cuda):
         _lib.check(ctx.lib.fitsne_set_option(ctx.h, OPT_COLS, 512), "set_option")
         cfg = optimizer.TsneConfig(dims=2, n_iter=30, seed=1, dtype="float32", min_intervals=50,
                                    exaggeration=optimizer.ExaggerationSchedule(12.0, 10))
-        logs[mode] = np.asarray(optimizer.run_tsne(affinities=P, config=cfg).kl_log, dtype=float)
-        _lib.check(ctx.lib.fitsne_set_option(ctx.h, OPT_TILED, 1), "set_option")
+        try:
+            logs[mode] = np.asarray(optimizer.run_tsne(affinities=P, config=cfg).kl_log, dtype=float)
+        finally:
+            # the context is the cached per-thread one: put the defaults back
+            for opt, val in ((OPT_TILED, 1), (OPT_ROWS, 3072), (OPT_COLS, 8192)):
+                _lib.check(ctx.lib.fitsne_set_option(ctx.h, opt, val), "set_option")
     assert np.max(np.abs(logs[2] - logs[0]) / np.abs(logs[0])) <= 1e-4
 
 
