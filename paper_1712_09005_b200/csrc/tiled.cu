@@ -124,6 +124,11 @@ static constexpr bool kWslab = FITSNE_TILED_WSLAB != 0;
 #define FITSNE_TILED_BANKROWS 1
 #endif
 static constexpr bool kBankRows = FITSNE_TILED_BANKROWS != 0;
+// a slab's rows placed in the lanes where their bank is free (k_slab_lanes)
+#ifndef FITSNE_TILED_LANEDEAL
+#define FITSNE_TILED_LANEDEAL 1
+#endif
+static constexpr bool kLaneDeal = FITSNE_TILED_LANEDEAL != 0;
 // Consumer-warp runs inside a tile: cut points balance groups + BETA per slab
 // start (a slab boundary costs about that many groups), and a cut within SNAP
 // groups of a slab boundary moves onto it (the slab is then not shared by two
@@ -374,6 +379,47 @@ __global__ void k_slab_kmax(const int32_t* __restrict__ tfirst, const int32_t* _
   for (int j = 0; j < ns; ++j) kmax[slab_begin[t] + j] = (uint32_t)seg_cnt[sidx[tfirst[t] + 32 * j]];
 }
 
+// Lane of each row inside its slab.  The sort deals a (tile, count) class's
+// rows round-robin over the shared-memory banks of their point / accumulator,
+// but a slab -- 32 consecutive rows of that order -- still mixes the tails of
+// two rank groups, and a 64-bit access conflicts inside a half-warp on row mod
+// 16.  The slab's rows may sit in any lane: put each row in a half-warp (2-D;
+// the whole warp in 1-D) where its bank is still free, the rest wherever room
+// is left.  One thread per slab; lane_of[q] for the sorted segment q.
+__global__ void k_slab_lanes(const uint64_t* __restrict__ key, const int32_t* __restrict__ tfirst,
+                             const int32_t* __restrict__ tcount, const int32_t* __restrict__ nslab,
+                             int64_t ntd, int nbanks, unsigned char* __restrict__ lane_of) {
+  const int64_t t = blockIdx.x;
+  if (t >= ntd) return;
+  const int ns = nslab[t];
+  for (int j = threadIdx.x; j < ns; j += blockDim.x) {
+    const int64_t q0 = (int64_t)tfirst[t] + 32 * j;
+    const int n = min(32, tcount[t] - 32 * j);
+    const int ngrp = 32 / nbanks;          // 2 half-warps of 16 banks, or 1 group of 32
+    unsigned used[2] = {0u, 0u};
+    unsigned taken = 0u;                   // lanes in use
+    unsigned deferred = 0u;
+    for (int i = 0; i < n; ++i) {
+      const int b = (int)(key[q0 + i] & (uint64_t)(nbanks - 1));
+      int g = -1;
+      for (int h = 0; h < ngrp; ++h)
+        if (g < 0 && !((used[h] >> b) & 1u)) g = h;
+      if (g < 0) { deferred |= 1u << i; continue; }
+      used[g] |= 1u << b;
+      // the bank's own lane of the group: lanes of one group then hold distinct banks by construction
+      const int lane = g * nbanks + b;
+      taken |= 1u << lane;
+      lane_of[q0 + i] = (unsigned char)lane;
+    }
+    for (int i = 0; i < n; ++i) {
+      if (!((deferred >> i) & 1u)) continue;
+      const int lane = __ffs(~taken) - 1;
+      taken |= 1u << lane;
+      lane_of[q0 + i] = (unsigned char)lane;
+    }
+  }
+}
+
 __global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __restrict__ sidx,
                             int64_t nseg, const int32_t* __restrict__ tfirst,
                             const int32_t* __restrict__ slab_begin, const int32_t* __restrict__ slab_pos,
@@ -381,6 +427,7 @@ __global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __
                             const int64_t* __restrict__ seg_begin, const int32_t* __restrict__ seg_row,
                             const int32_t* __restrict__ seg_cnt, const int32_t* __restrict__ col,
                             const float* __restrict__ val, int nch, int R, int C,
+                            const unsigned char* __restrict__ lane_of,
                             uint16_t* __restrict__ rows, uint16_t* __restrict__ cols,
                             float* __restrict__ vals) {
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -389,7 +436,7 @@ __global__ void k_tile_fill(const uint64_t* __restrict__ key, const uint32_t* __
   const int64_t rel = q - tfirst[t];
   // slab_pos: the slab's place in the tile's stored order (whole-slab split)
   const int64_t slab = slab_begin[t] + (slab_pos ? slab_pos[slab_begin[t] + rel / 32] : rel / 32);
-  const int lane = (int)(rel & 31);
+  const int lane = lane_of ? (int)lane_of[q] : (int)(rel & 31);
   const uint32_t s = sidx[q];
   const int32_t r = seg_row[s];
   const int rb = (int)(t / nch), ch = (int)(t % nch);
@@ -1023,9 +1070,15 @@ static int build_tiled_csr(fitsne_ctx* ctx, TiledP* T, const int64_t* rowptr, co
   FITSNE_CUDA(cudaMemsetAsync(T->rows.ptr, 0xFF, sizeof(uint16_t) * (size_t)nslabs * 32, st));
   FITSNE_CUDA(cudaMemsetAsync(T->cols.ptr, 0, sizeof(uint16_t) * (size_t)(nslots + kTiledPad), st));
   FITSNE_CUDA(cudaMemsetAsync(T->vals.ptr, 0, sizeof(float) * (size_t)(nslots + kTiledPad), st));
+  unsigned char* lane_of = nullptr;
+  if (kBankRows && kLaneDeal) {
+    FITSNE_TRY(tmp.alloc(&lane_of, (size_t)nseg));
+    k_slab_lanes<<<(unsigned)ntd, 128, 0, st>>>(key2, tfirst, tcount, nslab, ntd, bank_mask + 1, lane_of);
+    FITSNE_CHECK_LAUNCH();
+  }
   k_tile_fill<<<nb(nseg, 256), 256, 0, st>>>(key2, idx2, nseg, tfirst, slab_begin, slab_pos, slab_off, seg_begin,
                                              seg_row, seg_cnt, col, val,
-                                             (int)nch, R, C, (uint16_t*)T->rows.ptr,
+                                             (int)nch, R, C, lane_of, (uint16_t*)T->rows.ptr,
                                              (uint16_t*)T->cols.ptr, (float*)T->vals.ptr);
   FITSNE_CHECK_LAUNCH();
   if (ctx->tiled_bank_order) {
@@ -1697,10 +1750,13 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       const int64_t bb = (g0 + lo) >> 2;
       const uint2* cp = reinterpret_cast<const uint2*>(cols) + bb * 32 + lane;
       const float4* vp = reinterpret_cast<const float4*>(vals) + bb * 32 + lane;
+      // (loading the first batch of the warp's run in the NEXT tile before the
+      // current run's tail -- waiting for that tile's stage or only testing it
+      // -- measured 7% slower: SpMV 0.452 vs 0.420 ms on 120 CTAs at C3)
       uint2 cv = __ldcs(cp);
       float4 pv = __ldcs(vp);
       int g = (int)((bb << 2) - g0);  // tile-relative group of the batch's first slot (may precede lo)
-      auto full = [&](const uint2 c, const float4 p, const int gb) {
+      auto batch4 = [&](const uint2 c, const float4 p, const int gb) {
         step(gb, c.x & 0xFFFFu, p.x);
         step(gb + 1, c.x >> 16, p.y);
         step(gb + 2, c.y & 0xFFFFu, p.z);
@@ -1735,10 +1791,10 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       for (; nfull >= 2; nfull -= 2) {
         const uint2 c1 = __ldcs(cp + 32);
         const float4 p1 = __ldcs(vp + 32);
-        full(cv, pv, g);
+        batch4(cv, pv, g);
         cv = __ldcs(cp + 64);
         pv = __ldcs(vp + 64);
-        full(c1, p1, g + 4);
+        batch4(c1, p1, g + 4);
         cp += 64;
         vp += 64;
         g += 8;
@@ -1746,7 +1802,7 @@ k_attract_tiled(const TileLoad* __restrict__ tiles, const int32_t* __restrict__ 
       if (nfull == 1) {
         const uint2 cn = __ldcs(cp + 32);
         const float4 pn = __ldcs(vp + 32);
-        full(cv, pv, g);
+        batch4(cv, pv, g);
         cv = cn;
         pv = pn;
         g += 4;
