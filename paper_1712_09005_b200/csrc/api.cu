@@ -102,6 +102,10 @@ int fitsne_create(fitsne_ctx** out, int device, int dims, int dtype, int points_
   if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device) == cudaSuccess) c->num_sms = sms;
   cudaError_t e = cudaMallocHost(&c->h_grid, sizeof(fitsne_grid));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_scal, 64 * sizeof(double));
+  // pinned pages are recycled between contexts and come back dirty: the
+  // bounding-box sequence word polled in h_scal[15] must not hold an old
+  // context's value
+  if (e == cudaSuccess) std::memset(c->h_scal, 0, 64 * sizeof(double));
   if (e == cudaSuccess) e = cudaMallocHost(&c->h_status, 16 * sizeof(int32_t));
   if (e != cudaSuccess) {
     set_error(std::string("pinned allocation failed: ") + cudaGetErrorString(e));

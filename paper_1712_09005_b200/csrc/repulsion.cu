@@ -256,7 +256,10 @@ int bbox_launch(fitsne_ctx* ctx, const void* Y, int64_t n, cudaStream_t st) {
   // the kernel's last block writes the box and then a sequence number straight
   // into the pinned h_scal[8 .. 15] (bbox_wait polls it); the event is the
   // fallback and the error path
-  ++ctx->bbox_seq;
+  // sequence numbers are unique across the process's contexts (a recycled
+  // pinned page or a second context can never show this launch's number)
+  static std::atomic<unsigned long long> next_seq{1};
+  ctx->bbox_seq = next_seq.fetch_add(1, std::memory_order_relaxed);
   FITSNE_TRY(bbox_kernels(ctx, Y, n, nullptr, 0, st, &outd, nullptr, DevGridReq{}, ctx->h_scal + 8, ctx->bbox_seq));
   if (!ctx->ev_bbox) FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_bbox, cudaEventDisableTiming));
   FITSNE_CUDA(cudaEventRecord(ctx->ev_bbox, st));
