@@ -741,17 +741,25 @@ def full_run(P, dt, dev, n_iter=1000, reorder=True, dims=2):
         exaggeration=optimizer.ExaggerationSchedule(12.0, 250, *late), seed=0, pca_dims=None,
         repulsion_method="fft", dtype="float32" if dt == torch.float32 else "float64", device=dev,
         reorder_iters=(100, 250, 500, 750) if reorder else None)
-    torch.cuda.synchronize()
-    t0 = time.perf_counter()
-    res = optimizer.run_tsne(affinities=P, config=cfg)
-    torch.cuda.synchronize()
-    sec = time.perf_counter() - t0
+    # two runs: the first one also builds the tiled copy of P in run_tsne's
+    # (per-thread, cached) context, a one-time cost per P
+    secs = []
+    for _ in range(2):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        res = optimizer.run_tsne(affinities=P, config=cfg)
+        torch.cuda.synchronize()
+        secs.append(time.perf_counter() - t0)
+    sec = secs[1]
     span = np.ptp(res.embedding, axis=0)
     return {"iterations": n_iter, "seconds": sec, "grad_evals_per_s": n_iter / sec,
+            "first_run_seconds": secs[0],
             "kl_first": float(res.kl_log[0]), "kl_final": float(res.kl_log[-1]),
             "final_span": [float(s) for s in span],
             "reorder": bool(reorder),
-            "note": "wall clock of run_tsne incl. one bbox readback per iteration"}
+            "note": "wall clock of run_tsne (upload of Y0, 1000 fused iterations with one bbox readback each, "
+                    "download of the embedding and the KL log); first_run_seconds includes the one-time tiled "
+                    "layout build for this P"}
 
 
 def cufft_reference(n, L, dt, steps, stream, dims=2):

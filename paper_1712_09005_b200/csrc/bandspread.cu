@@ -37,6 +37,10 @@ static constexpr int kBandBlock = FITSNE_BAND_BLOCK;
 static constexpr int kBandPts = 4096;                 // points per count / scatter block
 static constexpr int kBandChunk = 2048;               // sorted points per reduce block
 static constexpr int kBandRun = kBandChunk / kBandBlock;  // sorted points per reduce thread
+#ifndef FITSNE_BAND_CROWD
+#define FITSNE_BAND_CROWD 4
+#endif
+static constexpr int kBandCrowd = FITSNE_BAND_CROWD;  // distinct boxes per warp up to which the warp reduces before flushing
 static constexpr int kBandKeys = FITSNE_BAND_KEYS;    // (box rows in a chunk) x n_int; 2048 keeps 4 blocks / SM
 static constexpr int kBandMaxRows = 1024;             // n_int bound (fp32: n_int <= 864)
 static constexpr int kBandSmem = kBandChunk * 16 + kBandKeys * 4 + kBandChunk * 4;
@@ -306,6 +310,10 @@ k_band_reduce(const float2* __restrict__ ys, const uint32_t* __restrict__ sidx, 
   // runs of kBandRun sorted points per thread: register sums per box
   const int s0 = tid * kBandRun, s1 = min(cnt, s0 + kBandRun);
   float s[3][3][3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a)
+#pragma unroll
+    for (int b = 0; b < 3; ++b) s[a][b][0] = s[a][b][1] = s[a][b][2] = 0.f;
   int cur = -1, ccx = 0, ccy = 0;
   for (int q = s0; q < s1; ++q) {
     const int k = order[q];
@@ -336,7 +344,36 @@ k_band_reduce(const float2* __restrict__ ys, const uint32_t* __restrict__ sidx, 
         s[a][b][2] += w * (y.y - g.cf[1]);
       }
   }
-  if (cur >= 0) band_flush(acc, nn, ccx, ccy, s);
+  // Crowded boxes (a collapsed embedding early in a run: hundreds of points
+  // per box): the lanes' runs are consecutive in box order, so a warp whose
+  // 32 runs end in at most kBandCrowd distinct boxes adds the partials of a
+  // box up with a segmented shuffle reduction and flushes once per box
+  // instead of once per lane -- the per-lane flushes then serialise in the
+  // L2 atomic units on a few thousand addresses (C3, span 1e-4: 570 us alone
+  // on the GPU, and the SpMV beside it slows down by 1.8x).
+  const unsigned all = 0xffffffffu;
+  const int prev = __shfl_up_sync(all, cur, 1);
+  const bool head = cur >= 0 && (lane == 0 || prev != cur);
+  const unsigned heads = __ballot_sync(all, head);
+  if (__popc(heads) <= kBandCrowd) {
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int ko = __shfl_down_sync(all, cur, o);
+      const bool take = lane + o < 32 && ko == cur;
+#pragma unroll
+      for (int a = 0; a < 3; ++a)
+#pragma unroll
+        for (int b = 0; b < 3; ++b)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            const float v = __shfl_down_sync(all, s[a][b][c], o);
+            if (take) s[a][b][c] += v;
+          }
+    }
+    if (head) band_flush(acc, nn, ccx, ccy, s);
+  } else if (cur >= 0) {
+    band_flush(acc, nn, ccx, ccy, s);
+  }
 }
 
 // F_rep of every point from the potentials (gather_potentials, nbody.py:344-350;
