@@ -56,7 +56,11 @@ def main():
 
     def step():
         nonlocal ya, yb, it
-        rc = ctx.lib.fitsne_iterate(ctx.h, _lib.ptr(ya), _lib.ptr(yb), _lib.ptr(vel), _lib.ptr(gains), 12.0, 0.5,
+        alpha, mom = 12.0, 0.5
+        if "--schedule" in sys.argv:   # the bench's full run: 12 until 250, 1 until 750, then 4; momentum 0.8 from 250
+            alpha = 12.0 if it < 250 else (4.0 if it >= 750 else 1.0)
+            mom = 0.5 if it < 250 else 0.8
+        rc = ctx.lib.fitsne_iterate(ctx.h, _lib.ptr(ya), _lib.ptr(yb), _lib.ptr(vel), _lib.ptr(gains), alpha, mom,
                                     lr, C.c_void_p(kl.data_ptr() + 8 * it), C.c_void_p(status.data_ptr() + 4 * it),
                                     ctx.stream)
         _lib.check(rc, "iterate")
