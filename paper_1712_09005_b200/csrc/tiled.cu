@@ -776,6 +776,45 @@ static int count_segments(const int64_t* rowptr, const int32_t* col, int64_t n_r
   return FITSNE_OK;
 }
 
+// (row, chunk) segments of the registered CSR in the caller's order (rows may
+// list their columns unsorted: counted on a sorted copy then)
+static int natural_segments(fitsne_ctx* ctx, TmpBufs& tmp, int64_t* out, cudaStream_t st) {
+  const int64_t n = ctx->n_total, nnz = ctx->nnz;
+  const int32_t* c0 = ctx->col;
+  int32_t* flag;
+  FITSNE_TRY(tmp.alloc(&flag, 1));
+  FITSNE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
+  k_rows_unsorted<<<nb(n * 32, 256), 256, 0, st>>>(ctx->rowptr, c0, n, flag);
+  int32_t hf = 0;
+  FITSNE_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  FITSNE_CUDA(cudaStreamSynchronize(st));
+  if (hf) {
+    int32_t* oc;
+    float* ov;
+    FITSNE_TRY(tmp.alloc(&oc, nnz));
+    FITSNE_TRY(tmp.alloc(&ov, nnz));
+    size_t bytes = 0;
+    FITSNE_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, ctx->col, oc, (const float*)ctx->val, ov,
+                                                    nnz, n, ctx->rowptr, ctx->rowptr + 1, st));
+    unsigned char* tb;
+    FITSNE_TRY(tmp.alloc(&tb, bytes));
+    FITSNE_CUDA(cub::DeviceSegmentedSort::SortPairs(tb, bytes, ctx->col, oc, (const float*)ctx->val, ov,
+                                                    nnz, n, ctx->rowptr, ctx->rowptr + 1, st));
+    c0 = oc;
+  }
+  return count_segments(ctx->rowptr, c0, n, tile_cols_eff(ctx), tmp, out, st);
+}
+
+// Auto relabelling skips the search for an ordering on a large matrix (many
+// column chunks) whose caller order already gives this many entries per (row,
+// chunk) segment: the Cuthill-McKee orderings of the large kNN graphs
+// measured reach ~7, so an input at 4 or more cannot have its segments halved
+// (the bar for using the ordering), and the search costs ~0.9 s at C3, 10x
+// the layout build itself.  Small matrices (few chunks: an ordering can bring
+// a row's neighbours into one or two of them) always search; it is cheap there.
+static constexpr double kRelabelSkipDensity = 4.0;
+static constexpr int64_t kRelabelSkipChunks = 64;
+
 static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
   FITSNE_RANGE("tiled_build");
   // relabel (FITSNE_OPT_RELABEL) only a whole matrix: the sharded layout's
@@ -784,6 +823,15 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
   if (ctx->relabel == 0 || !whole || ctx->n_total > 0x7fffffffLL)
     return build_tiled_csr(ctx, T, ctx->rowptr, ctx->col, (const float*)ctx->val, st);
   const int64_t n = ctx->n_total, nnz = ctx->nnz;
+  int64_t seg_natural = -1;
+  if (ctx->relabel == 1) {
+    TmpBufs tmp0(st);
+    FITSNE_TRY(natural_segments(ctx, tmp0, &seg_natural, st));
+    T->nseg_natural = seg_natural;
+    const int64_t nch = (ctx->n_total + tile_cols_eff(ctx) - 1) / tile_cols_eff(ctx);
+    if (nch >= kRelabelSkipChunks && (double)nnz >= kRelabelSkipDensity * (double)seg_natural)
+      return build_tiled_csr(ctx, T, ctx->rowptr, ctx->col, (const float*)ctx->val, st);
+  }
   TmpBufs tmp(st);
   FITSNE_TRY(alloc_exact(T->order, sizeof(int) * (size_t)n));
   int* order = (int*)T->order.ptr;
@@ -825,32 +873,7 @@ static int build_tiled(fitsne_ctx* ctx, TiledP* T, cudaStream_t st) {
     // segments, no tiled layout at all) gets the tiled SpMV back.
     int64_t seg_new = 0, seg_old = 0;
     FITSNE_TRY(count_segments(nrowptr, scol, n, tile_cols_eff(ctx), tmp, &seg_new, st));
-    const int32_t* c0 = ctx->col;
-    {
-      // the caller's rows may be unsorted: count on a sorted copy
-      int32_t* flag;
-      FITSNE_TRY(tmp.alloc(&flag, 1));
-      FITSNE_CUDA(cudaMemsetAsync(flag, 0, sizeof(int32_t), st));
-      k_rows_unsorted<<<nb(n * 32, 256), 256, 0, st>>>(ctx->rowptr, c0, n, flag);
-      int32_t hf = 0;
-      FITSNE_CUDA(cudaMemcpyAsync(&hf, flag, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
-      FITSNE_CUDA(cudaStreamSynchronize(st));
-      if (hf) {
-        int32_t* oc;
-        float* ov;
-        FITSNE_TRY(tmp.alloc(&oc, nnz));
-        FITSNE_TRY(tmp.alloc(&ov, nnz));
-        size_t bytes = 0;
-        FITSNE_CUDA(cub::DeviceSegmentedSort::SortPairs(nullptr, bytes, ctx->col, oc, (const float*)ctx->val, ov,
-                                                        nnz, n, ctx->rowptr, ctx->rowptr + 1, st));
-        unsigned char* tb;
-        FITSNE_TRY(tmp.alloc(&tb, bytes));
-        FITSNE_CUDA(cub::DeviceSegmentedSort::SortPairs(tb, bytes, ctx->col, oc, (const float*)ctx->val, ov,
-                                                        nnz, n, ctx->rowptr, ctx->rowptr + 1, st));
-        c0 = oc;
-      }
-    }
-    FITSNE_TRY(count_segments(ctx->rowptr, c0, n, tile_cols_eff(ctx), tmp, &seg_old, st));
+    seg_old = seg_natural;  // counted above (auto mode)
     T->nseg_natural = seg_old;
     use = (double)seg_new <= 0.5 * (double)seg_old;
   }
