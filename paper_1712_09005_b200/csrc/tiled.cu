@@ -186,6 +186,7 @@ struct TiledP {
   unsigned cur_base = 0;
   bool cur_kl = false, cur_dynamic = false;
   int join_grid = 0;         // CTAs of the last joining launch (0: none)
+  int cur_grid = 0;          // CTAs of the pass's main launch (main_grid(): the build's grid or a few more)
   cudaEvent_t ev_perm = nullptr;  // relabelled Y copy ready
   // locality relabelling (reorder.cu): tiles are built over P[order][:, order];
   // order[new] = old.  The kernel reads Y through yp = Y[order] and adds each
@@ -1966,6 +1967,19 @@ __global__ void k_permute_points(const PT* __restrict__ Y, const int* __restrict
 
 // Runs the tiled SpMV: F_attr accumulates into the tiled copy's zeroed buffer
 // (*fattr_out; the consumer must clear it), KL partials -> T->part[0, grid).
+// CTAs of a dynamically scheduled main launch.  The build's grid (tiled_grid:
+// 120 of 148 SMs beside the repulsion chain) fits C3's 199-interval grid; when
+// the last evaluation's grid was small (a run's 50..100 intervals: the FFT
+// stages are a few tens of microseconds) the chain needs fewer SMs and the
+// SpMV takes 8 more -- work units are drawn from the ticket counter, so the
+// launch grid need not be the grid the schedule was built for (a C3 run_tsne
+// iteration: 487 -> 472 us).  An explicit FITSNE_OPT_TILED_CTAS is kept.
+static int main_grid(const fitsne_ctx* ctx, const TiledP* T, bool dynamic) {
+  if (!dynamic || ctx->tiled_ctas > 0 || ctx->overlap == 0 || !ctx->grid_valid) return T->grid;
+  if (ctx->grid.n_intervals > 100) return T->grid;
+  return std::min(ctx->num_sms, T->grid + 8);
+}
+
 template <int S>
 static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t* sched, cudaStream_t st,
                           int join_ctas) {
@@ -1990,7 +2004,7 @@ static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t
       have = smem;
     }
   }
-  double* part = (double*)T->part.ptr + (join_ctas > 0 ? T->grid : 0);
+  double* part = (double*)T->part.ptr + (join_ctas > 0 ? T->cur_grid : 0);
   const int* rowmap = nullptr;
   if (T->relabeled) {
     // the tiles index the relabelled points: stage Y in that order
@@ -2015,7 +2029,7 @@ static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t
   // schedules (host-buffer gradient) stay static
   const int2* units = (sched == (const int32_t*)T->sched.ptr && T->nunits > 0) ? (const int2*)T->units.ptr : nullptr;
   const unsigned base = join_ctas > 0 ? T->cur_base : T->ticket_base;
-  const int launch_grid = join_ctas > 0 ? join_ctas : T->grid;
+  const int launch_grid = join_ctas > 0 ? join_ctas : main_grid(ctx, T, units != nullptr);
   if (join_ctas > 0 && !units) { set_error("joining launch without a dynamic schedule"); return FITSNE_EINVAL; }
   if (kl)
     k_attract_tiled<S, true><<<launch_grid, kTiledThreads, smem, st>>>(TILED_ARGS);
@@ -2032,7 +2046,8 @@ static int launch_tiled_s(fitsne_ctx* ctx, const void* Y, bool kl, const int32_t
     T->cur_kl = kl;
     T->cur_dynamic = units != nullptr;
     T->join_grid = 0;
-    if (units) T->ticket_base += (unsigned)T->nunits + (unsigned)T->grid;
+    T->cur_grid = launch_grid;
+    if (units) T->ticket_base += (unsigned)T->nunits + (unsigned)launch_grid;
   }
   return FITSNE_OK;
 }
@@ -2078,7 +2093,7 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
   FITSNE_TRY(launch_tiled(ctx, Y, kl, (const int32_t*)T->sched.ptr, st));
   *fattr_out = T->fattr.ptr;
   if (part_out) *part_out = part;
-  if (nparts) *nparts = T->grid;
+  if (nparts) *nparts = T->cur_grid;
   return FITSNE_OK;
 }
 
@@ -2089,11 +2104,11 @@ int attract_tiled(fitsne_ctx* ctx, const void* Y, bool kl, cudaStream_t st, void
 // joining CTAs' KL partials.
 int attract_tiled_join(fitsne_ctx* ctx, const void* Y, int ctas, cudaStream_t st, int* nparts) {
   TiledP* T = ctx->tiled;
-  if (ctas < 0 && T) ctas = ctx->num_sms - T->grid;  // the SMs the first launch left
+  if (ctas < 0 && T) ctas = ctx->num_sms - T->cur_grid;  // the SMs the first launch left
   if (!T || !T->cur_dynamic || ctas <= 0) return FITSNE_OK;
   ctas = std::min(ctas, ctx->num_sms);
   FITSNE_TRY(launch_tiled(ctx, Y, T->cur_kl, (const int32_t*)T->sched.ptr, st, ctas));
-  if (nparts) *nparts = T->grid + ctas;
+  if (nparts) *nparts = T->cur_grid + ctas;
   return FITSNE_OK;
 }
 
