@@ -197,8 +197,11 @@ def n_points(P) -> int:
 
 
 def ordered_total(P) -> float:
-    if hasattr(P, "ordered_total"):
-        return float(P.ordered_total)
+    # one evaluation: ordered_total is a property that sums every stored value
+    # (hasattr would evaluate it a first time -- 63 ms at C3)
+    t = getattr(P, "ordered_total", None)
+    if t is not None:
+        return float(t() if callable(t) else t)
     return float(P.sum())
 
 
