@@ -106,6 +106,8 @@ def parse():
     ap.add_argument("--tile", default=None, help="ROWSxCOLS tile shape of the tiled SpMV (A/B)")
     ap.add_argument("--side-gather", type=int, default=1, choices=[0, 1],
                     help="gather F_rep on the repulsion stream beside the SpMV (A/B)")
+    ap.add_argument("--spec-ahead", type=int, default=0, choices=[0, 1],
+                    help="FITSNE_OPT_SPEC_AHEAD: kernel spectrum on its own stream beside the spread (A/B)")
     ap.add_argument("--spmv-join", type=int, default=1, choices=[0, 1],
                     help="second SpMV launch behind the repulsion chain joins the dynamic schedule (A/B)")
     ap.add_argument("--tiled-ctas", type=int, default=0,
@@ -542,6 +544,7 @@ def run_ours(args):
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_DEVICE_GRID, args.device_grid), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SIDE_GATHER, args.side_gather), "set_option")
     _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SPMV_JOIN, args.spmv_join), "set_option")
+    _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SPEC_AHEAD, args.spec_ahead), "set_option")
     if args.tile:
         tr, tc = (int(v) for v in args.tile.lower().split("x"))
         _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_TILE_ROWS, tr), "set_option")

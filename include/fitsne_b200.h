@@ -106,7 +106,8 @@ enum fitsne_option {
   FITSNE_OPT_RELABEL = 14,
   FITSNE_OPT_DEVICE_GRID = 15,
   FITSNE_OPT_SIDE_GATHER = 16,
-  FITSNE_OPT_SPMV_JOIN = 17
+  FITSNE_OPT_SPMV_JOIN = 17,
+  FITSNE_OPT_SPEC_AHEAD = 18
 };
 /*   FITSNE_OPT_TILED_SPMV: 0 = row-per-warp CSR SpMV; 1 (default) = for fp32
  *   2-D embeddings with >= 2^22 stored entries, a copy of P in row-block x
@@ -150,6 +151,12 @@ enum fitsne_option {
  *   FITSNE_OPT_SPMV_JOIN: 1 (default) = when the repulsion chain beside the
  *   tiled SpMV is done, a second SpMV launch on its stream joins the dynamic
  *   work-unit schedule with the SMs the chain used; 0 = one launch only.
+ *   FITSNE_OPT_SPEC_AHEAD: 1 = in the overlapped schedule the kernel spectrum
+ *   (it depends on the grid only: nbody.py:264-283) is computed on a stream of
+ *   its own while the charges are still being spread, instead of in the FFT
+ *   stage behind the spread; 0 (default) = inside the FFT stage.  Measured at
+ *   C3: the spectrum kernels and the spread share the same ~28 SMs, the chain
+ *   ends 5 us earlier and the step is 0.6% slower, so it is off.
  *   FITSNE_OPT_DEVICE_GRID: 1 = fitsne_gradient / _host / _iterate compute
  *   the grid on the device and queue the spread and FFT stages without
  *   waiting for the bbox readback (the host checks the grid after queueing

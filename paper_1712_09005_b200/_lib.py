@@ -25,7 +25,7 @@ OK, EINVAL, ENONFINITE, EZ, ECUDA, ENOMEM, EOUTSIDE, ETOOBIG, EPOINTS, ENCCL = r
 (OPT_SORTED_SPREAD, OPT_OVERLAP, OPT_SPMV_BLOCKS_PER_SM, OPT_SPREAD_REPLICAS, OPT_TILED_SPMV,
  OPT_TILE_ROWS, OPT_TILE_COLS, OPT_TILED_CTAS, OPT_TILED_BANK_ORDER, OPT_HOST_PIECES, OPT_FFT_COLS,
  OPT_FFT_PATH, OPT_GRID_F64, OPT_RELABEL, OPT_DEVICE_GRID, OPT_SIDE_GATHER,
- OPT_SPMV_JOIN) = range(1, 18)
+ OPT_SPMV_JOIN, OPT_SPEC_AHEAD) = range(1, 19)
 F32, F64 = 0, 1
 CAUCHY, CAUCHY_SQUARED = 0, 1
 
@@ -237,7 +237,7 @@ class option:
     to `restore` (the library default unless given) on exit."""
 
     _DEFAULTS = {OPT_FFT_PATH: 0, OPT_GRID_F64: 1, OPT_TILED_SPMV: 1, OPT_SORTED_SPREAD: 1, OPT_RELABEL: 1,
-                 OPT_DEVICE_GRID: 0, OPT_SIDE_GATHER: 1, OPT_SPMV_JOIN: 1,
+                 OPT_DEVICE_GRID: 0, OPT_SIDE_GATHER: 1, OPT_SPMV_JOIN: 1, OPT_SPEC_AHEAD: 0,
                  OPT_OVERLAP: 1, OPT_HOST_PIECES: 0}
 
     def __init__(self, opt: int, value: int, restore: int | None = None):

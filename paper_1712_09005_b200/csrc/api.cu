@@ -136,6 +136,9 @@ int fitsne_destroy(fitsne_ctx* c) {
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->ev_bbox) cudaEventDestroy(c->ev_bbox);
   if (c->side) cudaStreamDestroy(c->side);
+  if (c->spec) cudaStreamDestroy(c->spec);
+  if (c->ev_spec_in) cudaEventDestroy(c->ev_spec_in);
+  if (c->ev_spec) cudaEventDestroy(c->ev_spec);
   for (cudaEvent_t e : c->ev_piece)
     if (e) cudaEventDestroy(e);
   if (c->ev_out) cudaEventDestroy(c->ev_out);
@@ -250,6 +253,11 @@ int fitsne_set_option(fitsne_ctx* ctx, int option, int value) {
   if (option == FITSNE_OPT_SPMV_JOIN) {
     if (value < 0 || value > 1) { set_error("spmv join must be 0 or 1"); return FITSNE_EINVAL; }
     ctx->spmv_join = value;
+    return FITSNE_OK;
+  }
+  if (option == FITSNE_OPT_SPEC_AHEAD) {
+    if (value < 0 || value > 1) { set_error("spectrum ahead must be 0 or 1"); return FITSNE_EINVAL; }
+    ctx->spec_opt = value;
     return FITSNE_OK;
   }
   if (option == FITSNE_OPT_SIDE_GATHER) {

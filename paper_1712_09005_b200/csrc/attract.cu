@@ -795,6 +795,7 @@ static int repulsion_beside_spmv(fitsne_ctx* ctx, const void* Y, int64_t n, cuda
     FITSNE_TRY(bbox_launch(ctx, Y, n, ctx->side));
     if (ctx->overlap != 4) FITSNE_TRY(spmv());
     FITSNE_TRY(make_grid_finish(ctx, ctx->side));
+    FITSNE_TRY(spectrum_ahead(ctx, ctx->side));  // kernel spectrum beside the spread
     FITSNE_TRY(spread_tsne(ctx, Y, n, nullptr, ctx->side));
     FITSNE_TRY(fft_tsne(ctx, nullptr, n, false, ctx->side));
     if (ctx->side_gather && ctx->band_sorted && ctx->band_n == n && !ctx->wide && ctx->dtype == FITSNE_F32) {

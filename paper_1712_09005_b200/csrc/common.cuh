@@ -270,6 +270,13 @@ struct fitsne_ctx {
   int kl_nparts = 0;
   cudaStream_t side = nullptr;     // repulsion stream (overlaps the attractive SpMV)
   cudaEvent_t ev_in = nullptr, ev_done = nullptr;
+  // kernel spectrum computed ahead of the charges (spectrum_ahead): its own
+  // stream, fork / join events, and the grid it was computed for
+  cudaStream_t spec = nullptr;
+  cudaEvent_t ev_spec_in = nullptr, ev_spec = nullptr;
+  bool spec_ahead = false;
+  int spec_ahead_L = 0, spec_ahead_n = 0;
+  int spec_opt = 0;  // FITSNE_OPT_SPEC_AHEAD (measured: no gain, off)
   cudaEvent_t ev_bbox = nullptr;   // bbox readback landed (bbox_launch / bbox_wait)
   // host-buffer gradient (fitsne_gradient_host): copy-out stream, one event
   // per SpMV row piece, device copies of Y and the gradient

@@ -38,6 +38,9 @@ int spread_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStre
 int spread_sorted(fitsne_ctx* ctx, const void* Y, int64_t n, void* accum, cudaStream_t st);
 // FFT stage: accum -> ctx->pot, Z -> ctx->scal[0] (needs n_total for Z)
 int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st);
+// start the kernel spectrum of the current grid on the context's spectrum
+// stream (after `from`); the next fft_tsne on this grid joins it
+int spectrum_ahead(fitsne_ctx* ctx, cudaStream_t from);
 // gather: pot -> forces (n, s) [+ k1 (n,), k2 (n, s+1)]
 int gather_tsne(fitsne_ctx* ctx, const void* Y, int64_t n, void* forces, void* k1, void* k2,
                 cudaStream_t st);

@@ -439,6 +439,7 @@ int shadow_frep(fitsne_ctx* ctx, const void* Y, int64_t n, double** frep, cudaSt
 
 int install_grid(fitsne_ctx* ctx, const fitsne_grid& g, cudaStream_t st) {
   FITSNE_RANGE("install_grid");
+  ctx->spec_ahead = false;  // a spectrum computed ahead belongs to the previous grid
   if (g.dims != ctx->dims) {
     set_error("grid dims do not match the context");
     return FITSNE_EINVAL;
@@ -819,7 +820,8 @@ __device__ __forceinline__ void kernel_pair(int i, int j, double hx, double hy, 
 
 // Row stage.  merged=1: block x transforms data row x (the packed pairs) and
 // kernel-spectrum row x in one batched FFT.  merged=0 (large L): blocks [0, n)
-// do the data rows, blocks [n, 2n) the spectrum rows.  Shared memory: the
+// do the data rows, blocks [n, 2n) the spectrum rows.  merged=2 / 3: one
+// launch for the data rows, another (spectrum_ahead) for the spectrum rows.  Shared memory: the
 // twiddle table (L) then the padded signals (stride plen(L), index pidx).
 template <typename T, int MODE>
 __global__ void __launch_bounds__(256)
@@ -836,9 +838,11 @@ k_rows_forward(T* __restrict__ acc, const T* __restrict__ coeffs, int ncol, int 
   const int H = L / 2 + 1;
   // unmerged launches put the data rows first: [0, split) data, [split, 2 split) spectrum
   const int split = gd ? (int)gridDim.x / 2 : n;
-  const bool do_data = merged || (int)blockIdx.x < split;
-  const bool do_spec = merged || (int)blockIdx.x >= split;
-  const int x = (merged || (int)blockIdx.x < split) ? (int)blockIdx.x : (int)blockIdx.x - split;
+  // merged: 1 = data + spectrum row in one block, 0 = data blocks then spectrum
+  // blocks, 2 = data rows only, 3 = spectrum rows only (spectrum_ahead)
+  const bool do_data = merged == 1 || merged == 2 || (merged == 0 && (int)blockIdx.x < split);
+  const bool do_spec = merged == 1 || merged == 3 || (merged == 0 && (int)blockIdx.x >= split);
+  const int x = (merged != 0 || (int)blockIdx.x < split) ? (int)blockIdx.x : (int)blockIdx.x - split;
   if (x >= n) return;  // capacity beyond the device grid
   const FftPlan& pl = *plp;
   V* s_tw = reinterpret_cast<V*>(smem_raw);
@@ -1332,14 +1336,19 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
     const int npair = std::min(maxpair, npair_total - pair0);
     // the spectrum rows are recomputed per pair group (one group for t-SNE)
     const int nd = (MODE == MODE_TSNE) ? 2 : npair;
-    const int merged = sizeof(V) * ((size_t)L + 2 * (size_t)(nd + 1) * plen(L)) <= 113 * 1024 ? 1 : 0;
-    size_t smem_r = sizeof(V) * ((size_t)L + 2 * (size_t)(merged ? nd + 1 : std::max(nd, 1)) * plen(L));
+    // the kernel spectrum of this grid may already be on its way (spectrum_ahead)
+    const bool ahead = MODE == MODE_TSNE && ctx->spec_ahead && ctx->spec_ahead_L == L && ctx->spec_ahead_n == n;
+    ctx->spec_ahead = false;
+    const int merged = ahead ? 2 : (sizeof(V) * ((size_t)L + 2 * (size_t)(nd + 1) * plen(L)) <= 113 * 1024 ? 1 : 0);
+    size_t smem_r = sizeof(V) * ((size_t)L + 2 * (size_t)(merged == 1 ? nd + 1 : std::max(nd, 1)) * plen(L));
     FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE>, smem_r));
-    k_rows_forward<T, MODE><<<merged ? n : 2 * n, 256, smem_r, st>>>(
+    k_rows_forward<T, MODE><<<merged == 0 ? 2 * n : n, 256, smem_r, st>>>(
         accum, coeffs, ncol, pair0, npair, F, Sb, g, tw, pl, merged, accum_reps_live(ctx, accum),
         (int64_t)accum_elems(gr));
     FITSNE_CHECK_LAUNCH();
-    if (pair0 == 0) {
+    if (ahead) {
+      FITSNE_CUDA(cudaStreamWaitEvent(st, ctx->ev_spec, 0));  // Khat ready
+    } else if (pair0 == 0) {
       // columns per block: as many as fit in shared memory (long transforms
       // take fewer)
       int cpb = kSpecCols;
@@ -1368,6 +1377,60 @@ static int run_conv(fitsne_ctx* ctx, T* accum, const T* coeffs, int ncol, int ke
     FITSNE_CHECK_LAUNCH();
   }
   return FITSNE_OK;
+}
+
+// The kernel spectrum depends on the grid only.  In the overlapped schedule it
+// is computed on a stream of its own as soon as the grid exists (`from`: the
+// stream the grid and its twiddle table were made on), while the spread --
+// latency-bound on the few SMs the SpMV leaves -- is still running; the FFT
+// stage then transforms the data rows only and joins ev_spec before the
+// column stage.  2-D one-block FFT path of this context only (not the fp64
+// twin, the four-step path or 1-D).
+template <typename T>
+static int spectrum_ahead_t(fitsne_ctx* ctx, cudaStream_t from) {
+  using V = typename C2<T>::type;
+  GridArgs g = grid_args(ctx->grid);
+  const int L = g.L, n = g.n, H = L / 2 + 1;
+  FftPlan pl;
+  make_plan(pl, L);
+  FITSNE_TRY(ensure(ctx->fbuf, sizeof(V) * (size_t)2 * n * L));
+  FITSNE_TRY(ensure(ctx->sbuf, sizeof(V) * ((size_t)n * H + (size_t)H * L)));
+  FITSNE_TRY(ensure(ctx->zpart, sizeof(double) * (size_t)L));
+  const V* tw = (const V*)ctx->tw.ptr;
+  V* Sb = (V*)ctx->sbuf.ptr;
+  V* Kh = Sb + (size_t)n * H;
+  if (!ctx->spec) {
+    int lo = 0, hi = 0;
+    FITSNE_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FITSNE_CUDA(cudaStreamCreateWithPriority(&ctx->spec, cudaStreamNonBlocking, lo));
+    FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_spec_in, cudaEventDisableTiming));
+    FITSNE_CUDA(cudaEventCreateWithFlags(&ctx->ev_spec, cudaEventDisableTiming));
+  }
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_spec_in, from));
+  FITSNE_CUDA(cudaStreamWaitEvent(ctx->spec, ctx->ev_spec_in, 0));
+  const size_t smem_r = sizeof(V) * ((size_t)L + 2 * (size_t)plen(L));
+  FITSNE_TRY(set_smem<T>((const void*)k_rows_forward<T, MODE_TSNE>, smem_r));
+  k_rows_forward<T, MODE_TSNE><<<n, 256, smem_r, ctx->spec>>>(nullptr, nullptr, 3, 0, 2, nullptr, Sb, g, tw, pl, 3,
+                                                             0, 0);
+  FITSNE_CHECK_LAUNCH();
+  int cpb = kSpecCols;
+  auto smem_spec = [&](int c) { return sizeof(V) * ((size_t)L + 2 * (size_t)c * plen(L)); };
+  while (cpb > 1 && smem_spec(cpb) > 227 * 1024) cpb /= 2;
+  FITSNE_TRY(set_smem<T>((const void*)k_spec_cols<T>, smem_spec(cpb)));
+  k_spec_cols<T><<<(H + cpb - 1) / cpb, 256, smem_spec(cpb), ctx->spec>>>(Sb, g, tw, pl, Kh, cpb);
+  FITSNE_CHECK_LAUNCH();
+  FITSNE_CUDA(cudaEventRecord(ctx->ev_spec, ctx->spec));
+  ctx->spec_ahead = true;
+  ctx->spec_ahead_L = L;
+  ctx->spec_ahead_n = n;
+  return FITSNE_OK;
+}
+
+int spectrum_ahead(fitsne_ctx* ctx, cudaStream_t from) {
+  ctx->spec_ahead = false;
+  if (!ctx->spec_opt || !ctx->grid_valid || ctx->wide || ctx->grid.dims != 2) return FITSNE_OK;
+  if (big_fft_applies(ctx, ctx->grid.fft_len)) return FITSNE_OK;
+  return ctx->dtype == FITSNE_F32 ? spectrum_ahead_t<float>(ctx, from) : spectrum_ahead_t<double>(ctx, from);
 }
 
 int fft_tsne(fitsne_ctx* ctx, void* accum, int64_t n_total, bool with_k1, cudaStream_t st) {

@@ -458,3 +458,32 @@ def test_tiled_1d_gradient_and_run(cuda):
     _, kl_o = O.tsne(rr, cc, v, n, dims=1, n_iter=5, lr=200.0, early_coeff=12.0, early_until=5,
                      min_intervals=50, p=3, method="fft", seed=0)
     assert np.max(np.abs(res.kl_log - kl_o) / np.abs(kl_o)) <= 1e-4
+
+
+@pytest.mark.parametrize("dtype", [torch.float32, torch.float64])
+def test_spectrum_ahead_option(cuda, dtype):
+    """FITSNE_OPT_SPEC_AHEAD (kernel spectrum on its own stream beside the
+    spread): the gradient equals the default schedule's and the oracle's,
+    over repeated calls with a changing grid."""
+    from paper_1712_09005_b200 import _lib
+    n = 4001
+    rr, cc, v, Y = _graph(n, 20, seed=3)
+    from paper_1712_09005_b200.affinities import SparseAffinities, device_csr
+    P = SparseAffinities(n=n, rows=rr, cols=cc, values=v)
+    csr = device_csr(P, dtype, 0)
+    tol = 1e-3 if dtype == torch.float32 else 1e-9
+    got = {}
+    for opt in (0, 1):
+        ctx = _lib.Context(0, 2, dtype, 3, 20, 1.0)
+        _lib.check(ctx.lib.fitsne_set_option(ctx.h, _lib.OPT_SPEC_AHEAD, opt), "set_option")
+        ctx.set_affinities(csr)
+        for k, scale in enumerate((1.0, 1.7, 0.6)):   # the grid (and its spectrum) changes between calls
+            yk = torch.from_numpy(Y * scale).to(dtype).cuda()
+            g = torch.empty_like(yk)
+            _lib.check(ctx.lib.fitsne_gradient(ctx.h, _lib.ptr(yk), 2.0, _lib.ptr(g), None, ctx.stream), "gradient")
+            torch.cuda.synchronize()
+            got[(opt, k)] = g.double().cpu().numpy()
+            want = O.grad(rr, cc, v, yk.double().cpu().numpy(), 2.0, min_intervals=20, p=3)
+            assert rel_l2(got[(opt, k)], want) <= tol, (opt, k)
+    for k in range(3):
+        assert rel_l2(got[(1, k)], got[(0, k)]) <= (2e-5 if dtype == torch.float32 else 1e-12), k
