@@ -69,3 +69,24 @@ def test_rejects_bad_files_and_asymmetry(tmp_path):
     np.savez(g, a=np.zeros(3))
     with pytest.raises(ValueError, match="not a"):
         load_affinities(g)
+
+
+def test_ordered_total_is_cached_with_the_contents():
+    """ordered_total sums every stored value once per contents of P: a second
+    call reuses it, an in-place rescaling of the values is seen."""
+    import numpy as np
+    from paper_1712_09005_b200.affinities import SparseAffinities, ordered_total
+    rng = np.random.default_rng(0)
+    n = 500
+    key = np.unique(rng.integers(0, n * n, 4000))
+    r, c = key // n, key % n
+    keep = r < c
+    r, c = r[keep], c[keep]
+    v = rng.random(r.size)
+    v /= 2 * v.sum()
+    P = SparseAffinities(n=n, rows=r, cols=c, values=v)
+    assert abs(ordered_total(P) - 1.0) < 1e-12
+    assert any(k[0] == "ordered_total" for k in P.__dict__["_fitsne_csr"] if isinstance(k, tuple))
+    assert abs(ordered_total(P) - 1.0) < 1e-12          # cached
+    P.values *= 2.0                                     # in-place edit: the sampled checksum changes
+    assert abs(ordered_total(P) - 2.0) < 1e-12
